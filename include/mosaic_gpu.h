@@ -1,0 +1,198 @@
+/* mosaic_gpu.h — C ABI of the B200 (sm_100a) backend for the Mosaic planner hot path.
+ *
+ * The reference (/root/reference/proj, header-only C++20, namespace mosaic) has no
+ * FFI; its replaceable seams are C++ calls.  Each entry point below replaces one of
+ * them and keeps its argument meaning and error behaviour:
+ *
+ *   mosaic_gpu_stage_time    <- stage_time / rectified_latency      perf_model.hpp:442-479
+ *   mosaic_gpu_options       <- candidate_options                   stage_eval.hpp:68-93
+ *   mosaic_gpu_stage_eval    <- stage_eval (tau doubling, bisection,
+ *                               confirmation probes; first leaf of the
+ *                               last successful FeasibilitySearch::run) stage_eval.hpp:302-382
+ *   mosaic_gpu_feasible      <- detail::FeasibilitySearch::run(tau)  stage_eval.hpp:113-164
+ *   mosaic_gpu_exact_stage   <- detail::ExactStageSolver::solve      oracle.hpp:86-103
+ *   mosaic_gpu_solve         <- solve (GAHC)                         solver.hpp:157-289
+ *   mosaic_gpu_brute_force   <- brute_force_optimum                  oracle.hpp:206-255
+ *
+ * Status codes map the reference's nullopt / exceptions:
+ *   0 OK, 1 INFEASIBLE (std::nullopt), 2 MODULE_NO_OPTION (StageInfeasibleError),
+ *   3 RANGE (SurfaceRangeError / invalid_argument), 4 TOO_LARGE (OracleTooLargeError
+ *   or a stage beyond the kernel limits), 5 CUDA (device error), 6 EMPTY (EmptyPlanError).
+ * No exception crosses the ABI; mosaic_gpu_last_error() returns a thread-local message.
+ * Plain pointers and sizes only; outputs are caller-allocated.  One context per host
+ * thread (like the reference, which is re-entrant but not thread-safe per EvalCache).
+ */
+#ifndef MOSAIC_GPU_H
+#define MOSAIC_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    MOSAIC_OK = 0,
+    MOSAIC_INFEASIBLE = 1,
+    MOSAIC_MODULE_NO_OPTION = 2,
+    MOSAIC_RANGE = 3,
+    MOSAIC_TOO_LARGE = 4,
+    MOSAIC_CUDA = 5,
+    MOSAIC_EMPTY = 6,
+};
+
+/* Kernel limits (a stage beyond them returns MOSAIC_TOO_LARGE, never a CPU path). */
+#define MOSAIC_GPU_MAX_STAGE_MODULES 12
+#define MOSAIC_GPU_MAX_GPUS 1024
+#define MOSAIC_GPU_MAX_MODULES 64
+
+/* One profiled surface point (perf_model.hpp:37-44). */
+typedef struct {
+    int32_t d;
+    double a, latency, bandwidth_util, memory, sm_active;
+} mosaic_gpu_point;
+
+/* One module: id (topological tie-break, core.hpp:219), memory_base (core.hpp:34) and
+ * its complete (d, a) surface grid in any order (perf_model.hpp:57-79). */
+typedef struct {
+    const char* id;
+    double memory_base;
+    const mosaic_gpu_point* points;
+    int32_t n_points;
+} mosaic_gpu_module;
+
+/* Everything a PerfContext + ClusterSpec + SolveConfig carry for the hot path. */
+typedef struct {
+    const mosaic_gpu_module* modules;
+    int32_t n_modules;
+    const int32_t* edges; /* 2*n_edges module indices (upstream, downstream) */
+    int32_t n_edges;
+    int32_t gpu_count;      /* ClusterSpec.gpu_count */
+    double memory_capacity; /* ClusterSpec.memory_capacity (bytes) */
+    double e1, e2, e3;      /* InterferenceModel */
+    int32_t additive_only;
+    int32_t include_self;   /* PerfContext.include_self */
+    int32_t quota_levels;   /* SolveConfig.quota_levels = 1/granularity */
+    double bisect_rel_tol;  /* SolveConfig.bisect_rel_tol */
+    int32_t enable_prune, enable_cache;
+} mosaic_gpu_problem;
+
+typedef struct mosaic_gpu_ctx mosaic_gpu_ctx;
+
+/* One stage entry (StageAllocation::Entry, core.hpp:80-84). gpus[] is sorted. */
+typedef struct {
+    int32_t module, dp_degree, quota_units;
+    int32_t n_gpus;
+    int32_t gpus[MOSAIC_GPU_MAX_GPUS];
+} mosaic_gpu_entry;
+
+/* StageEvalResult (stage_eval.hpp:50-54) + search counters. */
+typedef struct {
+    int32_t status;    /* MOSAIC_OK / MOSAIC_INFEASIBLE / MOSAIC_MODULE_NO_OPTION */
+    double stage_time;
+    int32_t n_entries; /* entries sorted by module index */
+    mosaic_gpu_entry entries[MOSAIC_GPU_MAX_STAGE_MODULES];
+    int64_t probes;      /* feasibility probes replayed (reference feasibility_calls) */
+    int64_t gpu_searches; /* device searches launched */
+    int64_t nodes;       /* partial allocations expanded on the device */
+    int64_t leaves;      /* complete allocations scored on the device */
+} mosaic_gpu_stage_result;
+
+/* Context: validates the graph, builds surfaces, packs candidate-option tables
+ * into the device layout on `device` (cudaSetDevice index). */
+int mosaic_gpu_create(const mosaic_gpu_problem* p, int device, mosaic_gpu_ctx** out);
+void mosaic_gpu_destroy(mosaic_gpu_ctx* ctx);
+const char* mosaic_gpu_last_error(void);
+
+/* Number of modules / candidate options of module m (candidate_options order):
+ * rows are (d, units, base_latency, solo_bandwidth, footprint). */
+int mosaic_gpu_num_options(mosaic_gpu_ctx* ctx, int module, int32_t* n_out);
+int mosaic_gpu_options(mosaic_gpu_ctx* ctx, int module, int32_t* d, int32_t* units,
+                       double* base_latency, double* solo_bandwidth, double* footprint);
+
+/* Surface lookup (perf_model.hpp:124-147) for one module at (d, a). */
+int mosaic_gpu_lookup(mosaic_gpu_ctx* ctx, int module, int d, double a, double out4[4]);
+
+/* Compact entry for the batched evaluator: its GPU list is gpus[gpu_off .. gpu_off+n_gpus). */
+typedef struct {
+    int32_t module, dp_degree, quota_units, n_gpus;
+    int64_t gpu_off;
+} mosaic_gpu_eval_entry;
+
+/* Batched evaluator on the device: stage_time of n explicit allocations.
+ * Allocation i owns entries [alloc_off[i], alloc_off[i+1]) of `entries`
+ * (sorted by module index, as StageAllocation requires).  Rectified latencies per
+ * entry are optionally written to rect_out (same indexing as entries; may be NULL).
+ * Returns MOSAIC_RANGE if an entry's (d, units) is outside the module's surface. */
+int mosaic_gpu_stage_time(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* entries,
+                          const int32_t* gpus, const int64_t* alloc_off, int64_t n_allocs,
+                          double* stage_time_out, double* rect_out);
+
+/* stage_eval / ExactStageSolver::solve / FeasibilitySearch::run for one module set. */
+int mosaic_gpu_stage_eval(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_result* out);
+int mosaic_gpu_exact_stage(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_result* out);
+int mosaic_gpu_feasible(mosaic_gpu_ctx* ctx, uint64_t mask, double tau,
+                        mosaic_gpu_stage_result* out);
+
+/* Plan = ordered stages (DeploymentPlan, core.hpp:100-104). */
+#define MOSAIC_GPU_MAX_STAGES 64
+typedef struct {
+    int32_t status;
+    int32_t n_stages;
+    uint64_t stage_mask[MOSAIC_GPU_MAX_STAGES];
+    double stage_time[MOSAIC_GPU_MAX_STAGES];
+    double iteration_time;   /* summed left to right (solver.hpp:281-285) */
+    int64_t partitions_examined; /* brute force only */
+    /* SolveTrace totals (solver.hpp:106-126) */
+    int64_t rounds, stage_eval_calls, feasibility_calls, cache_hits, prunes;
+    int64_t gpu_searches, nodes, leaves;
+    double elapsed_s;
+} mosaic_gpu_plan_result;
+
+/* Stage allocations of a finished plan (read after solve / brute_force). */
+int mosaic_gpu_plan_stage(mosaic_gpu_ctx* ctx, int stage, mosaic_gpu_stage_result* out);
+
+int mosaic_gpu_solve(mosaic_gpu_ctx* ctx, mosaic_gpu_plan_result* out);
+int mosaic_gpu_brute_force(mosaic_gpu_ctx* ctx, mosaic_gpu_plan_result* out);
+
+/* GAHC round trace: round r, candidate c -> (mask_x, mask_y, pruned, cache_hit, gain). */
+int mosaic_gpu_trace_rounds(mosaic_gpu_ctx* ctx, int64_t* n_rounds);
+int mosaic_gpu_trace_round(mosaic_gpu_ctx* ctx, int64_t r, uint64_t* chosen_x,
+                           uint64_t* chosen_y, double* applied_gain, int64_t* n_cands);
+int mosaic_gpu_trace_cand(mosaic_gpu_ctx* ctx, int64_t r, int64_t c, uint64_t* mask_x,
+                          uint64_t* mask_y, int32_t* pruned, int32_t* cache_hit, double* gain);
+
+/* Drop the EvalCache (solver.hpp:39-75). */
+void mosaic_gpu_clear_cache(mosaic_gpu_ctx* ctx);
+
+/* Multi-GPU sharding of the search frontier (one rank per GPU).  The caller
+ * supplies an all-gather of `bytes` from every rank (torch.distributed over NCCL
+ * in bench.py); the library calls it once per device search with a 16-byte
+ * record per rank.  world == 1 disables it. */
+typedef int (*mosaic_gpu_allgather_fn)(void* user, const void* send, void* recv, size_t bytes);
+int mosaic_gpu_set_shard(mosaic_gpu_ctx* ctx, int rank, int world, mosaic_gpu_allgather_fn fn,
+                         void* user);
+
+/* Host-side merge of per-rank search records (exported for the gloo tests):
+ * records are {u64 key, f64 value}; mode 0 = MIN (smallest value, then key),
+ * mode 1 = FIRST (smallest key).  Writes the winning record index. */
+int mosaic_gpu_merge_records(const void* records, int world, int mode, int* winner);
+
+/* Kernel launches issued by this context so far (evidence for bench.py). */
+int64_t mosaic_gpu_launch_count(mosaic_gpu_ctx* ctx);
+/* Device time (ms) spent in the search kernels, by CUDA events on the ctx stream. */
+double mosaic_gpu_search_ms(mosaic_gpu_ctx* ctx);
+void mosaic_gpu_reset_counters(mosaic_gpu_ctx* ctx);
+
+/* Synthetic inputs (the reference's profiler, profiler.hpp:65-111/185-338, restated
+ * in C++ so the GPU box needs no reference): fills a problem for a named BASELINE
+ * config "cfg1".."cfg5", "random:SEED:N:G" or "preset:NAME:COUNT:G".  The returned
+ * problem owns its storage until mosaic_gpu_free_problem. */
+int mosaic_gpu_synth_problem(const char* spec, int quota_levels, mosaic_gpu_problem** out);
+void mosaic_gpu_free_problem(mosaic_gpu_problem* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOSAIC_GPU_H */

@@ -1,0 +1,399 @@
+// TEST INFRASTRUCTURE ONLY — never linked into, or called by, the product path.
+//
+// Driver around the UNMODIFIED reference headers (/root/reference/proj/include,
+// compiled in place by oracle/Makefile; nothing is copied into this repo).  It
+// builds the five BASELINE configs and the reference's own random instances,
+// runs the reference planner entry points and prints one JSON object per call:
+//
+//   solve            mosaic::solve                 (solver.hpp:157)
+//   oracle           mosaic::brute_force_optimum   (oracle.hpp:206)
+//   stage MASK       mosaic::stage_eval            (stage_eval.hpp:302)
+//   exact MASK       detail::ExactStageSolver      (oracle.hpp:86)
+//   feas MASK TAU    detail::FeasibilitySearch::run (stage_eval.hpp:113)
+//   options          candidate_options per module  (stage_eval.hpp:68)
+//   stime ALLOC      stage_time                    (perf_model.hpp:474)
+//   partitions       enumerate_partitions count    (oracle.hpp:35)
+//
+// Doubles are printed twice: "%a" (bit-exact, what parity tests compare) and
+// "%.17g" (readable).  When compiled with -DMOSAIC_INSTR against the
+// instrumented header copy under oracle/_ref/instr (see Makefile), every
+// scored leaf (stage_eval.hpp:254 verify_complete, oracle.hpp:112 leaf) and
+// every feasibility probe tau is counted and reported.
+#include <chrono>
+#include <cinttypes>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#ifdef MOSAIC_INSTR
+#include <vector>
+namespace mosaic_instr {
+inline long long leaves = 0;
+inline std::vector<double> probes;
+inline std::vector<int> probe_ok;
+}  // namespace mosaic_instr
+#endif
+
+#include "mosaic/bench.hpp"
+#include "mosaic/oracle.hpp"
+#include "mosaic/profiler.hpp"
+#include "mosaic/solver.hpp"
+#include "mosaic/stage_eval.hpp"
+
+using namespace mosaic;
+
+namespace {
+
+struct Instance {
+    std::string name;
+    ModelGraph graph;
+    std::vector<ModuleWorkload> workloads;
+    ClusterSpec cluster;
+    int levels = 10;
+    InterferenceModel im = default_ground_truth();
+    bool include_self = true;
+    SurfaceSet surfaces;
+    PerfContext ctx;
+
+    void finish() {
+        surfaces = generate_surfaces(workloads, cluster);
+        ctx.graph = &graph;
+        ctx.surfaces = &surfaces;
+        ctx.interference = im;
+        ctx.include_self = include_self;
+    }
+};
+
+void add(Instance& in, const ModuleWorkload& w) {
+    in.workloads.push_back(w);
+    in.graph.modules.push_back(detail::make_spec(w, w.id));
+}
+
+// The five BASELINE configs.
+bool make_config(const std::string& name, Instance& in) {
+    using detail::make_workload;
+    in.name = name;
+    if (name == "cfg1") {
+        add(in, make_workload("vision", 4.17, 35.2, 0.30, 0.60));
+        add(in, make_workload("text", 1.04, 20.5, 0.12, 0.45));
+        in.cluster.gpu_count = 8;
+        in.levels = 10;
+    } else if (name == "cfg2") {
+        add(in, make_workload("vit", 4.17, 35.2, 0.30, 0.60));
+        add(in, make_workload("proj", 0.05, 4.0, 0.02, 0.30));
+        add(in, make_workload("llm", 22.27, 145.2, 7.00, 0.80));
+        in.graph.edges = {{"vit", "proj"}, {"proj", "llm"}};
+        in.cluster.gpu_count = 16;
+        in.levels = 8;
+    } else if (name == "cfg3") {
+        add(in, make_workload("vision", 2.58, 82.4, 0.60, 0.70));
+        add(in, make_workload("text", 0.15, 2.1, 0.05, 0.30));
+        add(in, make_workload("deepstack", 0.30, 6.0, 0.05, 0.35));
+        add(in, make_workload("llm", 22.27, 145.2, 7.00, 0.80));
+        in.graph.edges = {{"vision", "deepstack"}, {"deepstack", "llm"}, {"text", "llm"}};
+        in.cluster.gpu_count = 32;
+        in.levels = 10;
+    } else if (name == "cfg4") {
+        add(in, make_workload("image", 4.17, 35.2, 0.30, 0.60));
+        add(in, make_workload("video", 1.80, 22.0, 0.35, 0.60));
+        add(in, make_workload("audio", 2.09, 22.8, 0.25, 0.50));
+        add(in, make_workload("llm", 16.70, 110.5, 3.20, 0.80));
+        add(in, make_workload("speech_dec", 0.95, 14.8, 0.20, 0.50));
+        add(in, make_workload("image_dec", 1.48, 24.6, 0.25, 0.55));
+        in.graph.edges = {{"image", "llm"},      {"video", "llm"},
+                          {"audio", "llm"},      {"llm", "speech_dec"},
+                          {"llm", "image_dec"}};
+        in.cluster.gpu_count = 64;
+        in.levels = 10;
+    } else if (name == "cfg5") {
+        auto p = make_preset("ofasys", 8);
+        in.graph = p.graph;
+        in.workloads = p.workloads;
+        in.cluster.gpu_count = 128;
+        in.levels = 32;
+    } else {
+        return false;
+    }
+    return true;
+}
+
+// inst spec: cfgN | random:SEED:N:G | preset:NAME:COUNT:G
+bool make_instance(const std::string& spec, Instance& in) {
+    if (make_config(spec, in)) return true;
+    char kind[32] = {0}, a[64] = {0};
+    if (spec.rfind("random:", 0) == 0) {
+        unsigned long long seed;
+        int n, g;
+        if (std::sscanf(spec.c_str(), "random:%llu:%d:%d", &seed, &n, &g) != 3) return false;
+        auto r = random_instance(seed, n, g);
+        in.name = spec;
+        in.graph = r.graph;
+        in.workloads = r.workloads;
+        in.cluster = r.cluster;
+        return true;
+    }
+    if (spec.rfind("preset:", 0) == 0) {
+        int count, g;
+        if (std::sscanf(spec.c_str(), "preset:%31[^:]:%d:%d", a, &count, &g) != 3) return false;
+        auto p = make_preset(a, count);
+        in.name = spec;
+        in.graph = p.graph;
+        in.workloads = p.workloads;
+        in.cluster.gpu_count = g;
+        return true;
+    }
+    (void)kind;
+    return false;
+}
+
+void pd(const char* key, double v, bool comma = true) {
+    std::printf("\"%s\":\"%a\",\"%s_dec\":%.17g%s", key, v, key, v, comma ? "," : "");
+}
+
+void print_alloc(const StageAllocation& al) {
+    std::printf("[");
+    for (size_t i = 0; i < al.entries.size(); ++i) {
+        const auto& e = al.entries[i];
+        std::printf("%s{\"m\":%d,\"d\":%d,\"u\":%d,\"gpus\":[", i ? "," : "", e.module,
+                    e.option.dp_degree, e.option.quota_units);
+        for (size_t j = 0; j < e.gpus.size(); ++j) std::printf("%s%d", j ? "," : "", e.gpus[j]);
+        std::printf("]}");
+    }
+    std::printf("]");
+}
+
+void print_plan(const DeploymentPlan& plan) {
+    std::printf("\"stages\":[");
+    for (size_t s = 0; s < plan.stages.size(); ++s) {
+        std::printf("%s{", s ? "," : "");
+        pd("t", plan.predicted_stage_times[s]);
+        std::printf("\"alloc\":");
+        print_alloc(plan.stages[s]);
+        std::printf("}");
+    }
+    std::printf("],");
+    pd("iteration_time", plan.predicted_iteration_time);
+}
+
+std::vector<int> mask_mods(uint64_t mask) {
+    std::vector<int> out;
+    for (int m = 0; m < 64; ++m)
+        if (mask >> m & 1) out.push_back(m);
+    return out;
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+void instr_reset() {
+#ifdef MOSAIC_INSTR
+    mosaic_instr::leaves = 0;
+    mosaic_instr::probes.clear();
+#endif
+}
+
+void instr_print() {
+#ifdef MOSAIC_INSTR
+    std::printf(",\"leaves\":%lld,\"probes\":[", mosaic_instr::leaves);
+    for (size_t i = 0; i < mosaic_instr::probes.size(); ++i)
+        std::printf("%s\"%a\"", i ? "," : "", mosaic_instr::probes[i]);
+    std::printf("]");
+#endif
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    if (argc < 3) {
+        std::fprintf(stderr,
+                     "usage: ref_driver INST OP [args] [levels=L] [e=e1,e2,e3] [noself] "
+                     "[additive] [reps=R] [noprune] [nocache]\n");
+        return 2;
+    }
+    Instance in;
+    if (!make_instance(argv[1], in)) {
+        std::fprintf(stderr, "bad instance %s\n", argv[1]);
+        return 2;
+    }
+    std::string op = argv[2];
+    std::vector<std::string> pos;
+    int reps = 1;
+    bool prune = true, cache = true;
+    for (int i = 3; i < argc; ++i) {
+        std::string a = argv[i];
+        if (a.rfind("levels=", 0) == 0) in.levels = std::atoi(a.c_str() + 7);
+        else if (a.rfind("gpus=", 0) == 0) in.cluster.gpu_count = std::atoi(a.c_str() + 5);
+        else if (a.rfind("mem=", 0) == 0) in.cluster.memory_capacity = std::strtod(a.c_str() + 4, nullptr);
+        else if (a.rfind("e=", 0) == 0)
+            std::sscanf(a.c_str() + 2, "%lf,%lf,%lf", &in.im.e1, &in.im.e2, &in.im.e3);
+        else if (a == "noself") in.include_self = false;
+        else if (a == "additive") in.im.additive_only = true;
+        else if (a.rfind("reps=", 0) == 0) reps = std::atoi(a.c_str() + 5);
+        else if (a == "noprune") prune = false;
+        else if (a == "nocache") cache = false;
+        else pos.push_back(a);
+    }
+    in.finish();
+    const int L = in.levels;
+
+    std::printf("{\"inst\":\"%s\",\"op\":\"%s\",\"levels\":%d,\"gpus\":%d,", in.name.c_str(),
+                op.c_str(), L, in.cluster.gpu_count);
+    try {
+        if (op == "solve") {
+            SolveConfig cfg{L, 1e-3, prune, cache};
+            SolveResult r;
+            std::vector<double> times;
+            for (int i = 0; i < reps; ++i) {
+                instr_reset();
+                double t0 = now_s();
+                r = solve(in.ctx, in.cluster, cfg);
+                times.push_back(now_s() - t0);
+            }
+            print_plan(r.plan);
+            std::printf("\"rounds\":[");
+            for (size_t i = 0; i < r.trace.rounds.size(); ++i) {
+                const auto& rd = r.trace.rounds[i];
+                std::printf("%s{\"x\":%" PRIu64 ",\"y\":%" PRIu64 ",\"gain\":\"%a\",\"cands\":[",
+                            i ? "," : "", rd.chosen_x, rd.chosen_y, rd.applied_gain);
+                for (size_t j = 0; j < rd.candidates.size(); ++j) {
+                    const auto& c = rd.candidates[j];
+                    std::printf("%s{\"x\":%" PRIu64 ",\"y\":%" PRIu64
+                                ",\"pruned\":%d,\"hit\":%d,\"gain\":\"%a\"}",
+                                j ? "," : "", c.mask_x, c.mask_y, c.pruned, c.cache_hit, c.gain);
+                }
+                std::printf("]}");
+            }
+            std::printf("],\"stage_eval_calls\":%lld,\"feasibility_calls\":%lld,\"times\":[",
+                        r.trace.stage_eval_calls, r.trace.feasibility_calls);
+            for (size_t i = 0; i < times.size(); ++i) std::printf("%s%.9g", i ? "," : "", times[i]);
+            std::printf("]");
+            instr_print();
+        } else if (op == "oracle") {
+            std::optional<OracleResult> r;
+            std::vector<double> times;
+            for (int i = 0; i < reps; ++i) {
+                instr_reset();
+                double t0 = now_s();
+                r = brute_force_optimum(in.ctx, in.cluster, L);
+                times.push_back(now_s() - t0);
+            }
+            std::printf("\"feasible\":%d,", r ? 1 : 0);
+            if (r) {
+                print_plan(r->plan);
+                std::printf("\"partitions\":%lld,", r->partitions_examined);
+            }
+            std::printf("\"times\":[");
+            for (size_t i = 0; i < times.size(); ++i) std::printf("%s%.9g", i ? "," : "", times[i]);
+            std::printf("]");
+            instr_print();
+        } else if (op == "stage" || op == "exact") {
+            uint64_t mask = std::strtoull(pos.at(0).c_str(), nullptr, 0);
+            auto mods = mask_mods(mask);
+            std::optional<StageEvalResult> r;
+            std::vector<double> times;
+            int status = 0;
+            for (int i = 0; i < reps; ++i) {
+                instr_reset();
+                double t0 = now_s();
+                try {
+                    if (op == "stage") {
+                        r = stage_eval(in.ctx, in.cluster, mods, {L, 1e-3});
+                    } else {
+                        detail::ExactStageSolver ex(in.ctx, in.cluster, L);
+                        r = ex.solve(mods);
+                    }
+                } catch (const StageInfeasibleError&) {
+                    status = 2;
+                }
+                times.push_back(now_s() - t0);
+            }
+            std::printf("\"mask\":%" PRIu64 ",\"status\":%d,\"feasible\":%d,", mask, status,
+                        r ? 1 : 0);
+            if (r) {
+                pd("t", r->stage_time);
+                std::printf("\"alloc\":");
+                print_alloc(r->allocation);
+                std::printf(",\"feasibility_calls\":%lld,\"nodes\":%lld,",
+                            r->stats.feasibility_calls, r->stats.nodes);
+            }
+            std::printf("\"times\":[");
+            for (size_t i = 0; i < times.size(); ++i) std::printf("%s%.9g", i ? "," : "", times[i]);
+            std::printf("]");
+            instr_print();
+        } else if (op == "feas") {
+            uint64_t mask = std::strtoull(pos.at(0).c_str(), nullptr, 0);
+            double tau = std::strtod(pos.at(1).c_str(), nullptr);
+            auto mods = mask_mods(mask);
+            std::vector<std::vector<CandidateOption>> options;
+            for (int m : mods) options.push_back(candidate_options(in.ctx, in.cluster, m, L));
+            SolverStats stats;
+            detail::FeasibilitySearch fs(in.ctx, in.cluster, mods, options, L, stats);
+            auto r = fs.run(tau);
+            std::printf("\"mask\":%" PRIu64 ",", mask);
+            pd("tau", tau);
+            std::printf("\"feasible\":%d", r ? 1 : 0);
+            if (r) {
+                std::printf(",");
+                pd("t", stage_time(in.ctx, *r), false);
+                std::printf(",\"alloc\":");
+                print_alloc(*r);
+            }
+        } else if (op == "options") {
+            std::printf("\"modules\":[");
+            for (int m = 0; m < in.graph.size(); ++m) {
+                auto opts = candidate_options(in.ctx, in.cluster, m, L);
+                std::printf("%s{\"id\":\"%s\",\"rows\":[", m ? "," : "",
+                            in.graph.modules[m].id.c_str());
+                for (size_t i = 0; i < opts.size(); ++i) {
+                    const auto& c = opts[i];
+                    std::printf("%s[%d,%d,\"%a\",\"%a\",\"%a\"]", i ? "," : "", c.opt.dp_degree,
+                                c.opt.quota_units, c.base_latency, c.solo_bandwidth, c.footprint);
+                }
+                std::printf("]}");
+            }
+            std::printf("]");
+        } else if (op == "stime") {
+            // ALLOC: m:d:u:g0.g1.g2;m:d:u:...
+            StageAllocation al;
+            std::string s = pos.at(0);
+            size_t p = 0;
+            while (p < s.size()) {
+                size_t q = s.find(';', p);
+                if (q == std::string::npos) q = s.size();
+                std::string ent = s.substr(p, q - p);
+                StageAllocation::Entry e;
+                int m, d, u;
+                char gl[4096] = {0};
+                std::sscanf(ent.c_str(), "%d:%d:%d:%4095s", &m, &d, &u, gl);
+                e.module = m;
+                e.option = {d, u, L};
+                std::string g = gl;
+                size_t a = 0;
+                while (a < g.size()) {
+                    size_t b = g.find('.', a);
+                    if (b == std::string::npos) b = g.size();
+                    e.gpus.push_back(std::atoi(g.substr(a, b - a).c_str()));
+                    a = b + 1;
+                }
+                al.entries.push_back(e);
+                p = q + 1;
+            }
+            pd("t", stage_time(in.ctx, al), false);
+        } else if (op == "partitions") {
+            auto parts = enumerate_partitions(in.graph);
+            std::printf("\"count\":%zu", parts.size());
+        } else {
+            std::printf("\"error\":\"unknown op\"}\n");
+            return 2;
+        }
+    } catch (const std::exception& ex) {
+        std::printf("\"exception\":\"%s\"}\n", ex.what());
+        return 3;
+    }
+    std::printf("}\n");
+    return 0;
+}

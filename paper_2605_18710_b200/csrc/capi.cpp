@@ -1,0 +1,381 @@
+// capi.cpp — extern "C" boundary (include/mosaic_gpu.h).  No exception crosses it.
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/mosaic_gpu.h"
+#include "planner.hpp"
+
+using namespace mosaic_b200;
+
+struct mosaic_gpu_ctx {
+    std::unique_ptr<Planner> pl;
+    PlanResult plan;
+    int rank = 0, world = 1;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        g_err.clear();
+        return f();
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.status;
+    } catch (const RangeError& e) {
+        g_err = e.what();
+        return MOSAIC_RANGE;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return MOSAIC_CUDA;
+    }
+}
+
+void fill_stage(const StageResult& r, mosaic_gpu_stage_result* out) {
+    std::memset(out, 0, sizeof(*out));
+    out->status = r.status;
+    out->stage_time = r.stage_time;
+    if (r.entries.size() > MOSAIC_GPU_MAX_STAGE_MODULES)
+        throw Error(MOSAIC_TOO_LARGE, "too many entries for the result struct");
+    out->n_entries = (int32_t)r.entries.size();
+    for (size_t i = 0; i < r.entries.size(); ++i) {
+        const Entry& e = r.entries[i];
+        auto& o = out->entries[i];
+        o.module = e.module;
+        o.dp_degree = e.d;
+        o.quota_units = e.units;
+        if (e.gpus.size() > MOSAIC_GPU_MAX_GPUS) throw Error(MOSAIC_TOO_LARGE, "too many GPUs");
+        o.n_gpus = (int32_t)e.gpus.size();
+        for (size_t g = 0; g < e.gpus.size(); ++g) o.gpus[g] = e.gpus[g];
+    }
+    out->probes = r.probes;
+    out->gpu_searches = r.st.searches;
+    out->nodes = r.st.nodes;
+    out->leaves = r.st.leaves;
+}
+
+void fill_plan(const PlanResult& p, mosaic_gpu_plan_result* out) {
+    std::memset(out, 0, sizeof(*out));
+    out->status = p.status;
+    if (p.masks.size() > MOSAIC_GPU_MAX_STAGES) throw Error(MOSAIC_TOO_LARGE, "too many stages");
+    out->n_stages = (int32_t)p.masks.size();
+    for (size_t i = 0; i < p.masks.size(); ++i) {
+        out->stage_mask[i] = p.masks[i];
+        out->stage_time[i] = p.stages[i].stage_time;
+    }
+    out->iteration_time = p.iteration_time;
+    out->partitions_examined = p.partitions;
+    out->rounds = (int64_t)p.rounds.size();
+    out->stage_eval_calls = p.stage_eval_calls;
+    out->feasibility_calls = p.feasibility_calls;
+    out->cache_hits = p.cache_hits;
+    out->prunes = p.prunes;
+    out->gpu_searches = p.st.searches;
+    out->nodes = p.st.nodes;
+    out->leaves = p.st.leaves;
+    out->elapsed_s = p.elapsed;
+}
+
+Problem to_problem(const mosaic_gpu_problem* p) {
+    if (!p) throw Error(MOSAIC_RANGE, "null problem");
+    if (p->n_modules < 0 || p->n_modules > MOSAIC_GPU_MAX_MODULES)
+        throw Error(MOSAIC_RANGE, "module count out of range");
+    Problem P;
+    for (int m = 0; m < p->n_modules; ++m) {
+        const auto& src = p->modules[m];
+        Module mod;
+        mod.id = src.id ? src.id : "";
+        mod.memory_base = src.memory_base;
+        std::vector<Point> pts;
+        for (int i = 0; i < src.n_points; ++i) {
+            const auto& q = src.points[i];
+            pts.push_back(Point{q.d, q.a, q.latency, q.bandwidth_util, q.memory, q.sm_active});
+        }
+        mod.surface = Surface(mod.id, pts);
+        P.modules.push_back(std::move(mod));
+    }
+    for (int e = 0; e < p->n_edges; ++e) P.edges.push_back({p->edges[2 * e], p->edges[2 * e + 1]});
+    P.gpu_count = p->gpu_count;
+    if (P.gpu_count < 1 || P.gpu_count > MOSAIC_GPU_MAX_GPUS)
+        throw Error(MOSAIC_RANGE, "gpu_count out of range");
+    P.memory_capacity = p->memory_capacity;
+    P.im.e1 = p->e1;
+    P.im.e2 = p->e2;
+    P.im.e3 = p->e3;
+    P.im.additive_only = p->additive_only != 0;
+    P.include_self = p->include_self != 0;
+    P.quota_levels = p->quota_levels;
+    if (P.quota_levels < 1) throw Error(MOSAIC_RANGE, "quota_levels must be >= 1");
+    P.bisect_rel_tol = p->bisect_rel_tol;
+    P.enable_prune = p->enable_prune != 0;
+    P.enable_cache = p->enable_cache != 0;
+    return P;
+}
+
+struct OwnedProblem {
+    mosaic_gpu_problem p;  // must stay first
+    std::vector<mosaic_gpu_module> mods;
+    std::vector<std::vector<mosaic_gpu_point>> pts;
+    std::vector<std::string> ids;
+    std::vector<int32_t> edges;
+};
+}  // namespace
+
+extern "C" {
+
+const char* mosaic_gpu_last_error(void) { return g_err.c_str(); }
+
+int mosaic_gpu_create(const mosaic_gpu_problem* p, int device, mosaic_gpu_ctx** out) {
+    return guard([&] {
+        auto ctx = std::make_unique<mosaic_gpu_ctx>();
+        ctx->pl = std::make_unique<Planner>(to_problem(p), device);
+        *out = ctx.release();
+        return MOSAIC_OK;
+    });
+}
+
+void mosaic_gpu_destroy(mosaic_gpu_ctx* ctx) { delete ctx; }
+
+int mosaic_gpu_num_options(mosaic_gpu_ctx* ctx, int module, int32_t* n_out) {
+    return guard([&] {
+        if (module < 0 || module >= (int)ctx->pl->problem().modules.size())
+            throw Error(MOSAIC_RANGE, "module index out of range");
+        *n_out = (int32_t)ctx->pl->options(module).size();
+        return MOSAIC_OK;
+    });
+}
+
+int mosaic_gpu_options(mosaic_gpu_ctx* ctx, int module, int32_t* d, int32_t* units,
+                       double* base_latency, double* solo_bandwidth, double* footprint) {
+    return guard([&] {
+        if (module < 0 || module >= (int)ctx->pl->problem().modules.size())
+            throw Error(MOSAIC_RANGE, "module index out of range");
+        const auto& o = ctx->pl->options(module);
+        for (size_t i = 0; i < o.size(); ++i) {
+            d[i] = o[i].d;
+            units[i] = o[i].units;
+            base_latency[i] = o[i].base;
+            solo_bandwidth[i] = o[i].B;
+            footprint[i] = o[i].fp;
+        }
+        return MOSAIC_OK;
+    });
+}
+
+int mosaic_gpu_lookup(mosaic_gpu_ctx* ctx, int module, int d, double a, double out4[4]) {
+    return guard([&] {
+        if (module < 0 || module >= (int)ctx->pl->problem().modules.size())
+            throw Error(MOSAIC_RANGE, "module index out of range");
+        Sample s = ctx->pl->problem().modules[module].surface.lookup(d, a);
+        out4[0] = s.latency;
+        out4[1] = s.bandwidth_util;
+        out4[2] = s.memory;
+        out4[3] = s.sm_active;
+        return MOSAIC_OK;
+    });
+}
+
+int mosaic_gpu_stage_time(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* entries,
+                          const int32_t* gpus, const int64_t* alloc_off, int64_t n_allocs,
+                          double* stage_time_out, double* rect_out) {
+    return guard([&] {
+        std::vector<std::vector<Entry>> allocs(n_allocs);
+        for (int64_t i = 0; i < n_allocs; ++i) {
+            for (int64_t e = alloc_off[i]; e < alloc_off[i + 1]; ++e) {
+                const auto& E = entries[e];
+                Entry x{E.module, E.dp_degree, E.quota_units, {}};
+                x.gpus.assign(gpus + E.gpu_off, gpus + E.gpu_off + E.n_gpus);
+                allocs[i].push_back(std::move(x));
+            }
+        }
+        std::vector<double> st;
+        std::vector<std::vector<double>> rect;
+        ctx->pl->stage_time(allocs, st, rect);
+        for (int64_t i = 0; i < n_allocs; ++i) {
+            stage_time_out[i] = st[i];
+            if (rect_out)
+                for (int64_t e = alloc_off[i]; e < alloc_off[i + 1]; ++e)
+                    rect_out[e] = rect[i][e - alloc_off[i]];
+        }
+        return MOSAIC_OK;
+    });
+}
+
+int mosaic_gpu_stage_eval(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_result* out) {
+    return guard([&] {
+        StageResult r = ctx->pl->stage_eval(mask);
+        fill_stage(r, out);
+        return r.status;
+    });
+}
+
+int mosaic_gpu_exact_stage(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_result* out) {
+    return guard([&] {
+        StageResult r = ctx->pl->exact_stage(mask);
+        fill_stage(r, out);
+        return r.status;
+    });
+}
+
+int mosaic_gpu_feasible(mosaic_gpu_ctx* ctx, uint64_t mask, double tau,
+                        mosaic_gpu_stage_result* out) {
+    return guard([&] {
+        StageResult r = ctx->pl->feasible(mask, tau);
+        fill_stage(r, out);
+        return r.status;
+    });
+}
+
+int mosaic_gpu_plan_stage(mosaic_gpu_ctx* ctx, int stage, mosaic_gpu_stage_result* out) {
+    return guard([&] {
+        if (stage < 0 || stage >= (int)ctx->plan.stages.size())
+            throw Error(MOSAIC_RANGE, "stage index out of range");
+        fill_stage(ctx->plan.stages[stage], out);
+        return MOSAIC_OK;
+    });
+}
+
+int mosaic_gpu_solve(mosaic_gpu_ctx* ctx, mosaic_gpu_plan_result* out) {
+    return guard([&] {
+        ctx->plan = ctx->pl->solve();
+        fill_plan(ctx->plan, out);
+        return ctx->plan.status;
+    });
+}
+
+int mosaic_gpu_brute_force(mosaic_gpu_ctx* ctx, mosaic_gpu_plan_result* out) {
+    return guard([&] {
+        ctx->plan = ctx->pl->brute_force();
+        fill_plan(ctx->plan, out);
+        return ctx->plan.status;
+    });
+}
+
+int mosaic_gpu_trace_rounds(mosaic_gpu_ctx* ctx, int64_t* n_rounds) {
+    *n_rounds = (int64_t)ctx->plan.rounds.size();
+    return MOSAIC_OK;
+}
+
+int mosaic_gpu_trace_round(mosaic_gpu_ctx* ctx, int64_t r, uint64_t* chosen_x,
+                           uint64_t* chosen_y, double* applied_gain, int64_t* n_cands) {
+    return guard([&] {
+        if (r < 0 || r >= (int64_t)ctx->plan.rounds.size()) throw Error(MOSAIC_RANGE, "round");
+        const auto& R = ctx->plan.rounds[r];
+        *chosen_x = R.chosen_x;
+        *chosen_y = R.chosen_y;
+        *applied_gain = R.applied_gain;
+        *n_cands = (int64_t)R.cands.size();
+        return MOSAIC_OK;
+    });
+}
+
+int mosaic_gpu_trace_cand(mosaic_gpu_ctx* ctx, int64_t r, int64_t c, uint64_t* mask_x,
+                          uint64_t* mask_y, int32_t* pruned, int32_t* cache_hit, double* gain) {
+    return guard([&] {
+        if (r < 0 || r >= (int64_t)ctx->plan.rounds.size()) throw Error(MOSAIC_RANGE, "round");
+        const auto& R = ctx->plan.rounds[r];
+        if (c < 0 || c >= (int64_t)R.cands.size()) throw Error(MOSAIC_RANGE, "candidate");
+        const auto& C = R.cands[c];
+        *mask_x = C.mask_x;
+        *mask_y = C.mask_y;
+        *pruned = C.pruned;
+        *cache_hit = C.cache_hit;
+        *gain = C.gain;
+        return MOSAIC_OK;
+    });
+}
+
+void mosaic_gpu_clear_cache(mosaic_gpu_ctx* ctx) { ctx->pl->clear_cache(); }
+
+int mosaic_gpu_set_shard(mosaic_gpu_ctx* ctx, int rank, int world, mosaic_gpu_allgather_fn fn,
+                         void* user) {
+    return guard([&] {
+        if (world < 1 || rank < 0 || rank >= world) throw Error(MOSAIC_RANGE, "bad rank/world");
+        if (world > 1 && !fn) throw Error(MOSAIC_RANGE, "world > 1 needs an all-gather");
+        ctx->rank = rank;
+        ctx->world = world;
+        ctx->pl->engine().set_shard(rank, world, fn, user);
+        return MOSAIC_OK;
+    });
+}
+
+int mosaic_gpu_merge_records(const void* records, int world, int mode, int* winner) {
+    struct Rec {
+        uint64_t key;
+        double value;
+    };
+    const Rec* r = reinterpret_cast<const Rec*>(records);
+    int w = -1;
+    for (int i = 0; i < world; ++i) {
+        if (w < 0) {
+            w = i;
+            continue;
+        }
+        bool better = mode == 0 ? (r[i].value < r[w].value ||
+                                   (r[i].value == r[w].value && r[i].key < r[w].key))
+                                : r[i].key < r[w].key;
+        if (better) w = i;
+    }
+    *winner = w;
+    return w < 0 ? MOSAIC_RANGE : MOSAIC_OK;
+}
+
+int64_t mosaic_gpu_launch_count(mosaic_gpu_ctx* ctx) { return ctx->pl->engine().launches(); }
+double mosaic_gpu_search_ms(mosaic_gpu_ctx* ctx) {
+    return ctx->pl->engine().search_ms() + ctx->pl->engine().eval_ms();
+}
+void mosaic_gpu_reset_counters(mosaic_gpu_ctx* ctx) { ctx->pl->engine().reset_counters(); }
+
+int mosaic_gpu_synth_problem(const char* spec, int quota_levels, mosaic_gpu_problem** out) {
+    return guard([&] {
+        Problem P = synth_problem(spec ? spec : "", quota_levels);
+        auto op = std::make_unique<OwnedProblem>();
+        std::memset(&op->p, 0, sizeof(op->p));
+        op->ids.reserve(P.modules.size());
+        for (auto& m : P.modules) {
+            op->ids.push_back(m.id);
+            // re-emit the surface grid from the reference generator's own points
+            std::vector<mosaic_gpu_point> pts;
+            for (double dv : m.surface.d_values())
+                for (int i = 1; i <= 10; ++i) {
+                    double a = i / 10.0;
+                    Sample s = m.surface.lookup((int)dv, a);
+                    pts.push_back(mosaic_gpu_point{(int32_t)dv, a, s.latency, s.bandwidth_util,
+                                                   s.memory, s.sm_active});
+                }
+            op->pts.push_back(std::move(pts));
+        }
+        for (size_t i = 0; i < P.modules.size(); ++i)
+            op->mods.push_back(mosaic_gpu_module{op->ids[i].c_str(), P.modules[i].memory_base,
+                                                 op->pts[i].data(), (int32_t)op->pts[i].size()});
+        for (auto [u, v] : P.edges) {
+            op->edges.push_back(u);
+            op->edges.push_back(v);
+        }
+        op->p.modules = op->mods.data();
+        op->p.n_modules = (int32_t)op->mods.size();
+        op->p.edges = op->edges.data();
+        op->p.n_edges = (int32_t)P.edges.size();
+        op->p.gpu_count = P.gpu_count;
+        op->p.memory_capacity = P.memory_capacity;
+        op->p.e1 = P.im.e1;
+        op->p.e2 = P.im.e2;
+        op->p.e3 = P.im.e3;
+        op->p.additive_only = 0;
+        op->p.include_self = 1;
+        op->p.quota_levels = P.quota_levels;
+        op->p.bisect_rel_tol = 1e-3;
+        op->p.enable_prune = 1;
+        op->p.enable_cache = 1;
+        *out = &op.release()->p;
+        return MOSAIC_OK;
+    });
+}
+
+void mosaic_gpu_free_problem(mosaic_gpu_problem* p) { delete reinterpret_cast<OwnedProblem*>(p); }
+
+}  // extern "C"

@@ -1,0 +1,96 @@
+// engine.hpp — device search engine (sm_100a) used by the host planner.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "spec_build.hpp"
+
+namespace mg {
+
+typedef int (*AllGatherFn)(void* user, const void* send, void* recv, size_t bytes);
+
+struct SearchStats {
+    long long nodes = 0, leaves = 0, rounds = 0, searches = 0;
+};
+
+struct SearchResult {
+    bool found = false;  // FIRST: a leaf with value <= theta exists (in filter order)
+    Leaf leaf{};         // FIRST: that leaf
+    double value = POS_INF;  // MIN: best value found (< ub), else ub
+    bool aborted = false;    // MIN: incumbent fell below abort_below
+    bool overflow = false;   // a level needed more than MAXB blocks
+};
+
+struct EvalEntry {  // device evaluator input (one per allocation entry)
+    int row;        // option row (base, B) of this entry
+    int module;
+    int n_gpus;
+    int pad;
+    long long gpu_off;
+};
+
+class Engine {
+  public:
+    explicit Engine(int device);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    void upload_rows(const Model& M);
+    SearchResult search(const Spec& S, double ub, double abort_below, SearchStats& st);
+    // Batched stage_time (K1): per allocation, entries [off[i], off[i+1]).
+    void evaluate(const std::vector<EvalEntry>& ent, const std::vector<int>& gpus,
+                  const std::vector<long long>& off, const std::vector<double>& base,
+                  const std::vector<double>& Bt, int G, const Model& M,
+                  std::vector<double>& st_out, std::vector<double>& rect_out);
+    double eval_ms() const { return eval_ms_; }
+
+    void set_shard(int rank, int world, AllGatherFn fn, void* user) {
+        rank_ = rank;
+        world_ = world;
+        ag_ = fn;
+        ag_user_ = user;
+    }
+    long long launches() const { return launches_; }
+    double search_ms() const { return search_ms_; }
+    void reset_counters() {
+        launches_ = 0;
+        search_ms_ = 0;
+    }
+    long long budget = 1 << 14;   // DFS steps per frontier item per round
+    long long min_front = 8192;   // expand without searching below this many items
+    long long cap_front = 1 << 21;
+
+  private:
+    void ensure_front(long long n);
+    int device_;
+    int rank_ = 0, world_ = 1;
+    AllGatherFn ag_ = nullptr;
+    void* ag_user_ = nullptr;
+    void* stream_ = nullptr;
+    void* ev0_ = nullptr;
+    void* ev1_ = nullptr;
+    // device buffers
+    double *d_base_ = nullptr, *d_B_ = nullptr, *d_fp_ = nullptr, *d_bound_ = nullptr;
+    int *d_d_ = nullptr, *d_u_ = nullptr;
+    int n_rows_ = 0;
+    void* d_spec_ = nullptr;
+    void* d_ctl_ = nullptr;
+    void* d_leaf_ = nullptr;
+    void* d_front_[3] = {nullptr, nullptr, nullptr};
+    long long* d_key_[3] = {nullptr, nullptr, nullptr};
+    long long* d_cnt_ = nullptr;
+    long long* d_off_ = nullptr;
+    unsigned char* d_flag_ = nullptr;
+    long long* d_nsel_ = nullptr;
+    void* d_tmp_ = nullptr;
+    size_t tmp_bytes_ = 0;
+    long long front_cap_ = 0;
+    void* h_pin_ = nullptr;
+    long long launches_ = 0;
+    double search_ms_ = 0;
+    double eval_ms_ = 0;
+};
+
+}  // namespace mg

@@ -1,0 +1,104 @@
+// planner.hpp — host mirror of the reference planner API, backed by the device engine.
+//
+//   stage_eval      stage_eval.hpp:302-382 (tau doubling, bisection, confirmation)
+//   feasible        detail::FeasibilitySearch::run, stage_eval.hpp:113-164
+//   exact_stage     detail::ExactStageSolver::solve, oracle.hpp:86-103
+//   solve           GAHC, solver.hpp:157-289 (EvalCache, legal_merge, early_prune)
+//   brute_force     brute_force_optimum + enumerate_partitions, oracle.hpp:35-71, 206-255
+//   stage_time      rectified_latency/stage_time, perf_model.hpp:442-479 (batched, K1)
+//
+// Every candidate-plan search runs on the GPU (engine.cu).  The host only replays
+// the reference's control flow (which tau to probe next, which merge to apply) and
+// converts winning leaves back into StageAllocations.
+#pragma once
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "engine.hpp"
+#include "model.hpp"
+
+namespace mosaic_b200 {
+
+enum Status { OK = 0, INFEASIBLE = 1, MODULE_NO_OPTION = 2, RANGE = 3, TOO_LARGE = 4,
+              CUDA = 5, EMPTY = 6 };
+
+struct Error : std::runtime_error {
+    int status;
+    Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+struct Entry {
+    int module, d, units;
+    std::vector<int> gpus;
+};
+
+struct StageResult {
+    int status = INFEASIBLE;
+    double stage_time = 0.0;
+    std::vector<Entry> entries;  // sorted by module index
+    long long probes = 0;        // FeasibilitySearch::run calls replayed
+    mg::SearchStats st;
+};
+
+struct TraceCand {
+    uint64_t mask_x, mask_y;
+    bool pruned, cache_hit;
+    double gain;
+};
+struct TraceRound {
+    std::vector<TraceCand> cands;
+    uint64_t chosen_x = 0, chosen_y = 0;
+    double applied_gain = 0.0;
+};
+
+struct PlanResult {
+    int status = OK;
+    std::vector<uint64_t> masks;
+    std::vector<StageResult> stages;
+    double iteration_time = 0.0;
+    long long partitions = 0;
+    long long stage_eval_calls = 0, feasibility_calls = 0, cache_hits = 0, prunes = 0;
+    std::vector<TraceRound> rounds;
+    mg::SearchStats st;
+    double elapsed = 0.0;
+};
+
+class Planner {
+  public:
+    Planner(Problem P, int device);
+    const Problem& problem() const { return P_; }
+    const std::vector<Cand>& options(int m) const { return opts_.at(m); }
+
+    StageResult stage_eval(uint64_t mask);
+    StageResult exact_stage(uint64_t mask);
+    StageResult feasible(uint64_t mask, double tau);
+    PlanResult solve();
+    PlanResult brute_force();
+    // stage_time of explicit allocations (entries per allocation sorted by module)
+    void stage_time(const std::vector<std::vector<Entry>>& allocs, std::vector<double>& st,
+                    std::vector<std::vector<double>>& rect);
+
+    mg::Engine& engine() { return *eng_; }
+    void clear_cache() { cache_.clear(); }
+
+  private:
+    void check_rows(int m) const;
+    bool first_leaf(const std::vector<int>& order, bool filter, double theta, mg::Leaf& leaf,
+                    mg::SearchStats& st);
+    double min_value(const std::vector<int>& mods, double ub, mg::SearchStats& st);
+    std::vector<Entry> leaf_entries(const std::vector<int>& order, const mg::Leaf& lf) const;
+    std::optional<StageResult> evaluate_cached(uint64_t mask, bool* hit, PlanResult& pr);
+
+    Problem P_;
+    mg::Model M_;
+    std::vector<std::vector<Cand>> opts_;
+    std::vector<std::string> opt_err_;
+    std::unique_ptr<mg::Engine> eng_;
+    std::unordered_map<uint64_t, StageResult> cache_;
+};
+
+}  // namespace mosaic_b200

@@ -1,0 +1,530 @@
+// search_core.cuh — per-thread canonical-placement branch-and-bound over one stage.
+//
+// What it searches (reference semantics, SURVEY.md §7 "Exact leaf order"):
+//   levels j = 0..k-1 place module pi_j: choose an option (candidate_options order,
+//   stage_eval.hpp:68-93) then a placement.  GPUs are kept as BLOCKS — maximal runs of
+//   consecutive GPUs with identical resident sets, always contiguous — and a
+//   placement takes a prefix of each eligible block (count vector x), visited in
+//   descending lexicographic order of x.  That is exactly the set and order of leaves
+//   FeasibilitySearch::place visits with its signature skip (stage_eval.hpp:204-214)
+//   and, for ExactStageSolver (oracle.hpp:157-180), the order among canonical leaves,
+//   which always contains its lexicographically-first argmin.
+//
+//   MODE_FIRST: first leaf in that DFS order whose stage_time <= theta
+//               (FeasibilitySearch::run with theta = tau*(1+1e-12), filter
+//               stage_eval.hpp:119-130; or the exact argmin with theta = T*).
+//   MODE_MIN:   minimum stage_time over all leaves below an incumbent (T*).
+//
+// Leaf value is computed bit-exactly as stage_time (perf_model.hpp:442-479):
+// residents summed in module-index order, (e1 + e2*sum) + e3*prod, base + worst,
+// max starting at 0.0; the file is compiled with -fmad=false.  Because a block's
+// contribution depends only on its resident set, the LAST level is resolved in
+// closed form over blocks (per-block interval of admissible take counts) instead
+// of enumerating its compositions.
+//
+// Pruning is sound and never reorders leaves: option filter/break, total quota
+// demand (stage_eval.hpp:141-147,176-178), per-block capacity and memory
+// (:208-210), an interference lower bound per block that adds a product-term
+// envelope over the still-unplaced modules, and a one-step look-ahead that every
+// unplaced module still has an option that fits.  All bound comparisons carry a
+// 1e-12 relative slack so fp rounding can only weaken them.
+#pragma once
+#include <stdint.h>
+
+#ifndef MG_HD
+#define MG_HD __device__ __forceinline__
+#endif
+// Device code below is only compiled by nvcc (the host planner includes this header
+// for the Spec/Node/Leaf layouts only; there is no host search path).
+#if defined(__CUDACC__) || defined(MG_HOST_HARNESS)
+#define MG_DEVICE_CODE 1
+#endif
+
+namespace mg {
+
+constexpr int MAXK = 12;   // modules per stage
+constexpr int MAXB = 128;  // blocks per level
+constexpr int MAXENV = 16; // envelope lines per level
+constexpr int FB = MAXB;   // blocks carried by a frontier node
+constexpr double NEG_INF = -1.0e300;
+constexpr double POS_INF = 1.0e300;
+
+enum { MODE_MIN = 0, MODE_FIRST = 1 };
+
+struct Spec {
+    int k, G, L, mode;
+    int nonneg, include_self, additive, use_filter;
+    double e1, e2, e3, cap_slack;  // cap_slack = memory_capacity * (1 + 1e-12)
+    double theta;                  // FIRST: accept iff stage_time <= theta
+    double thp;                    // static prune threshold (theta or UB) * (1 + 1e-12)
+    int lvl_n[MAXK];               // viable options per level (a prefix of the sorted list)
+    int lvl_off[MAXK];             // row offset of each level's options
+    int pos_lvl[MAXK];             // module-index position -> level
+    int suffix_min[MAXK + 1];      // min quota demand d*u over levels >= j
+    int env_n[MAXK + 1];           // product-term envelope over unplaced levels >= j
+    double env_a[MAXK + 1][MAXENV];
+    double env_b[MAXK + 1][MAXENV];
+};
+
+struct Rows {
+    const double* base;
+    const double* B;
+    const double* fp;
+    const double* bound;  // reference filter bound (stage_eval.hpp:122-127)
+    const int* d;
+    const int* u;
+};
+
+// Frontier node: a partial allocation at `depth` (levels < depth placed).
+struct Node {
+    uint16_t opt[MAXK];
+    uint16_t depth, nb;
+    uint16_t bsz[FB];
+    uint16_t bmk[FB];
+};
+
+// Leaf: options of every level plus the final block list (sizes, level masks).
+struct Leaf {
+    double value;
+    int nb;
+    int pad;
+    uint16_t opt[MAXK];
+    uint16_t bsz[2 * MAXB];
+    uint16_t bmk[2 * MAXB];
+};
+
+// Block storage offsets: level j holds at most min(2^j, MAXB) blocks.
+#ifdef MG_DEVICE_CODE
+MG_HD int lvl_cap(int j) { return j >= 7 ? MAXB : (1 << j); }
+MG_HD int lvl_off(int j) {
+    int off = 0;
+    for (int i = 0; i < j; ++i) off += lvl_cap(i);
+    return off;
+}
+#endif
+constexpr int WALK_SLOTS = 255 + (MAXK + 1 - 8) * MAXB;  // sum_{j<=MAXK} lvl_cap(j)
+
+struct Walk {
+    uint16_t opt[MAXK];
+    int16_t oc[MAXK];
+    uint8_t ph[MAXK];
+    uint16_t nb[MAXK + 1];
+    int used[MAXK + 1];
+    uint16_t bsz[WALK_SLOTS];
+    uint16_t bmk[WALK_SLOTS];
+    uint16_t x[WALK_SLOTS];
+    uint16_t cap[WALK_SLOTS];
+    // scratch: stats of the child blocks / last-level contributions
+    int cu[MAXB];
+    double cm[MAXB], cs[MAXB], cb[MAXB];
+};
+
+#ifdef MG_DEVICE_CODE
+MG_HD double envelope(const Spec& S, int j, double P) {
+    double g = POS_INF;
+    for (int i = 0; i < S.env_n[j]; ++i) {
+        double v = S.env_a[j][i] + S.env_b[j][i] * P;
+        g = v < g ? v : g;
+    }
+    return S.env_n[j] ? g : 0.0;
+}
+
+// Exact contribution of one GPU block with resident levels `mask` (all k options set):
+// max over residents m of base_m + delta(residents), module-index order sums.
+MG_HD double contrib(const Spec& S, const Rows& R, const uint16_t* opt, unsigned mask) {
+    if (!mask) return NEG_INF;
+    if (S.include_self) {
+        double s = 0.0, p = 1.0, mb = NEG_INF;
+        for (int pos = 0; pos < S.k; ++pos) {
+            int l = S.pos_lvl[pos];
+            if (!(mask >> l & 1u)) continue;
+            int r = S.lvl_off[l] + opt[l];
+            double b = R.B[r];
+            s = s + b;
+            p = p * b;
+            double ba = R.base[r];
+            mb = ba > mb ? ba : mb;
+        }
+        double dl = S.e1 + S.e2 * s;
+        dl = dl + (S.additive ? 0.0 : S.e3 * p);
+        return mb + dl;
+    }
+    double best = NEG_INF;
+    for (int pos = 0; pos < S.k; ++pos) {
+        int l = S.pos_lvl[pos];
+        if (!(mask >> l & 1u)) continue;
+        double s = 0.0, p = 1.0;
+        int n = 0;
+        for (int pos2 = 0; pos2 < S.k; ++pos2) {
+            int l2 = S.pos_lvl[pos2];
+            if (l2 == l || !(mask >> l2 & 1u)) continue;
+            double b = R.B[S.lvl_off[l2] + opt[l2]];
+            s = s + b;
+            p = p * b;
+            ++n;
+        }
+        if (n == 0) p = 0.0;
+        double dl = S.e1 + S.e2 * s;
+        dl = dl + (S.additive ? 0.0 : S.e3 * p);
+        double v = R.base[S.lvl_off[l] + opt[l]] + dl;
+        best = v > best ? v : best;
+    }
+    return best;
+}
+
+// 0 accept, 1 skip, 2 stop the option loop (all later options fail too).
+MG_HD int opt_test(const Spec& S, const Rows& R, int r, double thr) {
+    double base = R.base[r];
+    if (S.use_filter && R.bound[r] > S.theta) {
+        if (S.nonneg && base + S.e1 > S.theta) return 2;
+        if (!S.nonneg && base > S.theta) return 2;
+        return 1;
+    }
+    if (S.nonneg) {
+        double be = base + S.e1;
+        if (be > thr) return 2;
+        double lb = S.include_self ? be + S.e2 * R.B[r] : be;
+        if (lb > thr) return 1;
+    }
+    return 0;
+}
+
+// Stats of a block (levels < nlev in `mask`), accumulated in placement order like
+// FeasibilitySearch::push_module (stage_eval.hpp:224-229).
+MG_HD void block_stats(const Spec& S, const Rows& R, const uint16_t* opt, unsigned mask,
+                       int nlev, int& units, double& mem, double& sum, double& mb,
+                       double& P, double& mbx) {
+    units = 0;
+    mem = 0.0;
+    sum = 0.0;
+    mb = NEG_INF;
+    P = 1.0;
+    mbx = NEG_INF;  // max(base - e2*B): residents' own-excluded additive bound
+    for (int l = 0; l < nlev; ++l) {
+        if (!(mask >> l & 1u)) continue;
+        int r = S.lvl_off[l] + opt[l];
+        units += R.u[r];
+        mem = mem + R.fp[r];
+        sum = sum + R.B[r];
+        P = P * R.B[r];
+        double ba = R.base[r];
+        mb = ba > mb ? ba : mb;
+        double bx = ba - S.e2 * R.B[r];
+        mbx = bx > mbx ? bx : mbx;
+    }
+}
+
+// First composition in descending lexicographic order.
+MG_HD bool first_comp(const uint16_t* cap, uint16_t* x, int nb, int d) {
+    int rem = d;
+    for (int b = 0; b < nb; ++b) {
+        int t = cap[b] < rem ? cap[b] : rem;
+        x[b] = (uint16_t)t;
+        rem -= t;
+    }
+    return rem == 0;
+}
+
+MG_HD bool next_comp(const uint16_t* cap, uint16_t* x, int nb) {
+    int acc = nb ? x[nb - 1] : 0;
+    int suff = nb ? cap[nb - 1] : 0;
+    int i = nb - 2;
+    for (; i >= 0; --i) {
+        if (x[i] > 0 && suff >= acc + 1) break;
+        acc += x[i];
+        suff += cap[i];
+    }
+    if (i < 0) return false;
+    x[i] -= 1;
+    int R = acc + 1;
+    for (int b = i + 1; b < nb; ++b) {
+        int t = cap[b] < R ? cap[b] : R;
+        x[b] = (uint16_t)t;
+        R -= t;
+    }
+    return true;
+}
+
+// Admissible take-count interval of every block at the last level for threshold t
+// (le: contribution <= t, else < t).  Returns false if some block has none or the
+// degree is unreachable.
+MG_HD bool last_intervals(const Walk& w, int o0, int nb, int d, double t, bool le,
+                          const double* rest, const double* take, int& sumlo, int& sumhi) {
+    sumlo = 0;
+    sumhi = 0;
+    for (int b = 0; b < nb; ++b) {
+        int s = w.bsz[o0 + b];
+        bool rok = le ? rest[b] <= t : rest[b] < t;
+        bool tok = w.cap[o0 + b] && (le ? take[b] <= t : take[b] < t);
+        if (rok && tok) {
+            sumhi += s;
+        } else if (rok) {
+        } else if (tok) {
+            sumlo += s;
+            sumhi += s;
+        } else {
+            return false;
+        }
+    }
+    return sumlo <= d && d <= sumhi;
+}
+
+// The per-thread DFS.  Starts at depth d0 (w holds opt[<d0], blocks of level d0);
+// stop < k: emit every surviving node of depth `stop` (frontier expansion);
+// stop == k: run to the leaves.  Returns 1 on a FIRST hit, 2 on abort, 0 when done.
+template <class H>
+MG_HD int dfs(const Spec& S, const Rows& R, Walk& w, int d0, int stop, H& h) {
+    const int k = S.k;
+    const int GL = S.G * S.L;
+    int j = d0;
+    w.ph[j] = 0;
+    w.oc[j] = -1;
+    while (j >= d0) {
+        const int o0 = lvl_off(j);
+        const int nb = w.nb[j];
+        if (w.ph[j] == 0) {
+            if (h.abort()) return 2;
+            const double thr = h.thr(S);
+            const int n = S.lvl_n[j], off = S.lvl_off[j];
+            int o = w.oc[j] + 1;
+            bool got = false;
+            for (; o < n; ++o) {
+                int r = off + o;
+                int t = opt_test(S, R, r, thr);
+                if (t == 2) break;
+                if (t == 1) continue;
+                if (w.used[j] + R.d[r] * R.u[r] + S.suffix_min[j + 1] > GL) continue;
+                got = true;
+                break;
+            }
+            if (!got) {
+                --j;
+                continue;
+            }
+            w.oc[j] = (int16_t)o;
+            w.opt[j] = (uint16_t)o;
+            const int r = off + o;
+            const int dd = R.d[r], uu = R.u[r];
+            const double ff = R.fp[r];
+            int tot = 0;
+            for (int b = 0; b < nb; ++b) {
+                int units;
+                double mem, sum, mb, P, mbx;
+                block_stats(S, R, w.opt, w.bmk[o0 + b], j, units, mem, sum, mb, P, mbx);
+                bool el = units + uu <= S.L && !(mem + ff > S.cap_slack);
+                w.cap[o0 + b] = el ? w.bsz[o0 + b] : 0;
+                tot += w.cap[o0 + b];
+            }
+            if (tot < dd) continue;
+            if (j == k - 1) {
+                // ---- last level: closed form over blocks ----
+                h.count_leaf();
+                double* rest = w.cs;
+                double* take = w.cb;
+                for (int b = 0; b < nb; ++b) {
+                    unsigned m = w.bmk[o0 + b];
+                    rest[b] = contrib(S, R, w.opt, m);
+                    take[b] = w.cap[o0 + b] ? contrib(S, R, w.opt, m | (1u << j)) : POS_INF;
+                }
+                if (S.mode == MODE_FIRST) {
+                    int lo, hi;
+                    if (!(0.0 <= S.theta)) continue;
+                    if (!last_intervals(w, o0, nb, dd, S.theta, true, rest, take, lo, hi)) continue;
+                    // greedy first composition (descending lexicographic)
+                    int rem = dd - lo;
+                    for (int b = 0; b < nb; ++b) {
+                        int s = w.bsz[o0 + b];
+                        bool rok = rest[b] <= S.theta;
+                        bool tok = w.cap[o0 + b] && take[b] <= S.theta;
+                        int l = (!rok) ? s : 0;
+                        int hgh = tok ? s : 0;
+                        int e = hgh - l < rem ? hgh - l : rem;
+                        w.x[o0 + b] = (uint16_t)(l + e);
+                        rem -= e;
+                    }
+                    double v = 0.0;
+                    for (int b = 0; b < nb; ++b) {
+                        int xb = w.x[o0 + b], s = w.bsz[o0 + b];
+                        if (xb > 0 && take[b] > v) v = take[b];
+                        if (xb < s && rest[b] > v) v = rest[b];
+                    }
+                    h.hit(w, j, v);
+                    return 1;
+                } else {
+                    double I = h.incumbent();
+                    int lo, hi;
+                    if (!last_intervals(w, o0, nb, dd, I, false, rest, take, lo, hi)) continue;
+                    double hiv = I;
+                    while (true) {
+                        double c = NEG_INF;
+                        for (int b = 0; b < nb; ++b) {
+                            if (rest[b] < hiv && rest[b] > c) c = rest[b];
+                            if (w.cap[o0 + b] && take[b] < hiv && take[b] > c) c = take[b];
+                        }
+                        if (c <= NEG_INF) break;
+                        if (last_intervals(w, o0, nb, dd, c, true, rest, take, lo, hi)) {
+                            hiv = c;
+                        } else {
+                            break;
+                        }
+                    }
+                    double v = hiv > 0.0 ? hiv : 0.0;
+                    if (v < I) h.improve(v);
+                }
+                continue;
+            }
+            if (!first_comp(w.cap + o0, w.x + o0, nb, dd)) continue;
+            w.ph[j] = 1;
+        } else {
+            if (!next_comp(w.cap + o0, w.x + o0, nb)) {
+                w.ph[j] = 0;
+                continue;
+            }
+        }
+        // ---- build the child (level j+1 blocks) and prune ----
+        h.count_node();
+        const int o1 = lvl_off(j + 1);
+        const int c1 = lvl_cap(j + 1);
+        const int r = S.lvl_off[j] + w.opt[j];
+        int m = 0;
+        bool overflow = false;
+        for (int b = 0; b < nb; ++b) {
+            int xb = w.x[o0 + b], s = w.bsz[o0 + b];
+            unsigned mk = w.bmk[o0 + b];
+            if (xb > 0) {
+                if (m >= c1) { overflow = true; break; }
+                w.bsz[o1 + m] = (uint16_t)xb;
+                w.bmk[o1 + m] = (uint16_t)(mk | (1u << j));
+                ++m;
+            }
+            if (xb < s) {
+                if (m >= c1) { overflow = true; break; }
+                w.bsz[o1 + m] = (uint16_t)(s - xb);
+                w.bmk[o1 + m] = (uint16_t)mk;
+                ++m;
+            }
+        }
+        if (overflow) {
+            h.overflow();
+            return 2;
+        }
+        w.nb[j + 1] = (uint16_t)m;
+        w.used[j + 1] = w.used[j] + R.d[r] * R.u[r];
+        bool prune = false;
+        const double thr = h.thr(S);
+        if (S.nonneg) {
+            for (int b = 0; b < m && !prune; ++b) {
+                int units;
+                double mem, sum, mb, P, mbx;
+                block_stats(S, R, w.opt, w.bmk[o1 + b], j + 1, units, mem, sum, mb, P, mbx);
+                w.cu[b] = units;
+                w.cm[b] = mem;
+                w.cs[b] = sum;
+                w.cb[b] = mb;
+                if (!w.bmk[o1 + b]) continue;
+                double lb;
+                if (S.include_self) {
+                    lb = mb + S.e1 + S.e2 * sum + envelope(S, j + 1, P);
+                } else {
+                    lb = mbx + S.e1 + S.e2 * sum + envelope(S, j + 1, 0.0);
+                }
+                if (lb > thr) prune = true;
+            }
+        } else {
+            for (int b = 0; b < m; ++b) {
+                int units;
+                double mem, sum, mb, P, mbx;
+                block_stats(S, R, w.opt, w.bmk[o1 + b], j + 1, units, mem, sum, mb, P, mbx);
+                w.cu[b] = units;
+                w.cm[b] = mem;
+                w.cs[b] = sum;
+                w.cb[b] = mb;
+            }
+        }
+        // look-ahead: every unplaced level keeps an option that fits somewhere
+        for (int l = j + 1; l < k && !prune; ++l) {
+            const int n = S.lvl_n[l], off = S.lvl_off[l];
+            bool ok = false;
+            for (int o = 0; o < n && !ok; ++o) {
+                int rr = off + o;
+                int t = opt_test(S, R, rr, thr);
+                if (t == 2) break;
+                if (t == 1) continue;
+                const int dd = R.d[rr], uu = R.u[rr];
+                const double ff = R.fp[rr], bb = R.B[rr], ba = R.base[rr];
+                int cnt = 0;
+                for (int b = 0; b < m; ++b) {
+                    if (w.cu[b] + uu > S.L) continue;
+                    if (w.cm[b] + ff > S.cap_slack) continue;
+                    if (S.nonneg && S.include_self) {
+                        double mb = w.cb[b] > ba ? w.cb[b] : ba;
+                        if (mb + S.e1 + S.e2 * (w.cs[b] + bb) > thr) continue;
+                    }
+                    cnt += w.bsz[o1 + b];
+                    if (cnt >= dd) break;
+                }
+                ok = cnt >= dd;
+            }
+            if (!ok) prune = true;
+        }
+        if (prune) continue;
+        if (j + 1 == stop) {
+            h.emit(w, j + 1);
+            continue;
+        }
+        ++j;
+        w.ph[j] = 0;
+        w.oc[j] = -1;
+    }
+    return 0;
+}
+
+// Load a frontier node into a walk.
+MG_HD void load_node(const Node& nd, Walk& w) {
+    int dep = nd.depth;
+    for (int l = 0; l < dep; ++l) w.opt[l] = nd.opt[l];
+    int o = lvl_off(dep);
+    w.nb[dep] = nd.nb;
+    for (int b = 0; b < nd.nb; ++b) {
+        w.bsz[o + b] = nd.bsz[b];
+        w.bmk[o + b] = nd.bmk[b];
+    }
+}
+
+MG_HD void store_node(const Walk& w, int dep, Node& nd) {
+    for (int l = 0; l < MAXK; ++l) nd.opt[l] = l < dep ? w.opt[l] : 0;
+    nd.depth = (uint16_t)dep;
+    int o = lvl_off(dep);
+    nd.nb = w.nb[dep];
+    for (int b = 0; b < nd.nb; ++b) {
+        nd.bsz[b] = w.bsz[o + b];
+        nd.bmk[b] = w.bmk[o + b];
+    }
+}
+
+// Write the FIRST leaf: options and the final block list after the last level.
+MG_HD void store_leaf(const Walk& w, int j, double v, Leaf& lf) {
+    lf.value = v;
+    for (int l = 0; l <= j; ++l) lf.opt[l] = w.opt[l];
+    int o0 = lvl_off(j);
+    int m = 0;
+    for (int b = 0; b < w.nb[j]; ++b) {
+        int xb = w.x[o0 + b], s = w.bsz[o0 + b];
+        unsigned mk = w.bmk[o0 + b];
+        if (xb > 0) {
+            lf.bsz[m] = (uint16_t)xb;
+            lf.bmk[m] = (uint16_t)(mk | (1u << j));
+            ++m;
+        }
+        if (xb < s) {
+            lf.bsz[m] = (uint16_t)(s - xb);
+            lf.bmk[m] = (uint16_t)mk;
+            ++m;
+        }
+    }
+    lf.nb = m;
+}
+
+#endif  // MG_DEVICE_CODE
+
+}  // namespace mg

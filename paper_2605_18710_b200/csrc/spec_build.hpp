@@ -1,0 +1,171 @@
+// spec_build.hpp — host side: turn one stage search request into the device Spec.
+//
+// The option rows of every module live in one device table in candidate_options
+// order (stage_eval.hpp:68-93).  A level's list is a PREFIX of its module's rows:
+// rows are sorted by base latency, and once base+e1 exceeds the threshold no later
+// row can pass (stage_eval.hpp:122-127 filter / oracle.hpp:130-135 bound), so the
+// prefix is all the device ever needs to scan.
+#pragma once
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <vector>
+
+#include "search_core.cuh"
+
+namespace mg {
+
+struct OptRow {
+    int d, u;
+    double base, B, fp, bound;
+};
+
+struct Model {
+    int G = 1, L = 10;
+    double cap = 80e9, e1 = 0, e2 = 0, e3 = 0;
+    bool additive = false, include_self = true;
+    bool nonneg() const { return e1 >= 0 && e2 >= 0 && (additive || e3 >= 0); }
+    std::vector<std::vector<OptRow>> rows;  // per module, candidate_options order
+    std::vector<int> row_off;               // per module offset into the flat table
+};
+
+// Filter bound exactly as FeasibilitySearch::run computes it (stage_eval.hpp:122-127).
+inline double filter_bound(const Model& M, double base, double B) {
+    double bound = base;
+    if (M.nonneg()) {
+        bound += M.e1;
+        if (M.include_self) bound += M.e2 * B;
+    }
+    return bound;
+}
+
+struct SearchReq {
+    int mode = MODE_FIRST;
+    bool use_filter = false;
+    double theta = POS_INF;  // FIRST acceptance threshold
+    double ub = POS_INF;     // MIN: incumbent upper bound (an achieved value or +inf)
+    std::vector<int> level_module;  // level -> module index (pi)
+};
+
+// Returns false if some level has no usable row (then no leaf can exist).
+inline bool build_spec(const Model& M, const SearchReq& q, Spec& S) {
+    const int k = (int)q.level_module.size();
+    S = Spec{};
+    S.k = k;
+    S.G = M.G;
+    S.L = M.L;
+    S.mode = q.mode;
+    S.nonneg = M.nonneg();
+    S.include_self = M.include_self;
+    S.additive = M.additive;
+    S.use_filter = q.use_filter;
+    S.e1 = M.e1;
+    S.e2 = M.e2;
+    S.e3 = M.e3;
+    S.cap_slack = M.cap * (1.0 + 1e-12);
+    S.theta = q.theta;
+    double t = q.mode == MODE_MIN ? q.ub : q.theta;
+    S.thp = t >= POS_INF ? POS_INF : t * (1.0 + 1e-12);
+    // module-index position -> level
+    std::vector<std::pair<int, int>> ml;
+    for (int l = 0; l < k; ++l) ml.push_back({q.level_module[l], l});
+    std::sort(ml.begin(), ml.end());
+    for (int p = 0; p < k; ++p) S.pos_lvl[p] = ml[p].second;
+
+    std::vector<double> bmin(k, 1.0);
+    std::vector<int> forced(k, 1), dmin(k, 0);
+    for (int l = 0; l < k; ++l) {
+        const int m = q.level_module[l];
+        const auto& rows = M.rows[m];
+        S.lvl_off[l] = M.row_off[m];
+        int n = 0, best_dem = INT32_MAX;
+        double bm = POS_INF;
+        bool all_full = true;
+        for (int i = 0; i < (int)rows.size(); ++i) {
+            const OptRow& r = rows[i];
+            // the same tests opt_test applies on the device, with the static threshold
+            bool stop = false, skip = false;
+            if (q.use_filter && r.bound > q.theta) {
+                if (S.nonneg ? (r.base + M.e1 > q.theta) : (r.base > q.theta)) stop = true;
+                skip = true;
+            } else if (S.nonneg) {
+                double be = r.base + M.e1;
+                if (be > S.thp) stop = true;
+                double lb = M.include_self ? be + M.e2 * r.B : be;
+                if (lb > S.thp) skip = true;
+            }
+            if (stop) break;
+            n = i + 1;
+            if (skip) continue;
+            best_dem = std::min(best_dem, r.d * r.u);
+            bm = std::min(bm, r.B);
+            if (r.d != M.G) all_full = false;
+        }
+        S.lvl_n[l] = n;
+        if (best_dem == INT32_MAX) return false;
+        dmin[l] = best_dem;
+        bmin[l] = std::min(1.0, std::max(0.0, bm));
+        forced[l] = all_full ? 1 : 0;
+    }
+    S.suffix_min[k] = 0;
+    for (int l = k - 1; l >= 0; --l) S.suffix_min[l] = S.suffix_min[l + 1] + dmin[l];
+
+    // Product-term envelope g_j(P) = min over subsets T of unplaced levels >= j that
+    // contain every forced level of  e2*sum_T Bmin + e3*P*prod_T Bmin.
+    const double e3 = S.additive ? 0.0 : M.e3;
+    for (int j = 0; j <= k; ++j) {
+        const int nf = k - j;
+        std::vector<std::pair<double, double>> lines;
+        if (nf <= 12) {
+            for (int T = 0; T < (1 << nf); ++T) {
+                bool ok = true;
+                double a = 0.0, b = e3;
+                for (int i = 0; i < nf; ++i) {
+                    if (T >> i & 1) {
+                        a += M.e2 * bmin[j + i];
+                        b *= bmin[j + i];
+                    } else if (forced[j + i]) {
+                        ok = false;
+                    }
+                }
+                if (ok) lines.push_back({a, b});
+            }
+        } else {
+            lines.push_back({0.0, 0.0});
+        }
+        // keep the lower envelope on P in [0, 1]
+        std::vector<std::pair<double, double>> keep;
+        for (size_t i = 0; i < lines.size(); ++i) {
+            bool dom = false;
+            for (size_t h = 0; h < lines.size() && !dom; ++h) {
+                if (h == i) continue;
+                bool le0 = lines[h].first <= lines[i].first;
+                bool le1 = lines[h].first + lines[h].second <= lines[i].first + lines[i].second;
+                bool strict = lines[h].first < lines[i].first ||
+                              lines[h].first + lines[h].second < lines[i].first + lines[i].second;
+                if (le0 && le1 && (strict || h < i)) dom = true;
+            }
+            if (!dom) keep.push_back(lines[i]);
+        }
+        if ((int)keep.size() > MAXENV) {
+            // conservative: fall back to the weakest bound (min over all lines at P)
+            double a = POS_INF, b = 0.0;
+            for (auto& l : keep) a = std::min(a, l.first);
+            keep.assign(1, {a, b});
+        }
+        S.env_n[j] = (int)keep.size();
+        // envelope is a lower bound: scale down by a hair so rounding cannot tighten it
+        for (int i = 0; i < S.env_n[j]; ++i) {
+            S.env_a[j][i] = keep[i].first * (1.0 - 1e-12);
+            S.env_b[j][i] = keep[i].second * (1.0 - 1e-12);
+        }
+        if (S.env_n[j] == 0) {
+            S.env_n[j] = 1;
+            S.env_a[j][0] = 0.0;
+            S.env_b[j][0] = 0.0;
+        }
+    }
+    return true;
+}
+
+}  // namespace mg

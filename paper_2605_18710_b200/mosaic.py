@@ -1,0 +1,549 @@
+"""Python mirror of the reference planner API over the C ABI (include/mosaic_gpu.h).
+
+The reference is header-only C++ (namespace mosaic); this module keeps its names,
+argument meaning and error behaviour so parity tests read like the reference's own
+doctest suites:
+
+    reference (C++)                                  here
+    stage_eval(ctx, cluster, modules, cfg)           stage_eval(planner, modules)
+    detail::ExactStageSolver(ctx, cluster, L).solve  exact_stage(planner, modules)
+    detail::FeasibilitySearch(...).run(tau)          feasibility_run(planner, modules, tau)
+    solve(ctx, cluster, cfg)                         solve(planner)
+    brute_force_optimum(ctx, cluster, L)             brute_force_optimum(planner)
+    stage_time / rectified_latency                   stage_time(planner, allocs)
+    candidate_options(ctx, cluster, m, L)            candidate_options(planner, m)
+    ScalingSurface::lookup                           planner.lookup(m, d, a)
+
+`Planner` plays the role of PerfContext + ClusterSpec + SolveConfig (one device
+context).  Every search runs in the CUDA library; if it is not built, importing
+fails loudly — there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmosaic_gpu.so")
+
+MAX_STAGE_MODULES = 12
+MAX_GPUS = 1024
+MAX_STAGES = 64
+
+OK, INFEASIBLE, MODULE_NO_OPTION, RANGE, TOO_LARGE, CUDA, EMPTY = range(7)
+
+
+class MosaicError(RuntimeError):
+    pass
+
+
+class StageInfeasibleError(MosaicError):
+    """stage_eval.hpp:26 — a module has no feasible deployment option."""
+
+
+class SurfaceRangeError(MosaicError):
+    """perf_model.hpp:46 — query outside the profiled hull / invalid input."""
+
+
+class OracleTooLargeError(MosaicError):
+    """oracle.hpp:24 — more than 8 modules, or a stage beyond kernel limits."""
+
+
+class EmptyPlanError(MosaicError):
+    """solver.hpp:25."""
+
+
+class DeviceError(MosaicError):
+    pass
+
+
+# ---------------------------------------------------------------------------
+# ctypes mirror of include/mosaic_gpu.h
+# ---------------------------------------------------------------------------
+class Point(C.Structure):
+    _fields_ = [("d", C.c_int32), ("a", C.c_double), ("latency", C.c_double),
+                ("bandwidth_util", C.c_double), ("memory", C.c_double), ("sm_active", C.c_double)]
+
+
+class ModuleC(C.Structure):
+    _fields_ = [("id", C.c_char_p), ("memory_base", C.c_double), ("points", C.POINTER(Point)),
+                ("n_points", C.c_int32)]
+
+
+class ProblemC(C.Structure):
+    _fields_ = [("modules", C.POINTER(ModuleC)), ("n_modules", C.c_int32),
+                ("edges", C.POINTER(C.c_int32)), ("n_edges", C.c_int32),
+                ("gpu_count", C.c_int32), ("memory_capacity", C.c_double),
+                ("e1", C.c_double), ("e2", C.c_double), ("e3", C.c_double),
+                ("additive_only", C.c_int32), ("include_self", C.c_int32),
+                ("quota_levels", C.c_int32), ("bisect_rel_tol", C.c_double),
+                ("enable_prune", C.c_int32), ("enable_cache", C.c_int32)]
+
+
+class EntryC(C.Structure):
+    _fields_ = [("module", C.c_int32), ("dp_degree", C.c_int32), ("quota_units", C.c_int32),
+                ("n_gpus", C.c_int32), ("gpus", C.c_int32 * MAX_GPUS)]
+
+
+class StageResultC(C.Structure):
+    _fields_ = [("status", C.c_int32), ("stage_time", C.c_double), ("n_entries", C.c_int32),
+                ("entries", EntryC * MAX_STAGE_MODULES), ("probes", C.c_int64),
+                ("gpu_searches", C.c_int64), ("nodes", C.c_int64), ("leaves", C.c_int64)]
+
+
+class EvalEntryC(C.Structure):
+    _fields_ = [("module", C.c_int32), ("dp_degree", C.c_int32), ("quota_units", C.c_int32),
+                ("n_gpus", C.c_int32), ("gpu_off", C.c_int64)]
+
+
+class PlanResultC(C.Structure):
+    _fields_ = [("status", C.c_int32), ("n_stages", C.c_int32),
+                ("stage_mask", C.c_uint64 * MAX_STAGES), ("stage_time", C.c_double * MAX_STAGES),
+                ("iteration_time", C.c_double), ("partitions_examined", C.c_int64),
+                ("rounds", C.c_int64), ("stage_eval_calls", C.c_int64),
+                ("feasibility_calls", C.c_int64), ("cache_hits", C.c_int64),
+                ("prunes", C.c_int64), ("gpu_searches", C.c_int64), ("nodes", C.c_int64),
+                ("leaves", C.c_int64), ("elapsed_s", C.c_double)]
+
+
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+
+# every symbol include/mosaic_gpu.h declares (checked by the CPU tests)
+EXPORTS = [
+    "mosaic_gpu_create", "mosaic_gpu_destroy", "mosaic_gpu_last_error",
+    "mosaic_gpu_num_options", "mosaic_gpu_options", "mosaic_gpu_lookup",
+    "mosaic_gpu_stage_time", "mosaic_gpu_stage_eval", "mosaic_gpu_exact_stage",
+    "mosaic_gpu_feasible", "mosaic_gpu_plan_stage", "mosaic_gpu_solve",
+    "mosaic_gpu_brute_force", "mosaic_gpu_trace_rounds", "mosaic_gpu_trace_round",
+    "mosaic_gpu_trace_cand", "mosaic_gpu_clear_cache", "mosaic_gpu_set_shard",
+    "mosaic_gpu_merge_records", "mosaic_gpu_launch_count", "mosaic_gpu_search_ms",
+    "mosaic_gpu_reset_counters", "mosaic_gpu_synth_problem", "mosaic_gpu_free_problem",
+]
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Load the CUDA library; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(path)
+    P = C.POINTER
+    vp = C.c_void_p
+    sig = {
+        "mosaic_gpu_create": (C.c_int, [P(ProblemC), C.c_int, P(vp)]),
+        "mosaic_gpu_destroy": (None, [vp]),
+        "mosaic_gpu_last_error": (C.c_char_p, []),
+        "mosaic_gpu_num_options": (C.c_int, [vp, C.c_int, P(C.c_int32)]),
+        "mosaic_gpu_options": (C.c_int, [vp, C.c_int, P(C.c_int32), P(C.c_int32), P(C.c_double),
+                                         P(C.c_double), P(C.c_double)]),
+        "mosaic_gpu_lookup": (C.c_int, [vp, C.c_int, C.c_int, C.c_double, P(C.c_double)]),
+        "mosaic_gpu_stage_time": (C.c_int, [vp, P(EvalEntryC), P(C.c_int32), P(C.c_int64),
+                                            C.c_int64, P(C.c_double), P(C.c_double)]),
+        "mosaic_gpu_stage_eval": (C.c_int, [vp, C.c_uint64, P(StageResultC)]),
+        "mosaic_gpu_exact_stage": (C.c_int, [vp, C.c_uint64, P(StageResultC)]),
+        "mosaic_gpu_feasible": (C.c_int, [vp, C.c_uint64, C.c_double, P(StageResultC)]),
+        "mosaic_gpu_plan_stage": (C.c_int, [vp, C.c_int, P(StageResultC)]),
+        "mosaic_gpu_solve": (C.c_int, [vp, P(PlanResultC)]),
+        "mosaic_gpu_brute_force": (C.c_int, [vp, P(PlanResultC)]),
+        "mosaic_gpu_trace_rounds": (C.c_int, [vp, P(C.c_int64)]),
+        "mosaic_gpu_trace_round": (C.c_int, [vp, C.c_int64, P(C.c_uint64), P(C.c_uint64),
+                                             P(C.c_double), P(C.c_int64)]),
+        "mosaic_gpu_trace_cand": (C.c_int, [vp, C.c_int64, C.c_int64, P(C.c_uint64),
+                                            P(C.c_uint64), P(C.c_int32), P(C.c_int32),
+                                            P(C.c_double)]),
+        "mosaic_gpu_clear_cache": (None, [vp]),
+        "mosaic_gpu_set_shard": (C.c_int, [vp, C.c_int, C.c_int, ALLGATHER_FN, vp]),
+        "mosaic_gpu_merge_records": (C.c_int, [vp, C.c_int, C.c_int, P(C.c_int)]),
+        "mosaic_gpu_launch_count": (C.c_int64, [vp]),
+        "mosaic_gpu_search_ms": (C.c_double, [vp]),
+        "mosaic_gpu_reset_counters": (None, [vp]),
+        "mosaic_gpu_synth_problem": (C.c_int, [C.c_char_p, C.c_int, P(P(ProblemC))]),
+        "mosaic_gpu_free_problem": (None, [P(ProblemC)]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _raise(code: int) -> None:
+    if code in (OK, INFEASIBLE):
+        return
+    msg = load_library().mosaic_gpu_last_error().decode()
+    exc = {MODULE_NO_OPTION: StageInfeasibleError, RANGE: SurfaceRangeError,
+           TOO_LARGE: OracleTooLargeError, EMPTY: EmptyPlanError}.get(code, DeviceError)
+    raise exc(msg or f"status {code}")
+
+
+# ---------------------------------------------------------------------------
+# result types (core.hpp:64-104, stage_eval.hpp:30-54, solver.hpp:106-131)
+# ---------------------------------------------------------------------------
+@dataclass
+class DeploymentOption:
+    dp_degree: int
+    quota_units: int
+    quota_levels: int
+
+    def quota(self) -> float:
+        return self.quota_units / self.quota_levels
+
+
+@dataclass
+class Entry:
+    module: int
+    option: DeploymentOption
+    gpus: list[int]
+
+
+@dataclass
+class StageAllocation:
+    entries: list[Entry] = field(default_factory=list)
+
+    def module_indices(self) -> list[int]:
+        return [e.module for e in self.entries]
+
+
+@dataclass
+class SolverStats:
+    feasibility_calls: int = 0
+    gpu_searches: int = 0
+    nodes: int = 0
+    leaves: int = 0
+
+
+@dataclass
+class StageEvalResult:
+    stage_time: float
+    allocation: StageAllocation
+    stats: SolverStats
+
+
+@dataclass
+class DeploymentPlan:
+    stages: list[StageAllocation] = field(default_factory=list)
+    predicted_stage_times: list[float] = field(default_factory=list)
+    predicted_iteration_time: float = 0.0
+
+
+@dataclass
+class TraceCandidate:
+    mask_x: int
+    mask_y: int
+    pruned: bool
+    cache_hit: bool
+    gain: float
+
+
+@dataclass
+class TraceRound:
+    candidates: list[TraceCandidate]
+    chosen_x: int
+    chosen_y: int
+    applied_gain: float
+
+
+@dataclass
+class SolveTrace:
+    rounds: list[TraceRound]
+    stage_eval_calls: int
+    feasibility_calls: int
+    cache_hits: int
+    prunes: int
+    gpu_searches: int
+    nodes: int
+    leaves: int
+    elapsed: float
+
+
+@dataclass
+class SolveResult:
+    plan: DeploymentPlan
+    trace: SolveTrace
+
+
+@dataclass
+class OracleResult:
+    plan: DeploymentPlan
+    iteration_time: float
+    partitions_examined: int
+
+
+@dataclass
+class CandidateOption:
+    opt: DeploymentOption
+    base_latency: float
+    solo_bandwidth: float
+    footprint: float
+
+
+# ---------------------------------------------------------------------------
+class Planner:
+    """One device context: PerfContext + ClusterSpec + SolveConfig of the reference."""
+
+    def __init__(self, problem: C.POINTER(ProblemC), device: int = 0, _owned=None):
+        L = load_library()
+        self._owned = _owned
+        self._ctx = C.c_void_p()
+        _raise(L.mosaic_gpu_create(problem, device, C.byref(self._ctx)))
+        p = problem.contents
+        self.n_modules = p.n_modules
+        self.gpu_count = p.gpu_count
+        self.quota_levels = p.quota_levels
+        self._keep = None
+
+    @classmethod
+    def from_spec(cls, spec: str, quota_levels: int = 0, device: int = 0,
+                  enable_prune: bool = True, enable_cache: bool = True) -> "Planner":
+        """Synthetic BASELINE inputs: 'cfg1'..'cfg5', 'random:SEED:N:G', 'preset:NAME:K:G'."""
+        L = load_library()
+        pp = C.POINTER(ProblemC)()
+        _raise(L.mosaic_gpu_synth_problem(spec.encode(), quota_levels, C.byref(pp)))
+        pp.contents.enable_prune = int(enable_prune)
+        pp.contents.enable_cache = int(enable_cache)
+        try:
+            return cls(pp, device, _owned=pp)
+        except Exception:
+            L.mosaic_gpu_free_problem(pp)
+            raise
+
+    @classmethod
+    def from_surfaces(cls, modules: Sequence[dict], edges: Sequence[tuple[int, int]],
+                      gpu_count: int, quota_levels: int = 10, memory_capacity: float = 80e9,
+                      e: tuple[float, float, float] = (0.4e-3, 1.2e-3, 0.8e-3),
+                      additive_only: bool = False, include_self: bool = True,
+                      bisect_rel_tol: float = 1e-3, enable_prune: bool = True,
+                      enable_cache: bool = True, device: int = 0) -> "Planner":
+        """modules: [{'id': str, 'memory_base': float, 'points': [(d,a,lat,bw,mem,sm), ...]}]"""
+        keep = []
+        mods = (ModuleC * max(1, len(modules)))()
+        for i, m in enumerate(modules):
+            pts = (Point * len(m["points"]))(*[Point(*p) for p in m["points"]])
+            idb = m["id"].encode()
+            keep += [pts, idb]
+            mods[i] = ModuleC(idb, m.get("memory_base", 0.0), pts, len(m["points"]))
+        flat = [x for uv in edges for x in uv]
+        ed = (C.c_int32 * max(1, len(flat)))(*flat)
+        prob = ProblemC(mods, len(modules), ed, len(edges), gpu_count, memory_capacity,
+                        e[0], e[1], e[2], int(additive_only), int(include_self), quota_levels,
+                        bisect_rel_tol, int(enable_prune), int(enable_cache))
+        keep += [mods, ed, prob]
+        pl = cls(C.pointer(prob), device)
+        pl._keep = keep
+        return pl
+
+    def close(self) -> None:
+        if self._ctx:
+            load_library().mosaic_gpu_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+        if self._owned is not None:
+            load_library().mosaic_gpu_free_problem(self._owned)
+            self._owned = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- helpers --------------------------------------------------------------
+    def _stage(self, r: StageResultC) -> StageEvalResult:
+        ents = []
+        for i in range(r.n_entries):
+            e = r.entries[i]
+            ents.append(Entry(e.module, DeploymentOption(e.dp_degree, e.quota_units,
+                                                         self.quota_levels),
+                              list(e.gpus[:e.n_gpus])))
+        return StageEvalResult(r.stage_time, StageAllocation(ents),
+                               SolverStats(r.probes, r.gpu_searches, r.nodes, r.leaves))
+
+    @staticmethod
+    def _mask(modules: Sequence[int]) -> int:
+        m = 0
+        for x in modules:
+            m |= 1 << int(x)
+        return m
+
+    # -- API -----------------------------------------------------------------
+    def lookup(self, module: int, d: int, a: float) -> tuple[float, float, float, float]:
+        out = (C.c_double * 4)()
+        _raise(load_library().mosaic_gpu_lookup(self._ctx, module, d, a, out))
+        return tuple(out)
+
+    def candidate_options(self, module: int) -> list[CandidateOption]:
+        L = load_library()
+        n = C.c_int32()
+        _raise(L.mosaic_gpu_num_options(self._ctx, module, C.byref(n)))
+        k = n.value
+        d = (C.c_int32 * max(1, k))()
+        u = (C.c_int32 * max(1, k))()
+        b = (C.c_double * max(1, k))()
+        bw = (C.c_double * max(1, k))()
+        fp = (C.c_double * max(1, k))()
+        _raise(L.mosaic_gpu_options(self._ctx, module, d, u, b, bw, fp))
+        return [CandidateOption(DeploymentOption(d[i], u[i], self.quota_levels), b[i], bw[i], fp[i])
+                for i in range(k)]
+
+    def stage_eval(self, modules: Sequence[int]) -> Optional[StageEvalResult]:
+        r = StageResultC()
+        code = load_library().mosaic_gpu_stage_eval(self._ctx, self._mask(modules), C.byref(r))
+        _raise(code)
+        if r.status == MODULE_NO_OPTION:
+            raise StageInfeasibleError("module has no feasible deployment option")
+        return self._stage(r) if r.status == OK else None
+
+    def exact_stage(self, modules: Sequence[int]) -> Optional[StageEvalResult]:
+        r = StageResultC()
+        _raise(load_library().mosaic_gpu_exact_stage(self._ctx, self._mask(modules), C.byref(r)))
+        return self._stage(r) if r.status == OK else None
+
+    def feasibility_run(self, modules: Sequence[int], tau: float) -> Optional[StageEvalResult]:
+        r = StageResultC()
+        _raise(load_library().mosaic_gpu_feasible(self._ctx, self._mask(modules), tau, C.byref(r)))
+        return self._stage(r) if r.status == OK else None
+
+    def _plan(self, pr: PlanResultC) -> DeploymentPlan:
+        L = load_library()
+        plan = DeploymentPlan()
+        for s in range(pr.n_stages):
+            r = StageResultC()
+            _raise(L.mosaic_gpu_plan_stage(self._ctx, s, C.byref(r)))
+            plan.stages.append(self._stage(r).allocation)
+            plan.predicted_stage_times.append(pr.stage_time[s])
+        plan.predicted_iteration_time = pr.iteration_time
+        return plan
+
+    def solve(self) -> SolveResult:
+        L = load_library()
+        pr = PlanResultC()
+        _raise(L.mosaic_gpu_solve(self._ctx, C.byref(pr)))
+        plan = self._plan(pr)
+        rounds = []
+        nr = C.c_int64()
+        L.mosaic_gpu_trace_rounds(self._ctx, C.byref(nr))
+        for r in range(nr.value):
+            cx, cy, g, nc = C.c_uint64(), C.c_uint64(), C.c_double(), C.c_int64()
+            _raise(L.mosaic_gpu_trace_round(self._ctx, r, C.byref(cx), C.byref(cy), C.byref(g),
+                                            C.byref(nc)))
+            cands = []
+            for c in range(nc.value):
+                mx, my, pru, hit, gain = (C.c_uint64(), C.c_uint64(), C.c_int32(), C.c_int32(),
+                                          C.c_double())
+                _raise(L.mosaic_gpu_trace_cand(self._ctx, r, c, C.byref(mx), C.byref(my),
+                                               C.byref(pru), C.byref(hit), C.byref(gain)))
+                cands.append(TraceCandidate(mx.value, my.value, bool(pru.value), bool(hit.value),
+                                            gain.value))
+            rounds.append(TraceRound(cands, cx.value, cy.value, g.value))
+        tr = SolveTrace(rounds, pr.stage_eval_calls, pr.feasibility_calls, pr.cache_hits,
+                        pr.prunes, pr.gpu_searches, pr.nodes, pr.leaves, pr.elapsed_s)
+        return SolveResult(plan, tr)
+
+    def brute_force_optimum(self) -> Optional[OracleResult]:
+        pr = PlanResultC()
+        code = load_library().mosaic_gpu_brute_force(self._ctx, C.byref(pr))
+        _raise(code)
+        if pr.status != OK:
+            return None
+        return OracleResult(self._plan(pr), pr.iteration_time, pr.partitions_examined)
+
+    def stage_time(self, allocs: Sequence[StageAllocation],
+                   with_rectified: bool = False):
+        """Batched stage_time (and per-entry rectified_latency) on the device."""
+        ents, gpus, off = [], [], [0]
+        for a in allocs:
+            for e in a.entries:
+                ents.append(EvalEntryC(e.module, e.option.dp_degree, e.option.quota_units,
+                                       len(e.gpus), len(gpus)))
+                gpus.extend(e.gpus)
+            off.append(len(ents))
+        n = len(allocs)
+        E = (EvalEntryC * max(1, len(ents)))(*ents)
+        G = (C.c_int32 * max(1, len(gpus)))(*gpus)
+        O = (C.c_int64 * len(off))(*off)
+        st = (C.c_double * max(1, n))()
+        rect = (C.c_double * max(1, len(ents)))()
+        _raise(load_library().mosaic_gpu_stage_time(self._ctx, E, G, O, n, st, rect))
+        if with_rectified:
+            return list(st[:n]), [list(rect[off[i]:off[i + 1]]) for i in range(n)]
+        return list(st[:n])
+
+    def launch_count(self) -> int:
+        return load_library().mosaic_gpu_launch_count(self._ctx)
+
+    def device_ms(self) -> float:
+        return load_library().mosaic_gpu_search_ms(self._ctx)
+
+    def reset_counters(self) -> None:
+        load_library().mosaic_gpu_reset_counters(self._ctx)
+
+    def clear_cache(self) -> None:
+        load_library().mosaic_gpu_clear_cache(self._ctx)
+
+    def set_shard(self, rank: int, world: int, allgather=None) -> None:
+        """allgather(send: bytes) -> list[bytes] over ranks (torch.distributed in bench.py)."""
+        if world <= 1:
+            _raise(load_library().mosaic_gpu_set_shard(self._ctx, 0, 1, ALLGATHER_FN(), None))
+            return
+
+        def _cb(user, send, recv, nbytes):
+            try:
+                parts = allgather(C.string_at(send, nbytes))
+                C.memmove(recv, b"".join(parts), nbytes * world)
+                return 0
+            except Exception:
+                return 1
+
+        self._ag = ALLGATHER_FN(_cb)
+        _raise(load_library().mosaic_gpu_set_shard(self._ctx, rank, world, self._ag, None))
+
+
+# module-level spellings of the reference entry points
+def stage_eval(planner: Planner, modules: Sequence[int]) -> Optional[StageEvalResult]:
+    return planner.stage_eval(modules)
+
+
+def exact_stage(planner: Planner, modules: Sequence[int]) -> Optional[StageEvalResult]:
+    return planner.exact_stage(modules)
+
+
+def feasibility_run(planner: Planner, modules: Sequence[int], tau: float):
+    return planner.feasibility_run(modules, tau)
+
+
+def solve(planner: Planner) -> SolveResult:
+    return planner.solve()
+
+
+def brute_force_optimum(planner: Planner) -> Optional[OracleResult]:
+    return planner.brute_force_optimum()
+
+
+def stage_time(planner: Planner, allocation: StageAllocation) -> float:
+    return planner.stage_time([allocation])[0]
+
+
+def rectified_latency(planner: Planner, allocation: StageAllocation, module: int) -> float:
+    _, rect = planner.stage_time([allocation], with_rectified=True)
+    for e, r in zip(allocation.entries, rect[0]):
+        if e.module == module:
+            return r
+    raise ValueError("module not in stage")
+
+
+def candidate_options(planner: Planner, module: int) -> list[CandidateOption]:
+    return planner.candidate_options(module)
+
+
+def merge_records(records: bytes, world: int, mode: int) -> int:
+    """Winner index among per-rank 16-byte {u64 key, f64 value} records."""
+    w = C.c_int()
+    buf = C.create_string_buffer(records, len(records))
+    _raise(load_library().mosaic_gpu_merge_records(buf, world, mode, C.byref(w)))
+    return w.value

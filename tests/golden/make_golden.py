@@ -1,0 +1,167 @@
+"""Generate the golden fixtures under tests/golden/ from the REAL reference.
+
+Runs oracle/_ref/ref_driver (the unmodified reference headers compiled in place by
+oracle/Makefile) and records its outputs.  Run here, where /root/reference exists:
+
+    make -C oracle ref && python tests/golden/make_golden.py
+
+The fixtures travel with the repo; nothing at test time reads /root/reference.
+"""
+from __future__ import annotations
+
+import itertools
+import json
+import os
+import random
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+
+
+def ref(*args: str, timeout: float = 600) -> dict:
+    out = subprocess.run([DRIVER, *args], capture_output=True, text=True, timeout=timeout)
+    if out.returncode not in (0, 3):
+        raise RuntimeError(f"{args}: {out.stderr}")
+    d = json.loads(out.stdout)
+    d.pop("times", None)
+    d["args"] = list(args)
+    return d
+
+
+def dump(name: str, obj) -> None:
+    path = os.path.join(HERE, name)
+    with open(path, "w") as f:
+        json.dump(obj, f, separators=(",", ":"))
+    print(f"wrote {path} ({os.path.getsize(path)} bytes)", flush=True)
+
+
+def configs() -> None:
+    out = {}
+    for c in ["cfg1", "cfg2", "cfg3", "cfg4"]:
+        out[c] = {"solve": ref(c, "solve"), "options": ref(c, "options")}
+        out[c]["solve_noprune_nocache"] = ref(c, "solve", "noprune", "nocache")
+    out["cfg1"]["oracle"] = ref("cfg1", "oracle")
+    out["cfg2"]["oracle"] = ref("cfg2", "oracle")
+    out["cfg5"] = {"options": ref("cfg5", "options")}
+    dump("configs.json", out)
+
+
+def cfg5_stages() -> None:
+    """Per-mask stage_eval parity on cfg5 for every mask the CPU finishes quickly."""
+    out = []
+    enc = list(range(7))
+    for k in (1, 2, 3):
+        for c in itertools.combinations(enc, k):
+            mask = sum(1 << i for i in c)
+            out.append(ref("cfg5", "stage", str(mask)))
+    out.append(ref("cfg5", "stage", str(1 << 7)))  # backbone alone
+    for mask in (15, 0b1010101, 0b1110000):
+        out.append(ref("cfg5", "stage", str(mask), timeout=1200))
+    feas = []
+    for mask in (7, 15):
+        for tau in ("0.0851", "0.0852", "0.0896", "0.09", "0.1", "0.2"):
+            feas.append(ref("cfg5", "feas", str(mask), tau))
+    dump("cfg5_stages.json", {"stage": out, "feas": feas})
+
+
+def random_sets() -> None:
+    # acceptance.cpp:94-120 (C2): stage_eval vs exhaustive at L=2
+    c2 = []
+    for seed in range(1, 201):
+        n = 1 + seed % 3
+        g = 2 if n >= 2 else 1
+        inst = f"random:{seed}:{n}:{g}"
+        mask = str((1 << n) - 1)
+        c2.append({"stage": ref(inst, "stage", mask, "levels=2"),
+                   "exact": ref(inst, "exact", mask, "levels=2")})
+    # test_stage_eval.cpp:113-127: 60 seeds, 3 modules, 2 GPUs, L=4
+    se = []
+    for seed in range(1, 61):
+        inst = f"random:{seed}:3:2"
+        se.append({"stage": ref(inst, "stage", "7", "levels=4"),
+                   "exact": ref(inst, "exact", "7", "levels=4")})
+    # acceptance.cpp:57-90 (C1): solve vs oracle, 4 GPUs, L=4
+    c1 = []
+    for seed in range(1, 101):
+        n = 2 + seed % 3
+        inst = f"random:{seed}:{n}:4"
+        c1.append({"solve": ref(inst, "solve", "levels=4"),
+                   "oracle": ref(inst, "oracle", "levels=4")})
+    c1b = []
+    for seed in range(1, 21):
+        inst = f"random:{seed}:6:4"
+        c1b.append({"solve": ref(inst, "solve", "levels=4"),
+                    "oracle": ref(inst, "oracle", "levels=4")})
+    # larger random stages (G=8..32, L=10) for exact/stage parity
+    big = []
+    for seed in range(1, 41):
+        n = 2 + seed % 3
+        g = [8, 16, 32][seed % 3]
+        inst = f"random:{seed}:{n}:{g}"
+        mask = str((1 << n) - 1)
+        big.append({"stage": ref(inst, "stage", mask),
+                    "exact": ref(inst, "exact", mask) if n <= 3 and g <= 8 else None})
+    dump("random_sets.json", {"c2": c2, "stage_eval_60": se, "c1": c1, "c1_6mod": c1b,
+                              "big": big})
+
+
+def presets() -> None:
+    # acceptance.cpp:171-198 (C5): all presets at 8 GPUs, with and without prune+cache
+    out = []
+    for name, count in [("clip", 3), ("qwen3vl", 3), ("unifiedio2", 4), ("imagebind", 7),
+                        ("ofasys", 10)]:
+        inst = f"preset:{name}:{count}:8"
+        out.append({"solve": ref(inst, "solve"),
+                    "solve_noprune_nocache": ref(inst, "solve", "noprune", "nocache")})
+    # ofasys-8 at G=32, L=32: cfg5 shape at a CPU-finishable size
+    out.append({"solve": ref("preset:ofasys:8:32", "solve", "levels=32", timeout=1800)})
+    dump("presets.json", out)
+
+
+def variants() -> None:
+    """Model variants the reference tests exercise: include_self=false, additive-only,
+    negative coefficients, tight memory, infeasible modules."""
+    out = []
+    for seed in range(1, 16):
+        inst = f"random:{seed}:3:4"
+        for extra in (["noself"], ["additive"], ["e=0.4e-3,1.2e-3,0"],
+                      ["e=1e-3,-2e-4,5e-4"], ["mem=20e9"], ["mem=6e9"]):
+            row = {"extra": extra,
+                   "stage": ref(inst, "stage", "7", "levels=4", *extra),
+                   "exact": ref(inst, "exact", "7", "levels=4", *extra),
+                   "solve": ref(inst, "solve", "levels=4", *extra)}
+            out.append(row)
+    dump("variants.json", out)
+
+
+def stime() -> None:
+    """K1 evaluator parity: random explicit allocations scored by the reference."""
+    rng = random.Random(12345)
+    out = []
+    for inst, n, g, L in [("cfg4", 6, 64, 10), ("cfg5", 8, 128, 32), ("random:7:5:16", 5, 16, 10),
+                          ("random:11:4:8", 4, 8, 10)]:
+        opts = ref(inst, "options")["modules"]
+        for t in range(60):
+            k = rng.randint(1, n)
+            mods = sorted(rng.sample(range(n), k))
+            ents = []
+            for m in mods:
+                rows = opts[m]["rows"]
+                d, u = rows[rng.randrange(len(rows))][:2]
+                gp = sorted(rng.sample(range(g), d))
+                ents.append((m, d, u, gp))
+            spec = ";".join(f"{m}:{d}:{u}:{'.'.join(map(str, gp))}" for m, d, u, gp in ents)
+            for extra in ([], ["noself"], ["additive"]):
+                r = ref(inst, "stime", spec, *extra)
+                out.append({"inst": inst, "extra": extra, "entries": ents, "t": r["t"]})
+    dump("stime.json", out)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["configs", "cfg5_stages", "random_sets", "presets", "variants",
+                             "stime"]
+    for w in which:
+        globals()[w]()
