@@ -184,6 +184,17 @@ int64_t mosaic_gpu_launch_count(mosaic_gpu_ctx* ctx);
 /* Device time (ms) spent in the search kernels, by CUDA events on the ctx stream. */
 double mosaic_gpu_search_ms(mosaic_gpu_ctx* ctx);
 void mosaic_gpu_reset_counters(mosaic_gpu_ctx* ctx);
+/* Counters for bench.py: own kernel launches (k_expand/k_search/k_extract/k_eval,
+ * library CUB launches excluded), k_search device time and launch count, and bytes
+ * moved host->device / device->host. */
+int64_t mosaic_gpu_own_launches(mosaic_gpu_ctx* ctx);
+double mosaic_gpu_ksearch_ms(mosaic_gpu_ctx* ctx);
+int64_t mosaic_gpu_ksearch_launches(mosaic_gpu_ctx* ctx);
+int64_t mosaic_gpu_h2d_bytes(mosaic_gpu_ctx* ctx);
+int64_t mosaic_gpu_d2h_bytes(mosaic_gpu_ctx* ctx);
+/* CUDA events on the context's stream: which = 0 start, 1 stop; elapsed in ms. */
+void mosaic_gpu_mark(mosaic_gpu_ctx* ctx, int which);
+double mosaic_gpu_marked_ms(mosaic_gpu_ctx* ctx);
 
 /* Synthetic inputs (the reference's profiler, profiler.hpp:65-111/185-338, restated
  * in C++ so the GPU box needs no reference): fills a problem for a named BASELINE

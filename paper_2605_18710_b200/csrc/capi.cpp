@@ -329,6 +329,26 @@ double mosaic_gpu_search_ms(mosaic_gpu_ctx* ctx) {
     return ctx->pl->engine().search_ms() + ctx->pl->engine().eval_ms();
 }
 void mosaic_gpu_reset_counters(mosaic_gpu_ctx* ctx) { ctx->pl->engine().reset_counters(); }
+int64_t mosaic_gpu_own_launches(mosaic_gpu_ctx* ctx) { return ctx->pl->engine().own_launches(); }
+double mosaic_gpu_ksearch_ms(mosaic_gpu_ctx* ctx) { return ctx->pl->engine().ksearch_ms(); }
+int64_t mosaic_gpu_ksearch_launches(mosaic_gpu_ctx* ctx) {
+    return ctx->pl->engine().ksearch_launches();
+}
+int64_t mosaic_gpu_h2d_bytes(mosaic_gpu_ctx* ctx) { return ctx->pl->engine().h2d_bytes(); }
+int64_t mosaic_gpu_d2h_bytes(mosaic_gpu_ctx* ctx) { return ctx->pl->engine().d2h_bytes(); }
+void mosaic_gpu_mark(mosaic_gpu_ctx* ctx, int which) {
+    try {
+        ctx->pl->engine().mark(which);
+    } catch (...) {
+    }
+}
+double mosaic_gpu_marked_ms(mosaic_gpu_ctx* ctx) {
+    try {
+        return ctx->pl->engine().marked_ms();
+    } catch (...) {
+        return -1.0;
+    }
+}
 
 int mosaic_gpu_synth_problem(const char* spec, int quota_levels, mosaic_gpu_problem** out) {
     return guard([&] {

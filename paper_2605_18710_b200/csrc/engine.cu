@@ -308,6 +308,15 @@ Engine::Engine(int device) : device_(device) {
     CK(cudaEventCreate(&b));
     ev0_ = a;
     ev1_ = b;
+    cudaEvent_t c, d, e, f;
+    CK(cudaEventCreate(&c));
+    CK(cudaEventCreate(&d));
+    CK(cudaEventCreate(&e));
+    CK(cudaEventCreate(&f));
+    evk0_ = c;
+    evk1_ = d;
+    evm0_ = e;
+    evm1_ = f;
     CK(cudaMalloc(&d_spec_, sizeof(Spec)));
     CK(cudaMalloc(&d_ctl_, sizeof(Ctl)));
     CK(cudaMalloc(&d_leaf_, sizeof(Leaf)));
@@ -338,6 +347,10 @@ Engine::~Engine() {
     cudaFreeHost(h_pin_);
     cudaEventDestroy((cudaEvent_t)ev0_);
     cudaEventDestroy((cudaEvent_t)ev1_);
+    cudaEventDestroy((cudaEvent_t)evk0_);
+    cudaEventDestroy((cudaEvent_t)evk1_);
+    cudaEventDestroy((cudaEvent_t)evm0_);
+    cudaEventDestroy((cudaEvent_t)evm1_);
     cudaStreamDestroy(S_(stream_));
 }
 
@@ -355,6 +368,7 @@ void Engine::upload_rows(const Model& M) {
             u.push_back(r.u);
         }
     n_rows_ = (int)base.size();
+    h2d_ += (long long)base.size() * 40;
     size_t n = std::max<size_t>(1, base.size());
     cudaFree(d_base_);
     cudaFree(d_B_);
@@ -422,6 +436,7 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     long long* hx = reinterpret_cast<long long*>(pin + sizeof(Spec) + sizeof(Ctl) + sizeof(Leaf));
     *hs = S;
     CK(cudaMemcpyAsync(d_spec_, hs, sizeof(Spec), cudaMemcpyHostToDevice, s));
+    h2d_ += sizeof(Spec) + sizeof(Ctl) + sizeof(Node) + sizeof(long long);
     std::memset(hc, 0, sizeof(Ctl));
     union {
         double d;
@@ -460,6 +475,7 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
         k_expand<<<(unsigned)((nP + tb - 1) / tb), tb, 0, s>>>((const Spec*)d_spec_, R, P, PK, nP,
                                                                 dc, d_cnt_, d_off_, F, FK, 0);
         ++launches_;
+        ++own_launches_;
         CK(cudaMemsetAsync(d_cnt_ + nP, 0, sizeof(long long), s));
         size_t tb2 = tmp_bytes_;
         CK(cub::DeviceScan::ExclusiveSum(d_tmp_, tb2, d_cnt_, d_off_, (int)(nP + 1), s));
@@ -477,10 +493,12 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
             if (take == 0) throw std::runtime_error("frontier capacity exceeded by one node");
             total = offs[take];
         }
-        if (total > 0)
+        if (total > 0) {
             k_expand<<<(unsigned)((take + tb - 1) / tb), tb, 0, s>>>(
                 (const Spec*)d_spec_, R, P, PK, take, dc, d_cnt_, d_off_, F, FK, 1);
-        ++launches_;
+            ++launches_;
+            ++own_launches_;
+        }
         const long long nF = total;
         const long long rest = nP - take;
         if (nF == 0 && rest == 0) break;
@@ -503,11 +521,21 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
             CK(cudaMemsetAsync(d_flag_, 0, nF, s));
             CK(cudaMemsetAsync(&dc->next, 0, sizeof(unsigned long long), s));
             long long blocks = std::min<long long>((nF + tb - 1) / tb, 148LL * 8);
+            CK(cudaEventRecord((cudaEvent_t)evk0_, s));
             k_search<<<(unsigned)blocks, tb, 0, s>>>((const Spec*)d_spec_, R, F, nF, dc, budget,
                                                      d_flag_);
+            CK(cudaEventRecord((cudaEvent_t)evk1_, s));
             ++launches_;
+            ++own_launches_;
             CK(cudaMemcpyAsync(hc, d_ctl_, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+            d2h_ += sizeof(Ctl);
             CK(cudaStreamSynchronize(s));
+            {
+                float kms = 0;
+                CK(cudaEventElapsedTime(&kms, (cudaEvent_t)evk0_, (cudaEvent_t)evk1_));
+                ksearch_ms_ += kms;
+                ++ksearch_n_;
+            }
             CK(cudaGetLastError());
             if (hc->overflow) {
                 res.overflow = true;
@@ -521,6 +549,8 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
                 const long long bi = hc->best_idx;
                 k_extract<<<1, 32, 0, s>>>((const Spec*)d_spec_, R, F, bi, dc, (Leaf*)d_leaf_);
                 ++launches_;
+                ++own_launches_;
+                d2h_ += sizeof(Leaf);
                 CK(cudaMemcpyAsync(hl, d_leaf_, sizeof(Leaf), cudaMemcpyDeviceToHost, s));
                 hx[2] = LLONG_MAX;
                 CK(cudaMemcpyAsync(&dc->best_idx, hx + 2, sizeof(long long),
@@ -613,6 +643,9 @@ void Engine::evaluate(const std::vector<EvalEntry>& ent, const std::vector<int>&
     k_eval<<<(unsigned)((n + EVAL_WARPS - 1) / EVAL_WARPS), 32 * EVAL_WARPS, 0, s>>>(
         de, dg, doff, n, db, dB, P, dst, drect);
     ++launches_;
+    ++own_launches_;
+    h2d_ += ent.size() * sizeof(EvalEntry) + gpus.size() * 4 + off.size() * 8 + base.size() * 16;
+    d2h_ += n * 8 + ent.size() * 8;
     CK(cudaEventRecord((cudaEvent_t)ev1_, s));
     CK(cudaMemcpyAsync(st_out.data(), dst, n * 8, cudaMemcpyDeviceToHost, s));
     if (!ent.empty())
@@ -630,6 +663,18 @@ void Engine::evaluate(const std::vector<EvalEntry>& ent, const std::vector<int>&
     cudaFreeAsync(dst, s);
     cudaFreeAsync(drect, s);
     CK(cudaStreamSynchronize(s));
+}
+
+void Engine::mark(int which) {
+    CK(cudaSetDevice(device_));
+    CK(cudaEventRecord((cudaEvent_t)(which ? evm1_ : evm0_), S_(stream_)));
+}
+
+double Engine::marked_ms() {
+    CK(cudaEventSynchronize((cudaEvent_t)evm1_));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, (cudaEvent_t)evm0_, (cudaEvent_t)evm1_));
+    return ms;
 }
 
 }  // namespace mg

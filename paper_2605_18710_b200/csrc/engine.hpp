@@ -56,8 +56,22 @@ class Engine {
     double search_ms() const { return search_ms_; }
     void reset_counters() {
         launches_ = 0;
+        own_launches_ = 0;
         search_ms_ = 0;
+        eval_ms_ = 0;
+        ksearch_ms_ = 0;
+        ksearch_n_ = 0;
+        h2d_ = 0;
+        d2h_ = 0;
     }
+    long long own_launches() const { return own_launches_; }
+    double ksearch_ms() const { return ksearch_ms_; }
+    long long ksearch_launches() const { return ksearch_n_; }
+    long long h2d_bytes() const { return h2d_; }
+    long long d2h_bytes() const { return d2h_; }
+    // device-side timing marks on the engine stream (bench.py)
+    void mark(int which);
+    double marked_ms();
     long long budget = 1 << 14;   // DFS steps per frontier item per round
     long long min_front = 8192;   // expand without searching below this many items
     long long cap_front = 1 << 21;
@@ -91,6 +105,14 @@ class Engine {
     long long launches_ = 0;
     double search_ms_ = 0;
     double eval_ms_ = 0;
+    long long own_launches_ = 0;
+    double ksearch_ms_ = 0;
+    long long ksearch_n_ = 0;
+    long long h2d_ = 0, d2h_ = 0;
+    void* evk0_ = nullptr;
+    void* evk1_ = nullptr;
+    void* evm0_ = nullptr;
+    void* evm1_ = nullptr;
 };
 
 }  // namespace mg

@@ -120,6 +120,8 @@ EXPORTS = [
     "mosaic_gpu_trace_cand", "mosaic_gpu_clear_cache", "mosaic_gpu_set_shard",
     "mosaic_gpu_merge_records", "mosaic_gpu_launch_count", "mosaic_gpu_search_ms",
     "mosaic_gpu_reset_counters", "mosaic_gpu_synth_problem", "mosaic_gpu_free_problem",
+    "mosaic_gpu_own_launches", "mosaic_gpu_ksearch_ms", "mosaic_gpu_ksearch_launches",
+    "mosaic_gpu_h2d_bytes", "mosaic_gpu_d2h_bytes", "mosaic_gpu_mark", "mosaic_gpu_marked_ms",
 ]
 
 _lib = None
@@ -165,6 +167,13 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "mosaic_gpu_reset_counters": (None, [vp]),
         "mosaic_gpu_synth_problem": (C.c_int, [C.c_char_p, C.c_int, P(P(ProblemC))]),
         "mosaic_gpu_free_problem": (None, [P(ProblemC)]),
+        "mosaic_gpu_own_launches": (C.c_int64, [vp]),
+        "mosaic_gpu_ksearch_ms": (C.c_double, [vp]),
+        "mosaic_gpu_ksearch_launches": (C.c_int64, [vp]),
+        "mosaic_gpu_h2d_bytes": (C.c_int64, [vp]),
+        "mosaic_gpu_d2h_bytes": (C.c_int64, [vp]),
+        "mosaic_gpu_mark": (None, [vp, C.c_int]),
+        "mosaic_gpu_marked_ms": (C.c_double, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -482,6 +491,22 @@ class Planner:
 
     def reset_counters(self) -> None:
         load_library().mosaic_gpu_reset_counters(self._ctx)
+
+    def counters(self) -> dict:
+        L = load_library()
+        return {"own_launches": L.mosaic_gpu_own_launches(self._ctx),
+                "launches": L.mosaic_gpu_launch_count(self._ctx),
+                "ksearch_ms": L.mosaic_gpu_ksearch_ms(self._ctx),
+                "ksearch_launches": L.mosaic_gpu_ksearch_launches(self._ctx),
+                "h2d_bytes": L.mosaic_gpu_h2d_bytes(self._ctx),
+                "d2h_bytes": L.mosaic_gpu_d2h_bytes(self._ctx),
+                "device_ms": L.mosaic_gpu_search_ms(self._ctx)}
+
+    def mark(self, which: int) -> None:
+        load_library().mosaic_gpu_mark(self._ctx, which)
+
+    def marked_ms(self) -> float:
+        return load_library().mosaic_gpu_marked_ms(self._ctx)
 
     def clear_cache(self) -> None:
         load_library().mosaic_gpu_clear_cache(self._ctx)
