@@ -87,7 +87,7 @@ struct DevHooks {
             double I = load_inc();
             inc_cache = I < inc_cache ? I : inc_cache;
         }
-        double t = inc_cache >= POS_INF ? POS_INF : inc_cache * (1.0 + 1e-12);
+        double t = inc_cache >= POS_INF ? POS_INF : inc_cache * (1.0 - TIE_EPS);
         return t < S.thp ? t : S.thp;
     }
     __device__ double incumbent() {

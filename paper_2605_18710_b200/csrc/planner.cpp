@@ -86,7 +86,7 @@ bool Planner::first_leaf(const std::vector<int>& order, bool filter, double thet
 double Planner::min_value(const std::vector<int>& mods, double ub, mg::SearchStats& st) {
     while (true) {
         // fail-first: fewest viable options first (any order is valid for MIN)
-        const double thp = ub >= POS_INF ? POS_INF : ub * (1.0 + 1e-12);
+        const double thp = ub >= POS_INF ? POS_INF : ub * (1.0 - mg::TIE_EPS);
         std::vector<std::pair<int, int>> cnt;
         for (int m : mods) {
             int c = 0;
@@ -182,7 +182,9 @@ StageResult Planner::stage_eval(uint64_t mask) {
             if (c == 0) return false;
             cnt.push_back({c, m});
         }
-        if (nonneg && have_T && Tstar > th) return false;  // no leaf can reach tau
+        // T* lies in [Tstar*(1 - TIE_EPS - rounding), Tstar]: below that band no leaf can
+        // reach tau; inside it the probe is decided by an exact FIRST search.
+        if (nonneg && have_T && th < Tstar * (1.0 - 1e-13)) return false;
         std::stable_sort(cnt.begin(), cnt.end());
         order.clear();
         for (auto& [c, m] : cnt) order.push_back(m);

@@ -48,6 +48,10 @@ constexpr int MAXENV = 16; // envelope lines per level
 constexpr int FB = MAXB;   // blocks carried by a frontier node
 constexpr double NEG_INF = -1.0e300;
 constexpr double POS_INF = 1.0e300;
+// MIN mode treats leaves within TIE_EPS (relative) of the incumbent as ties: it returns
+// I* with T* in [I*(1 - TIE_EPS - rounding), I*].  Callers resolve a probe inside that
+// band with an exact FIRST search (planner.cpp).
+constexpr double TIE_EPS = 1e-14;
 
 enum { MODE_MIN = 0, MODE_FIRST = 1 };
 
@@ -113,8 +117,13 @@ struct Walk {
     uint16_t bsz[WALK_SLOTS];
     uint16_t bmk[WALK_SLOTS];
     uint16_t x[WALK_SLOTS];
-    uint16_t cap[WALK_SLOTS];
-    // scratch: stats of the child blocks / last-level contributions
+    uint16_t lo[WALK_SLOTS];   // admissible take count per block: [lo, hi]
+    uint16_t hi[WALK_SLOTS];
+    // parent-block stats of level `ps_lvl` (recomputed when a deeper level overwrote them)
+    int ps_lvl;
+    int pu[MAXB];
+    double pm[MAXB], psum[MAXB], pmb[MAXB], pP[MAXB], pmx[MAXB];
+    // child-block stats (look-ahead) / last-level contributions
     int cu[MAXB];
     double cm[MAXB], cs[MAXB], cb[MAXB];
 };
@@ -214,33 +223,38 @@ MG_HD void block_stats(const Spec& S, const Rows& R, const uint16_t* opt, unsign
     }
 }
 
-// First composition in descending lexicographic order.
-MG_HD bool first_comp(const uint16_t* cap, uint16_t* x, int nb, int d) {
-    int rem = d;
+// First composition in descending lexicographic order with x_b in [lo_b, hi_b].
+MG_HD bool first_comp(const uint16_t* lo, const uint16_t* hi, uint16_t* x, int nb, int d) {
+    int R = d;
+    for (int b = 0; b < nb; ++b) R -= lo[b];
+    if (R < 0) return false;
     for (int b = 0; b < nb; ++b) {
-        int t = cap[b] < rem ? cap[b] : rem;
-        x[b] = (uint16_t)t;
-        rem -= t;
+        int room = hi[b] - lo[b];
+        int e = room < R ? room : R;
+        x[b] = (uint16_t)(lo[b] + e);
+        R -= e;
     }
-    return rem == 0;
+    return R == 0;
 }
 
-MG_HD bool next_comp(const uint16_t* cap, uint16_t* x, int nb) {
-    int acc = nb ? x[nb - 1] : 0;
-    int suff = nb ? cap[nb - 1] : 0;
+MG_HD bool next_comp(const uint16_t* lo, const uint16_t* hi, uint16_t* x, int nb) {
+    if (nb < 2) return false;
+    int slack = hi[nb - 1] - x[nb - 1];
+    int extra = x[nb - 1] - lo[nb - 1];
     int i = nb - 2;
     for (; i >= 0; --i) {
-        if (x[i] > 0 && suff >= acc + 1) break;
-        acc += x[i];
-        suff += cap[i];
+        if (x[i] > lo[i] && slack >= 1) break;
+        slack += hi[i] - x[i];
+        extra += x[i] - lo[i];
     }
     if (i < 0) return false;
     x[i] -= 1;
-    int R = acc + 1;
+    int R = extra + 1;
     for (int b = i + 1; b < nb; ++b) {
-        int t = cap[b] < R ? cap[b] : R;
-        x[b] = (uint16_t)t;
-        R -= t;
+        int room = hi[b] - lo[b];
+        int e = room < R ? room : R;
+        x[b] = (uint16_t)(lo[b] + e);
+        R -= e;
     }
     return true;
 }
@@ -255,7 +269,7 @@ MG_HD bool last_intervals(const Walk& w, int o0, int nb, int d, double t, bool l
     for (int b = 0; b < nb; ++b) {
         int s = w.bsz[o0 + b];
         bool rok = le ? rest[b] <= t : rest[b] < t;
-        bool tok = w.cap[o0 + b] && (le ? take[b] <= t : take[b] < t);
+        bool tok = w.hi[o0 + b] && (le ? take[b] <= t : take[b] < t);
         if (rok && tok) {
             sumhi += s;
         } else if (rok) {
@@ -269,6 +283,15 @@ MG_HD bool last_intervals(const Walk& w, int o0, int nb, int d, double t, bool l
     return sumlo <= d && d <= sumhi;
 }
 
+// Stats of the blocks of level j into the parent scratch.
+MG_HD void parent_stats(const Spec& S, const Rows& R, Walk& w, int j) {
+    const int o0 = lvl_off(j);
+    for (int b = 0; b < w.nb[j]; ++b)
+        block_stats(S, R, w.opt, w.bmk[o0 + b], j, w.pu[b], w.pm[b], w.psum[b], w.pmb[b], w.pP[b],
+                    w.pmx[b]);
+    w.ps_lvl = j;
+}
+
 // The per-thread DFS.  Starts at depth d0 (w holds opt[<d0], blocks of level d0);
 // stop < k: emit every surviving node of depth `stop` (frontier expansion);
 // stop == k: run to the leaves.  Returns 1 on a FIRST hit, 2 on abort, 0 when done.
@@ -279,6 +302,7 @@ MG_HD int dfs(const Spec& S, const Rows& R, Walk& w, int d0, int stop, H& h) {
     int j = d0;
     w.ph[j] = 0;
     w.oc[j] = -1;
+    w.ps_lvl = -1;
     while (j >= d0) {
         const int o0 = lvl_off(j);
         const int nb = w.nb[j];
@@ -305,26 +329,106 @@ MG_HD int dfs(const Spec& S, const Rows& R, Walk& w, int d0, int stop, H& h) {
             w.opt[j] = (uint16_t)o;
             const int r = off + o;
             const int dd = R.d[r], uu = R.u[r];
-            const double ff = R.fp[r];
-            int tot = 0;
-            for (int b = 0; b < nb; ++b) {
-                int units;
-                double mem, sum, mb, P, mbx;
-                block_stats(S, R, w.opt, w.bmk[o0 + b], j, units, mem, sum, mb, P, mbx);
-                bool el = units + uu <= S.L && !(mem + ff > S.cap_slack);
-                w.cap[o0 + b] = el ? w.bsz[o0 + b] : 0;
-                tot += w.cap[o0 + b];
+            const double ff = R.fp[r], bo = R.B[r], ba = R.base[r];
+            const bool last = j == k - 1;
+            if (w.ps_lvl != j) {
+                parent_stats(S, R, w, j);
+                if (last) {
+                    // approximate rest contributions (any summation order) for the fast filter
+                    for (int b = 0; b < nb; ++b)
+                        w.cm[b] = w.bmk[o0 + b] ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] +
+                                                      (S.additive ? 0.0 : S.e3 * w.pP[b])
+                                                : NEG_INF;
+                }
             }
-            if (tot < dd) continue;
-            if (j == k - 1) {
+            // per-block admissible take interval: capacity, memory, and (non-negative
+            // models) the interference bound of the taken and the remaining part
+            int sumlo = 0, sumhi = 0;
+            bool dead = false;
+            for (int b = 0; b < nb; ++b) {
+                const int s = w.bsz[o0 + b];
+                bool el = w.pu[b] + uu <= S.L && !(w.pm[b] + ff > S.cap_slack);
+                bool tok = el, rok = true;
+                if (!last && S.nonneg) {
+                    if (el) {
+                        double lbt;
+                        if (S.include_self) {
+                            double mb = w.pmb[b] > ba ? w.pmb[b] : ba;
+                            lbt = mb + S.e1 + S.e2 * (w.psum[b] + bo) +
+                                  envelope(S, j + 1, w.pP[b] * bo);
+                        } else {
+                            double bx = ba - S.e2 * bo;
+                            double mx = w.pmx[b] > bx ? w.pmx[b] : bx;
+                            lbt = mx + S.e1 + S.e2 * (w.psum[b] + bo) + envelope(S, j + 1, 0.0);
+                        }
+                        tok = !(lbt > thr);
+                    }
+                    if (w.bmk[o0 + b]) {
+                        double lbr = S.include_self
+                                         ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] +
+                                               envelope(S, j + 1, w.pP[b])
+                                         : w.pmx[b] + S.e1 + S.e2 * w.psum[b] +
+                                               envelope(S, j + 1, 0.0);
+                        rok = !(lbr > thr);
+                    }
+                }
+                int l, hgh;
+                if (rok) {
+                    l = 0;
+                    hgh = tok ? s : 0;
+                } else if (tok) {
+                    l = s;
+                    hgh = s;
+                } else {
+                    dead = true;
+                    break;
+                }
+                w.lo[o0 + b] = (uint16_t)l;
+                w.hi[o0 + b] = (uint16_t)hgh;
+                sumlo += l;
+                sumhi += hgh;
+            }
+            if (dead || sumlo > dd || sumhi < dd) continue;
+            if (last) {
                 // ---- last level: closed form over blocks ----
                 h.count_leaf();
+                if (S.include_self) {
+                    // fast filter with approximate contributions and a 1e-12 slack: exact
+                    // values differ by a few ulps, so a rejection here is always sound
+                    // MIN rejects ties with the incumbent (and anything within TIE_EPS
+                    // below it): the planner only ever needs T* to that precision.
+                    const bool fm = S.mode == MODE_FIRST;
+                    const double tx = fm ? S.theta * (1.0 + 1e-12) : h.incumbent() * (1.0 - TIE_EPS);
+                    int flo = 0, fhi = 0;
+                    bool fdead = false;
+                    for (int b = 0; b < nb; ++b) {
+                        const int s = w.bsz[o0 + b];
+                        bool rok = fm ? w.cm[b] <= tx : w.cm[b] < tx;
+                        bool tok = false;
+                        if (w.hi[o0 + b]) {
+                            double mb = w.pmb[b] > ba ? w.pmb[b] : ba;
+                            double tv = mb + S.e1 + S.e2 * (w.psum[b] + bo) +
+                                        (S.additive ? 0.0 : S.e3 * (w.pP[b] * bo));
+                            tok = fm ? tv <= tx : tv < tx;
+                        }
+                        if (rok) {
+                            fhi += tok ? s : 0;
+                        } else if (tok) {
+                            flo += s;
+                            fhi += s;
+                        } else {
+                            fdead = true;
+                            break;
+                        }
+                    }
+                    if (fdead || flo > dd || fhi < dd) continue;
+                }
                 double* rest = w.cs;
                 double* take = w.cb;
                 for (int b = 0; b < nb; ++b) {
                     unsigned m = w.bmk[o0 + b];
                     rest[b] = contrib(S, R, w.opt, m);
-                    take[b] = w.cap[o0 + b] ? contrib(S, R, w.opt, m | (1u << j)) : POS_INF;
+                    take[b] = w.hi[o0 + b] ? contrib(S, R, w.opt, m | (1u << j)) : POS_INF;
                 }
                 if (S.mode == MODE_FIRST) {
                     int lo, hi;
@@ -335,7 +439,7 @@ MG_HD int dfs(const Spec& S, const Rows& R, Walk& w, int d0, int stop, H& h) {
                     for (int b = 0; b < nb; ++b) {
                         int s = w.bsz[o0 + b];
                         bool rok = rest[b] <= S.theta;
-                        bool tok = w.cap[o0 + b] && take[b] <= S.theta;
+                        bool tok = w.hi[o0 + b] && take[b] <= S.theta;
                         int l = (!rok) ? s : 0;
                         int hgh = tok ? s : 0;
                         int e = hgh - l < rem ? hgh - l : rem;
@@ -352,14 +456,15 @@ MG_HD int dfs(const Spec& S, const Rows& R, Walk& w, int d0, int stop, H& h) {
                     return 1;
                 } else {
                     double I = h.incumbent();
+                    double Ie = I * (1.0 - TIE_EPS);
                     int lo, hi;
-                    if (!last_intervals(w, o0, nb, dd, I, false, rest, take, lo, hi)) continue;
-                    double hiv = I;
+                    if (!last_intervals(w, o0, nb, dd, Ie, false, rest, take, lo, hi)) continue;
+                    double hiv = Ie;
                     while (true) {
                         double c = NEG_INF;
                         for (int b = 0; b < nb; ++b) {
                             if (rest[b] < hiv && rest[b] > c) c = rest[b];
-                            if (w.cap[o0 + b] && take[b] < hiv && take[b] > c) c = take[b];
+                            if (w.hi[o0 + b] && take[b] < hiv && take[b] > c) c = take[b];
                         }
                         if (c <= NEG_INF) break;
                         if (last_intervals(w, o0, nb, dd, c, true, rest, take, lo, hi)) {
@@ -373,19 +478,22 @@ MG_HD int dfs(const Spec& S, const Rows& R, Walk& w, int d0, int stop, H& h) {
                 }
                 continue;
             }
-            if (!first_comp(w.cap + o0, w.x + o0, nb, dd)) continue;
+            if (!first_comp(w.lo + o0, w.hi + o0, w.x + o0, nb, dd)) continue;
             w.ph[j] = 1;
         } else {
-            if (!next_comp(w.cap + o0, w.x + o0, nb)) {
+            if (!next_comp(w.lo + o0, w.hi + o0, w.x + o0, nb)) {
                 w.ph[j] = 0;
                 continue;
             }
         }
-        // ---- build the child (level j+1 blocks) and prune ----
+        // ---- build the child (level j+1 blocks + their stats) ----
         h.count_node();
+        if (w.ps_lvl != j) parent_stats(S, R, w, j);
         const int o1 = lvl_off(j + 1);
         const int c1 = lvl_cap(j + 1);
         const int r = S.lvl_off[j] + w.opt[j];
+        const int uu = R.u[r];
+        const double ff = R.fp[r], bo = R.B[r], ba = R.base[r];
         int m = 0;
         bool overflow = false;
         for (int b = 0; b < nb; ++b) {
@@ -395,12 +503,20 @@ MG_HD int dfs(const Spec& S, const Rows& R, Walk& w, int d0, int stop, H& h) {
                 if (m >= c1) { overflow = true; break; }
                 w.bsz[o1 + m] = (uint16_t)xb;
                 w.bmk[o1 + m] = (uint16_t)(mk | (1u << j));
+                w.cu[m] = w.pu[b] + uu;
+                w.cm[m] = w.pm[b] + ff;
+                w.cs[m] = w.psum[b] + bo;
+                w.cb[m] = w.pmb[b] > ba ? w.pmb[b] : ba;
                 ++m;
             }
             if (xb < s) {
                 if (m >= c1) { overflow = true; break; }
                 w.bsz[o1 + m] = (uint16_t)(s - xb);
                 w.bmk[o1 + m] = (uint16_t)mk;
+                w.cu[m] = w.pu[b];
+                w.cm[m] = w.pm[b];
+                w.cs[m] = w.psum[b];
+                w.cb[m] = w.pmb[b];
                 ++m;
             }
         }
@@ -410,37 +526,8 @@ MG_HD int dfs(const Spec& S, const Rows& R, Walk& w, int d0, int stop, H& h) {
         }
         w.nb[j + 1] = (uint16_t)m;
         w.used[j + 1] = w.used[j] + R.d[r] * R.u[r];
-        bool prune = false;
         const double thr = h.thr(S);
-        if (S.nonneg) {
-            for (int b = 0; b < m && !prune; ++b) {
-                int units;
-                double mem, sum, mb, P, mbx;
-                block_stats(S, R, w.opt, w.bmk[o1 + b], j + 1, units, mem, sum, mb, P, mbx);
-                w.cu[b] = units;
-                w.cm[b] = mem;
-                w.cs[b] = sum;
-                w.cb[b] = mb;
-                if (!w.bmk[o1 + b]) continue;
-                double lb;
-                if (S.include_self) {
-                    lb = mb + S.e1 + S.e2 * sum + envelope(S, j + 1, P);
-                } else {
-                    lb = mbx + S.e1 + S.e2 * sum + envelope(S, j + 1, 0.0);
-                }
-                if (lb > thr) prune = true;
-            }
-        } else {
-            for (int b = 0; b < m; ++b) {
-                int units;
-                double mem, sum, mb, P, mbx;
-                block_stats(S, R, w.opt, w.bmk[o1 + b], j + 1, units, mem, sum, mb, P, mbx);
-                w.cu[b] = units;
-                w.cm[b] = mem;
-                w.cs[b] = sum;
-                w.cb[b] = mb;
-            }
-        }
+        bool prune = false;
         // look-ahead: every unplaced level keeps an option that fits somewhere
         for (int l = j + 1; l < k && !prune; ++l) {
             const int n = S.lvl_n[l], off = S.lvl_off[l];
@@ -450,15 +537,15 @@ MG_HD int dfs(const Spec& S, const Rows& R, Walk& w, int d0, int stop, H& h) {
                 int t = opt_test(S, R, rr, thr);
                 if (t == 2) break;
                 if (t == 1) continue;
-                const int dd = R.d[rr], uu = R.u[rr];
-                const double ff = R.fp[rr], bb = R.B[rr], ba = R.base[rr];
+                const int dd = R.d[rr], u2 = R.u[rr];
+                const double f2 = R.fp[rr], b2 = R.B[rr], a2 = R.base[rr];
                 int cnt = 0;
                 for (int b = 0; b < m; ++b) {
-                    if (w.cu[b] + uu > S.L) continue;
-                    if (w.cm[b] + ff > S.cap_slack) continue;
+                    if (w.cu[b] + u2 > S.L) continue;
+                    if (w.cm[b] + f2 > S.cap_slack) continue;
                     if (S.nonneg && S.include_self) {
-                        double mb = w.cb[b] > ba ? w.cb[b] : ba;
-                        if (mb + S.e1 + S.e2 * (w.cs[b] + bb) > thr) continue;
+                        double mb = w.cb[b] > a2 ? w.cb[b] : a2;
+                        if (mb + S.e1 + S.e2 * (w.cs[b] + b2) > thr) continue;
                     }
                     cnt += w.bsz[o1 + b];
                     if (cnt >= dd) break;

@@ -64,8 +64,10 @@ inline bool build_spec(const Model& M, const SearchReq& q, Spec& S) {
     S.e3 = M.e3;
     S.cap_slack = M.cap * (1.0 + 1e-12);
     S.theta = q.theta;
-    double t = q.mode == MODE_MIN ? q.ub : q.theta;
-    S.thp = t >= POS_INF ? POS_INF : t * (1.0 + 1e-12);
+    if (q.mode == MODE_MIN)
+        S.thp = q.ub >= POS_INF ? POS_INF : q.ub * (1.0 - TIE_EPS);
+    else
+        S.thp = q.theta >= POS_INF ? POS_INF : q.theta * (1.0 + 1e-12);
     // module-index position -> level
     std::vector<std::pair<int, int>> ml;
     for (int l = 0; l < k; ++l) ml.push_back({q.level_module[l], l});
