@@ -192,6 +192,8 @@ double mosaic_gpu_ksearch_ms(mosaic_gpu_ctx* ctx);
 int64_t mosaic_gpu_ksearch_launches(mosaic_gpu_ctx* ctx);
 int64_t mosaic_gpu_h2d_bytes(mosaic_gpu_ctx* ctx);
 int64_t mosaic_gpu_d2h_bytes(mosaic_gpu_ctx* ctx);
+/* Algorithmic bytes of the scored leaves: 24*k per leaf (k option rows x 3 fp64). */
+int64_t mosaic_gpu_alg_bytes(mosaic_gpu_ctx* ctx);
 /* CUDA events on the context's stream: which = 0 start, 1 stop; elapsed in ms. */
 void mosaic_gpu_mark(mosaic_gpu_ctx* ctx, int which);
 double mosaic_gpu_marked_ms(mosaic_gpu_ctx* ctx);

@@ -336,6 +336,7 @@ int64_t mosaic_gpu_ksearch_launches(mosaic_gpu_ctx* ctx) {
 }
 int64_t mosaic_gpu_h2d_bytes(mosaic_gpu_ctx* ctx) { return ctx->pl->engine().h2d_bytes(); }
 int64_t mosaic_gpu_d2h_bytes(mosaic_gpu_ctx* ctx) { return ctx->pl->engine().d2h_bytes(); }
+int64_t mosaic_gpu_alg_bytes(mosaic_gpu_ctx* ctx) { return ctx->pl->engine().alg_bytes(); }
 void mosaic_gpu_mark(mosaic_gpu_ctx* ctx, int which) {
     try {
         ctx->pl->engine().mark(which);

@@ -1,22 +1,17 @@
 // engine.cu — sm_100a kernels of the planner hot path and their host driver.
 //
-//   k_expand  : one thread per frontier node; enumerates its children (next level's
-//               option x canonical composition) with all pruning, count pass + write
-//               pass (stable, so the frontier stays in reference DFS order).
-//   k_search  : persistent threads pull frontier nodes from an atomic counter and run
-//               the budgeted DFS of search_core.cuh to the leaves (MIN: shared
-//               incumbent via atomicMin on the fp64 bits; FIRST: smallest frontier
-//               index with a hit via atomicMin, later subtrees abort).
-//   k_extract : re-walks the winning FIRST subtree and writes its leaf.
-//   k_eval    : batched stage_time of explicit allocations (perf_model.hpp:442-479),
-//               one warp per allocation, resident bitmaps in shared memory.
-//
-// Load balance: subtrees that exceed the per-item step budget are flagged, compacted
-// (cub::DeviceSelect, stable) and expanded one level deeper for the next round, so
-// heavy subtrees fan out over the whole GPU instead of pinning one thread.
+//   k_search : one resident persistent grid per stage search.  Every thread runs the
+//              canonical-block DFS of search_core.cuh on cursors popped from a shared
+//              queue; busy threads donate shallow subtrees when others go idle, so
+//              irregular trees stay spread over all 148 SMs without host round trips.
+//              MIN: shared fp64 incumbent (atomicMin on the bits).  FIRST: the earliest
+//              hit in reference DFS order wins (path comparison under a seqlock).
+//   k_eval   : batched stage_time of explicit allocations (perf_model.hpp:442-479),
+//              one warp per allocation, resident bitmaps in shared memory.
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -37,46 +32,102 @@ namespace mg {
                                      " at " #x);                                       \
     } while (0)
 
+// Control block.  Fields that different threads write often live on their own 128-B
+// lines so spinning workers do not serialize the busy ones.
 struct Ctl {
-    unsigned long long inc;  // MIN incumbent, fp64 bits (values are >= 0)
-    long long best_idx;      // FIRST: smallest frontier index with a hit
-    unsigned long long next; // work counter
+    alignas(128) unsigned long long inc;  // MIN incumbent, fp64 bits (values are >= 0)
+    double abort_below;
     int abort;
     int overflow;
-    unsigned long long nodes, leaves;
-    double abort_below;
+    alignas(128) unsigned long long q_head;
+    alignas(128) unsigned long long q_tail;
+    unsigned long long q_cap;
+    alignas(128) unsigned long long outstanding;  // queued + in-flight cursors
+    alignas(128) unsigned int idle;
+    alignas(128) int lock;  // FIRST: best hit, published under a seqlock
+    int ver;
+    int has_hit;
+    alignas(128) unsigned long long nodes, leaves;
 };
 
 struct DevHooks {
     Ctl* ctl;
     int mode;
-    int expanding;
-    int extract;
-    int write;
-    long long idx;
-    long long budget;
     long long steps;
-    int unfinished;
     double inc_cache;
     int refresh;
     Leaf* leaf_out;
-    Node* out;
-    long long out_base;
-    long long emitted;
+    HitPath* best;
+    Cont* q;
+    int* ready;
     unsigned long long nodes, leaves;
+    const Walk* w;
+    int cur_level;
 
-    __device__ bool abort() {
-        if (expanding) return false;
-        if (++steps > budget) {
-            unfinished = 1;
-            return true;
+    // 0 continue, 2 abandon (MIN restart, or a FIRST hit precedes everything left here),
+    // 3 idle threads are waiting: donate shallow work
+    __device__ int abort() {
+        ++steps;
+        if (*(volatile int*)&ctl->abort) return 2;
+        if ((steps & 15) == 0) {
+            if (mode == MODE_FIRST && *(volatile int*)&ctl->has_hit && hit_precedes()) return 2;
+            unsigned int idle = *(volatile unsigned int*)&ctl->idle;
+            if (idle) {
+                unsigned long long qn = *(volatile unsigned long long*)&ctl->q_tail -
+                                        *(volatile unsigned long long*)&ctl->q_head;
+                if (qn < idle) return 3;
+            }
         }
-        if (mode == MODE_FIRST) {
-            if (!extract && *(volatile long long*)&ctl->best_idx < idx) return true;
-        } else if (*(volatile int*)&ctl->abort) {
-            return true;
+        return 0;
+    }
+    // does the published hit come before every leaf this thread can still reach?
+    // Walk state: levels < cur_level fixed at (opt, x); at cur_level the options after
+    // oc[cur_level] remain.
+    __device__ bool hit_precedes() {
+        int v0 = *(volatile int*)&ctl->ver;
+        if (v0 & 1) return false;
+        __threadfence();
+        bool before = path_precedes_rest((const volatile HitPath*)best, *w, cur_level);
+        __threadfence();
+        int v1 = *(volatile int*)&ctl->ver;
+        return v0 == v1 && before;
+    }
+    // publish a FIRST hit at the last level if it precedes the current best
+    __device__ void hit(const Walk& wk, int j, double v) {
+        while (atomicCAS(&ctl->lock, 0, 1) != 0) __nanosleep(64);
+        __threadfence();
+        bool better = !*(volatile int*)&ctl->has_hit ||
+                      path_cmp((const volatile HitPath*)best, wk, j) > 0;
+        if (better) {
+            atomicAdd(&ctl->ver, 1);
+            __threadfence();
+            path_store((volatile HitPath*)best, wk, j);
+            store_leaf(wk, j, v, *leaf_out);
+            ctl->has_hit = 1;
+            __threadfence();
+            atomicAdd(&ctl->ver, 1);
         }
-        return false;
+        __threadfence();
+        atomicExch(&ctl->lock, 0);
+    }
+    __device__ void split(const Walk&, int, int) {}
+    // push the cursor "rest of level l" onto the ring queue (ticket t -> slot t % cap,
+    // published by writing ready[slot] = t + 1)
+    __device__ bool donate(const Walk& wk, int l) {
+        unsigned long long t = *(volatile unsigned long long*)&ctl->q_tail;
+        while (true) {
+            unsigned long long head = *(volatile unsigned long long*)&ctl->q_head;
+            if (t + 1 - head > ctl->q_cap) return false;  // ring full
+            unsigned long long old = atomicCAS(&ctl->q_tail, t, t + 1);
+            if (old == t) break;
+            t = old;
+        }
+        atomicAdd(&ctl->outstanding, 1ULL);
+        const unsigned long long slot = t % ctl->q_cap;
+        store_cont(wk, l, 1, 0, q[slot]);
+        __threadfence();
+        atomicExch(&ready[slot], (int)(t + 1));
+        return true;
     }
     __device__ double load_inc() {
         return __longlong_as_double(*(volatile long long*)&ctl->inc);
@@ -100,19 +151,13 @@ struct DevHooks {
         if (v < inc_cache) inc_cache = v;
         if (v < ctl->abort_below) atomicExch(&ctl->abort, 1);
     }
-    __device__ void hit(const Walk& w, int j, double v) {
-        if (extract)
-            store_leaf(w, j, v, *leaf_out);
-        else
-            atomicMin(&ctl->best_idx, idx);
-    }
     __device__ void count_node() { ++nodes; }
     __device__ void count_leaf() { ++leaves; }
-    __device__ void emit(const Walk& w, int dep) {
-        if (write) store_node(w, dep, out[out_base + emitted]);
-        ++emitted;
+    __device__ void overflow() {
+        atomicExch(&ctl->overflow, 1);
+        atomicExch(&ctl->abort, 1);
     }
-    __device__ void overflow() { atomicExch(&ctl->overflow, 1); }
+    __device__ void level(int j) { cur_level = j; }
 };
 
 __device__ __forceinline__ void load_spec(const Spec* g, Spec* s) {
@@ -123,114 +168,72 @@ __device__ __forceinline__ void load_spec(const Spec* g, Spec* s) {
     __syncthreads();
 }
 
-__device__ __forceinline__ void load_walk(const Spec& S, const Rows& R, const Node& nd, Walk& w) {
-    load_node(nd, w);
-    int used = 0;
-    for (int l = 0; l < nd.depth; ++l) {
-        int r = S.lvl_off[l] + nd.opt[l];
-        used += R.d[r] * R.u[r];
-    }
-    w.used[nd.depth] = used;
-}
-
-__device__ __forceinline__ DevHooks make_hooks(Ctl* ctl, int mode) {
-    DevHooks h;
-    h.ctl = ctl;
-    h.mode = mode;
-    h.expanding = 0;
-    h.extract = 0;
-    h.write = 0;
-    h.idx = 0;
-    h.budget = LLONG_MAX;
-    h.steps = 0;
-    h.unfinished = 0;
-    h.inc_cache = POS_INF;
-    h.refresh = 0;
-    h.leaf_out = nullptr;
-    h.out = nullptr;
-    h.out_base = 0;
-    h.emitted = 0;
-    h.nodes = 0;
-    h.leaves = 0;
-    return h;
-}
-
-__global__ void __launch_bounds__(128) k_expand(const Spec* Sg, Rows R, const Node* in,
-                                                const long long* in_key, long long n, Ctl* ctl,
-                                                long long* cnt, const long long* off, Node* out,
-                                                long long* out_key, int write) {
-    __shared__ Spec S;
-    load_spec(Sg, &S);
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const Node& nd = in[i];
-    if (nd.depth >= S.k - 1) {  // cannot be split further: carried over as is
-        if (write) {
-            out[off[i]] = nd;
-            out_key[off[i]] = in_key[i];
-        } else {
-            cnt[i] = 1;
-        }
-        return;
-    }
-    Walk w;
-    load_walk(S, R, nd, w);
-    DevHooks h = make_hooks(ctl, S.mode);
-    h.expanding = 1;
-    h.write = write;
-    h.out = out;
-    h.out_base = write ? off[i] : 0;
-    h.inc_cache = h.load_inc();
-    dfs(S, R, w, nd.depth, nd.depth + 1, h);
-    if (write) {
-        for (long long e = 0; e < h.emitted; ++e) out_key[off[i] + e] = in_key[i];
-    } else {
-        cnt[i] = h.emitted;
-        atomicAdd(&ctl->nodes, h.nodes);
-    }
-}
-
-__global__ void __launch_bounds__(128) k_search(const Spec* Sg, Rows R, const Node* in,
-                                                long long n, Ctl* ctl, long long budget,
-                                                unsigned char* unfin) {
+// One resident persistent grid per search with a shared cursor queue.  Threads pop
+// cursors; a busy thread that sees idle threads and a short queue donates the untried
+// siblings of every level above its current one and keeps the current level.
+// `outstanding` counts queued + in-flight cursors; all threads exit when it reaches 0.
+//   MIN:   shared incumbent (atomicMin on the fp64 bits), tie band TIE_EPS.
+//   FIRST: hits are ordered by their reference-DFS path; the earliest is kept under a
+//          seqlock, and work that lies after it is abandoned.
+__global__ void __launch_bounds__(128) k_search(const Spec* Sg, Rows R, Cont* Q, int* ready,
+                                                Ctl* ctl, HitPath* best, Leaf* leaf_out) {
     __shared__ Spec S;
     load_spec(Sg, &S);
     Walk w;
     unsigned long long nodes = 0, leaves = 0;
     while (true) {
-        long long i = (long long)atomicAdd(&ctl->next, 1ULL);
-        if (i >= n) break;
-        if (S.mode == MODE_FIRST && i > *(volatile long long*)&ctl->best_idx) break;
-        if (S.mode == MODE_MIN && *(volatile int*)&ctl->abort) break;
-        const Node& nd = in[i];
-        load_walk(S, R, nd, w);
-        DevHooks h = make_hooks(ctl, S.mode);
-        h.idx = i;
-        h.budget = nd.depth >= S.k - 1 ? LLONG_MAX : budget;
+        long long slot = -1;
+        bool idle = false;
+        unsigned backoff = 128;
+        while (true) {
+            if (*(volatile int*)&ctl->abort) break;
+            unsigned long long h = *(volatile unsigned long long*)&ctl->q_head;
+            unsigned long long t = *(volatile unsigned long long*)&ctl->q_tail;
+            if (h < t) {
+                if (atomicCAS(&ctl->q_head, h, h + 1) == h) {
+                    slot = (long long)h;
+                    break;
+                }
+                continue;
+            }
+            if (*(volatile unsigned long long*)&ctl->outstanding == 0) break;
+            if (!idle) {
+                atomicAdd(&ctl->idle, 1u);
+                idle = true;
+            }
+            __nanosleep(backoff);
+            backoff = backoff < 4096 ? backoff * 2 : 4096;
+        }
+        if (idle) atomicSub(&ctl->idle, 1u);
+        if (slot < 0) break;
+        const long long ticket = slot;
+        slot = (long long)((unsigned long long)ticket % ctl->q_cap);
+        while (*(volatile int*)&ready[slot] != (int)(ticket + 1)) __nanosleep(32);
+        __threadfence();
+        load_cont(Q[slot], w);
+        DevHooks h;
+        h.ctl = ctl;
+        h.mode = S.mode;
+        h.steps = 0;
+        h.refresh = 0;
+        h.leaf_out = leaf_out;
+        h.best = best;
+        h.q = Q;
+        h.ready = ready;
+        h.nodes = 0;
+        h.leaves = 0;
+        h.w = &w;
+        h.cur_level = Q[slot].depth;
+        h.inc_cache = POS_INF;
         h.inc_cache = h.load_inc();
-        dfs(S, R, w, nd.depth, S.k, h);
-        unfin[i] = (unsigned char)h.unfinished;
+        dfs(S, R, w, Q[slot].depth, h);
         nodes += h.nodes;
         leaves += h.leaves;
+        __threadfence();
+        atomicAdd(&ctl->outstanding, ~0ULL);  // -1
     }
     atomicAdd(&ctl->nodes, nodes);
     atomicAdd(&ctl->leaves, leaves);
-}
-
-__global__ void k_extract(const Spec* Sg, Rows R, const Node* in, long long idx, Ctl* ctl,
-                          Leaf* out) {
-    __shared__ Spec S;
-    load_spec(Sg, &S);
-    if (threadIdx.x != 0) return;
-    Walk w;
-    const Node& nd = in[idx];
-    load_walk(S, R, nd, w);
-    DevHooks h = make_hooks(ctl, MODE_FIRST);
-    h.extract = 1;
-    h.idx = idx;
-    h.leaf_out = out;
-    out->nb = -1;
-    dfs(S, R, w, nd.depth, S.k, h);
 }
 
 // ---------------------------------------------------------------------------
@@ -298,7 +301,16 @@ __global__ void __launch_bounds__(32 * EVAL_WARPS)
 // ---------------------------------------------------------------------------
 static inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// pinned staging layout: Spec | Ctl | Leaf | Cont | int, each 256-B aligned
+static inline size_t pin_off(int i) {
+    const size_t sz[5] = {sizeof(Spec), sizeof(Ctl), sizeof(Leaf), sizeof(Cont), sizeof(int)};
+    size_t off = 0;
+    for (int k = 0; k < i; ++k) off += (sz[k] + 255) & ~size_t(255);
+    return off;
+}
+
 Engine::Engine(int device) : device_(device) {
+    trace_ = std::getenv("MOSAIC_TRACE") != nullptr;
     CK(cudaSetDevice(device));
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -320,8 +332,7 @@ Engine::Engine(int device) : device_(device) {
     CK(cudaMalloc(&d_spec_, sizeof(Spec)));
     CK(cudaMalloc(&d_ctl_, sizeof(Ctl)));
     CK(cudaMalloc(&d_leaf_, sizeof(Leaf)));
-    CK(cudaMalloc(&d_nsel_, sizeof(long long)));
-    CK(cudaMallocHost(&h_pin_, sizeof(Spec) + sizeof(Ctl) + sizeof(Leaf) + 64 + sizeof(Node)));
+    CK(cudaMallocHost(&h_pin_, pin_off(5)));
 }
 
 Engine::~Engine() {
@@ -335,15 +346,9 @@ Engine::~Engine() {
     cudaFree(d_spec_);
     cudaFree(d_ctl_);
     cudaFree(d_leaf_);
-    for (int i = 0; i < 3; ++i) {
-        cudaFree(d_front_[i]);
-        cudaFree(d_key_[i]);
-    }
-    cudaFree(d_cnt_);
-    cudaFree(d_off_);
-    cudaFree(d_flag_);
-    cudaFree(d_nsel_);
-    cudaFree(d_tmp_);
+    cudaFree(d_front_[0]);
+    cudaFree(d_ready_);
+    cudaFree(d_best_);
     cudaFreeHost(h_pin_);
     cudaEventDestroy((cudaEvent_t)ev0_);
     cudaEventDestroy((cudaEvent_t)ev1_);
@@ -395,29 +400,11 @@ void Engine::upload_rows(const Model& M) {
 void Engine::ensure_front(long long n) {
     if (n <= front_cap_) return;
     long long cap = std::max<long long>(n, 1024);
-    for (int i = 0; i < 3; ++i) {
-        cudaFree(d_front_[i]);
-        cudaFree(d_key_[i]);
-        CK(cudaMalloc(&d_front_[i], cap * sizeof(Node)));
-        CK(cudaMalloc(&d_key_[i], cap * sizeof(long long)));
-    }
-    cudaFree(d_cnt_);
-    cudaFree(d_off_);
-    cudaFree(d_flag_);
-    CK(cudaMalloc(&d_cnt_, (cap + 1) * sizeof(long long)));
-    CK(cudaMalloc(&d_off_, (cap + 1) * sizeof(long long)));
-    CK(cudaMalloc(&d_flag_, cap));
-    size_t b1 = 0, b2 = 0, b3 = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, b1, d_cnt_, d_off_, (int)cap + 1);
-    cub::DeviceSelect::Flagged(nullptr, b2, (Node*)d_front_[0], d_flag_, (Node*)d_front_[1],
-                               d_nsel_, (int)cap);
-    cub::DeviceSelect::Flagged(nullptr, b3, d_key_[0], d_flag_, d_key_[1], d_nsel_, (int)cap);
-    size_t need = std::max(b1, std::max(b2, b3));
-    if (need > tmp_bytes_) {
-        cudaFree(d_tmp_);
-        CK(cudaMalloc(&d_tmp_, need));
-        tmp_bytes_ = need;
-    }
+    cudaFree(d_front_[0]);
+    CK(cudaMalloc(&d_front_[0], cap * sizeof(Cont)));
+    cudaFree(d_ready_);
+    CK(cudaMalloc(&d_ready_, cap * sizeof(int)));
+    if (!d_best_) CK(cudaMalloc(&d_best_, sizeof(HitPath)));
     front_cap_ = cap;
 }
 
@@ -430,13 +417,12 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     ensure_front(cap);
     Rows R{d_base_, d_B_, d_fp_, d_bound_, d_d_, d_u_};
     char* pin = reinterpret_cast<char*>(h_pin_);
-    Spec* hs = reinterpret_cast<Spec*>(pin);
-    Ctl* hc = reinterpret_cast<Ctl*>(pin + sizeof(Spec));
-    Leaf* hl = reinterpret_cast<Leaf*>(pin + sizeof(Spec) + sizeof(Ctl));
-    long long* hx = reinterpret_cast<long long*>(pin + sizeof(Spec) + sizeof(Ctl) + sizeof(Leaf));
+    Spec* hs = reinterpret_cast<Spec*>(pin + pin_off(0));
+    Ctl* hc = reinterpret_cast<Ctl*>(pin + pin_off(1));
+    Leaf* hl = reinterpret_cast<Leaf*>(pin + pin_off(2));
+    Cont* hr = reinterpret_cast<Cont*>(pin + pin_off(3));
+    int* hone = reinterpret_cast<int*>(pin + pin_off(4));
     *hs = S;
-    CK(cudaMemcpyAsync(d_spec_, hs, sizeof(Spec), cudaMemcpyHostToDevice, s));
-    h2d_ += sizeof(Spec) + sizeof(Ctl) + sizeof(Node) + sizeof(long long);
     std::memset(hc, 0, sizeof(Ctl));
     union {
         double d;
@@ -444,158 +430,62 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     } cv;
     cv.d = ub;
     hc->inc = cv.u;
-    hc->best_idx = LLONG_MAX;
     hc->abort_below = abort_below;
-    CK(cudaMemcpyAsync(d_ctl_, hc, sizeof(Ctl), cudaMemcpyHostToDevice, s));
-    Ctl* dc = reinterpret_cast<Ctl*>(d_ctl_);
-
-    Node* P = reinterpret_cast<Node*>(d_front_[0]);
-    Node* F = reinterpret_cast<Node*>(d_front_[1]);
-    Node* Q = reinterpret_cast<Node*>(d_front_[2]);
-    long long* PK = d_key_[0];
-    long long* FK = d_key_[1];
-    long long* QK = d_key_[2];
-    {
-        Node* hr = reinterpret_cast<Node*>(hx + 4);
-        std::memset(hr, 0, sizeof(Node));
-        hr->depth = 0;
-        hr->nb = 1;
-        hr->bsz[0] = (uint16_t)S.G;
-        hx[0] = 0;
-        CK(cudaMemcpyAsync(P, hr, sizeof(Node), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(PK, hx, sizeof(long long), cudaMemcpyHostToDevice, s));
-    }
+    hc->q_head = 0;
+    hc->q_tail = 1;
+    hc->q_cap = (unsigned long long)cap;
+    hc->outstanding = 1;
+    std::memset(hr, 0, sizeof(Cont));
+    hr->depth = 0;
+    hr->nb = 1;
+    hr->ph = 0;
+    hr->oc = -1;
+    hr->bsz[0] = (uint16_t)S.G;
+    *hone = 1;
+    Cont* Q = reinterpret_cast<Cont*>(d_front_[0]);
     CK(cudaEventRecord((cudaEvent_t)ev0_, s));
-    long long nP = 1;
-    bool searched_once = false;
-    const int tb = 128;
-    while (nP > 0) {
-        ++st.rounds;
-        // ---- expand a prefix of P by one level into F (count, scan, write) ----
-        k_expand<<<(unsigned)((nP + tb - 1) / tb), tb, 0, s>>>((const Spec*)d_spec_, R, P, PK, nP,
-                                                                dc, d_cnt_, d_off_, F, FK, 0);
-        ++launches_;
-        ++own_launches_;
-        CK(cudaMemsetAsync(d_cnt_ + nP, 0, sizeof(long long), s));
-        size_t tb2 = tmp_bytes_;
-        CK(cub::DeviceScan::ExclusiveSum(d_tmp_, tb2, d_cnt_, d_off_, (int)(nP + 1), s));
-        ++launches_;
-        CK(cudaMemcpyAsync(hx + 1, d_off_ + nP, sizeof(long long), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        long long total = hx[1];
-        long long take = nP;
-        if (total > cap) {
-            std::vector<long long> offs(nP + 1);
-            CK(cudaMemcpy(offs.data(), d_off_, (nP + 1) * sizeof(long long),
-                          cudaMemcpyDeviceToHost));
-            take = 0;
-            while (take < nP && offs[take + 1] <= cap) ++take;
-            if (take == 0) throw std::runtime_error("frontier capacity exceeded by one node");
-            total = offs[take];
-        }
-        if (total > 0) {
-            k_expand<<<(unsigned)((take + tb - 1) / tb), tb, 0, s>>>(
-                (const Spec*)d_spec_, R, P, PK, take, dc, d_cnt_, d_off_, F, FK, 1);
-            ++launches_;
-            ++own_launches_;
-        }
-        const long long nF = total;
-        const long long rest = nP - take;
-        if (nF == 0 && rest == 0) break;
-        if (!searched_once && rest == 0 && nF > 0 && nF < min_front) {
-            // pure expansion while the frontier is small (depths are uniform here)
-            CK(cudaMemcpyAsync(hx + 4, F, sizeof(Node), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            if (reinterpret_cast<Node*>(hx + 4)->depth < S.k - 1) {
-                std::swap(P, F);
-                std::swap(PK, FK);
-                nP = nF;
-                continue;
-            }
-        }
-        searched_once = true;
-        long long upto = nF;
-        bool drop_rest = false;
-        if (nF > 0) {
-            // ---- search F with a per-item step budget ----
-            CK(cudaMemsetAsync(d_flag_, 0, nF, s));
-            CK(cudaMemsetAsync(&dc->next, 0, sizeof(unsigned long long), s));
-            long long blocks = std::min<long long>((nF + tb - 1) / tb, 148LL * 8);
-            CK(cudaEventRecord((cudaEvent_t)evk0_, s));
-            k_search<<<(unsigned)blocks, tb, 0, s>>>((const Spec*)d_spec_, R, F, nF, dc, budget,
-                                                     d_flag_);
-            CK(cudaEventRecord((cudaEvent_t)evk1_, s));
-            ++launches_;
-            ++own_launches_;
-            CK(cudaMemcpyAsync(hc, d_ctl_, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
-            d2h_ += sizeof(Ctl);
-            CK(cudaStreamSynchronize(s));
-            {
-                float kms = 0;
-                CK(cudaEventElapsedTime(&kms, (cudaEvent_t)evk0_, (cudaEvent_t)evk1_));
-                ksearch_ms_ += kms;
-                ++ksearch_n_;
-            }
-            CK(cudaGetLastError());
-            if (hc->overflow) {
-                res.overflow = true;
-                break;
-            }
-            if (S.mode == MODE_MIN && hc->abort) {
-                res.aborted = true;
-                break;
-            }
-            if (S.mode == MODE_FIRST && hc->best_idx != LLONG_MAX) {
-                const long long bi = hc->best_idx;
-                k_extract<<<1, 32, 0, s>>>((const Spec*)d_spec_, R, F, bi, dc, (Leaf*)d_leaf_);
-                ++launches_;
-                ++own_launches_;
-                d2h_ += sizeof(Leaf);
-                CK(cudaMemcpyAsync(hl, d_leaf_, sizeof(Leaf), cudaMemcpyDeviceToHost, s));
-                hx[2] = LLONG_MAX;
-                CK(cudaMemcpyAsync(&dc->best_idx, hx + 2, sizeof(long long),
-                                   cudaMemcpyHostToDevice, s));
-                CK(cudaStreamSynchronize(s));
-                if (hl->nb < 0) throw std::runtime_error("extract did not reproduce the hit");
-                res.found = true;
-                res.leaf = *hl;
-                upto = bi;          // later items follow the hit in DFS order
-                drop_rest = true;   // so does every untouched pending item
-            }
-        }
-        // ---- next pending list: unfinished items (stable) then the untouched rest ----
-        long long nsel = 0;
-        if (upto > 0) {
-            size_t tb3 = tmp_bytes_;
-            CK(cub::DeviceSelect::Flagged(d_tmp_, tb3, F, d_flag_, Q, d_nsel_, (int)upto, s));
-            tb3 = tmp_bytes_;
-            CK(cub::DeviceSelect::Flagged(d_tmp_, tb3, FK, d_flag_, QK, d_nsel_, (int)upto, s));
-            launches_ += 2;
-            CK(cudaMemcpyAsync(hx + 3, d_nsel_, sizeof(long long), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            nsel = hx[3];
-        }
-        long long nrest = drop_rest ? 0 : rest;
-        if (nsel + nrest > cap) throw std::runtime_error("pending list exceeds frontier capacity");
-        if (nrest > 0) {
-            CK(cudaMemcpyAsync(Q + nsel, P + take, nrest * sizeof(Node), cudaMemcpyDeviceToDevice,
-                               s));
-            CK(cudaMemcpyAsync(QK + nsel, PK + take, nrest * sizeof(long long),
-                               cudaMemcpyDeviceToDevice, s));
-        }
-        std::swap(P, Q);
-        std::swap(PK, QK);
-        nP = nsel + nrest;
+    CK(cudaMemcpyAsync(d_spec_, hs, sizeof(Spec), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_ctl_, hc, sizeof(Ctl), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(Q, hr, sizeof(Cont), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(d_ready_, 0, cap * sizeof(int), s));
+    CK(cudaMemcpyAsync(d_ready_, hone, sizeof(int), cudaMemcpyHostToDevice, s));
+    h2d_ += sizeof(Spec) + sizeof(Ctl) + sizeof(Cont) + sizeof(int);
+    if (grid_ == 0) {
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search, 128, 0));
+        int sms = 148;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+        grid_ = std::max(1, per_sm) * sms;  // all resident: spin-waiting needs it
     }
+    CK(cudaEventRecord((cudaEvent_t)evk0_, s));
+    k_search<<<(unsigned)grid_, 128, 0, s>>>((const Spec*)d_spec_, R, Q, d_ready_,
+                                             (Ctl*)d_ctl_, (HitPath*)d_best_, (Leaf*)d_leaf_);
+    CK(cudaEventRecord((cudaEvent_t)evk1_, s));
+    ++launches_;
+    ++own_launches_;
+    ++st.rounds;
     CK(cudaMemcpyAsync(hc, d_ctl_, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+    d2h_ += sizeof(Ctl);
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    if (S.mode == MODE_FIRST && hc->has_hit && !hc->overflow) {
+        CK(cudaMemcpyAsync(hl, d_leaf_, sizeof(Leaf), cudaMemcpyDeviceToHost, s));
+        d2h_ += sizeof(Leaf);
+        CK(cudaStreamSynchronize(s));
+        res.found = true;
+        res.leaf = *hl;
+    }
     CK(cudaEventRecord((cudaEvent_t)ev1_, s));
     CK(cudaEventSynchronize((cudaEvent_t)ev1_));
-    CK(cudaGetLastError());
-    float ms = 0;
+    float kms = 0, ms = 0;
+    CK(cudaEventElapsedTime(&kms, (cudaEvent_t)evk0_, (cudaEvent_t)evk1_));
     CK(cudaEventElapsedTime(&ms, (cudaEvent_t)ev0_, (cudaEvent_t)ev1_));
+    ksearch_ms_ += kms;
+    ++ksearch_n_;
     search_ms_ += ms;
     if (hc->overflow) res.overflow = true;
     if (S.mode == MODE_MIN) {
+        if (hc->abort && !hc->overflow) res.aborted = true;
         union {
             unsigned long long u;
             double d;
@@ -606,6 +496,13 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     st.nodes += (long long)hc->nodes;
     st.leaves += (long long)hc->leaves;
     ++st.searches;
+    alg_bytes_ += (long long)hc->leaves * 24LL * S.k;  // k option rows x 3 fp64 per leaf
+    if (trace_)
+        std::fprintf(stderr, "[mosaic] %s k=%d thr=%.17g kernel=%.3fms total=%.3fms nodes=%llu "
+                             "leaves=%llu donated=%llu %s\n",
+                     S.mode == MODE_MIN ? "MIN  " : "FIRST", S.k,
+                     S.mode == MODE_MIN ? ub : S.theta, kms, ms, hc->nodes, hc->leaves,
+                     hc->q_tail - 1, res.found ? "hit" : (res.aborted ? "restart" : ""));
     return res;
 }
 

@@ -63,18 +63,18 @@ class Engine {
         ksearch_n_ = 0;
         h2d_ = 0;
         d2h_ = 0;
+        alg_bytes_ = 0;
     }
     long long own_launches() const { return own_launches_; }
     double ksearch_ms() const { return ksearch_ms_; }
     long long ksearch_launches() const { return ksearch_n_; }
     long long h2d_bytes() const { return h2d_; }
     long long d2h_bytes() const { return d2h_; }
+    long long alg_bytes() const { return alg_bytes_; }
     // device-side timing marks on the engine stream (bench.py)
     void mark(int which);
     double marked_ms();
-    long long budget = 1 << 14;   // DFS steps per frontier item per round
-    long long min_front = 8192;   // expand without searching below this many items
-    long long cap_front = 1 << 21;
+    long long cap_front = 1 << 20; // cursors in flight
 
   private:
     void ensure_front(long long n);
@@ -92,14 +92,11 @@ class Engine {
     void* d_spec_ = nullptr;
     void* d_ctl_ = nullptr;
     void* d_leaf_ = nullptr;
-    void* d_front_[3] = {nullptr, nullptr, nullptr};
-    long long* d_key_[3] = {nullptr, nullptr, nullptr};
-    long long* d_cnt_ = nullptr;
-    long long* d_off_ = nullptr;
-    unsigned char* d_flag_ = nullptr;
-    long long* d_nsel_ = nullptr;
-    void* d_tmp_ = nullptr;
-    size_t tmp_bytes_ = 0;
+    void* d_front_[1] = {nullptr};
+    int* d_ready_ = nullptr;
+    void* d_best_ = nullptr;
+    long long grid_ = 0;
+    bool trace_ = false;
     long long front_cap_ = 0;
     void* h_pin_ = nullptr;
     long long launches_ = 0;
@@ -108,7 +105,7 @@ class Engine {
     long long own_launches_ = 0;
     double ksearch_ms_ = 0;
     long long ksearch_n_ = 0;
-    long long h2d_ = 0, d2h_ = 0;
+    long long h2d_ = 0, d2h_ = 0, alg_bytes_ = 0;
     void* evk0_ = nullptr;
     void* evk1_ = nullptr;
     void* evm0_ = nullptr;

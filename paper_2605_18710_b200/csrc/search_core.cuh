@@ -79,12 +79,21 @@ struct Rows {
     const int* u;
 };
 
-// Frontier node: a partial allocation at `depth` (levels < depth placed).
-struct Node {
+// Work item: a DFS cursor.  Levels < depth are placed; `ph` says how to continue at
+// level `depth`: 0 = try the options after `oc`, 1 = try the compositions after `x` of
+// option opt[depth] (within [lo, hi]).  The root is {depth 0, ph 0, oc -1}.  Items
+// are ordered by `key`, which follows the reference DFS order.
+struct alignas(16) Cont {
+    unsigned long long key;
     uint16_t opt[MAXK];
-    uint16_t depth, nb;
-    uint16_t bsz[FB];
-    uint16_t bmk[FB];
+    uint16_t depth, nb, ph;
+    int16_t oc;
+    int used;
+    uint16_t bsz[MAXB];
+    uint16_t bmk[MAXB];
+    uint16_t x[MAXB];
+    uint16_t lo[MAXB];
+    uint16_t hi[MAXB];
 };
 
 // Leaf: options of every level plus the final block list (sizes, level masks).
@@ -223,6 +232,8 @@ MG_HD void block_stats(const Spec& S, const Rows& R, const uint16_t* opt, unsign
     }
 }
 
+MG_HD int hi_minus_x(const Walk& w, int i) { return (int)w.hi[i] - (int)w.x[i]; }
+
 // First composition in descending lexicographic order with x_b in [lo_b, hi_b].
 MG_HD bool first_comp(const uint16_t* lo, const uint16_t* hi, uint16_t* x, int nb, int d) {
     int R = d;
@@ -283,6 +294,21 @@ MG_HD bool last_intervals(const Walk& w, int o0, int nb, int d, double t, bool l
     return sumlo <= d && d <= sumhi;
 }
 
+// Does level l (at ph 1: current composition x of option opt[l]) have untried work:
+// another composition of this option, or a later option?
+MG_HD bool level_has_rest(const Spec& S, const Rows& R, const Walk& w, int l) {
+    if (w.opt[l] + 1 < S.lvl_n[l]) return true;
+    const int o0 = lvl_off(l);
+    const int nb = w.nb[l];
+    // next_comp succeeds iff some x_i > lo_i has slack to its right
+    int slack = hi_minus_x(w, o0 + nb - 1);
+    for (int i = nb - 2; i >= 0; --i) {
+        if (w.x[o0 + i] > w.lo[o0 + i] && slack >= 1) return true;
+        slack += hi_minus_x(w, o0 + i);
+    }
+    return false;
+}
+
 // Stats of the blocks of level j into the parent scratch.
 MG_HD void parent_stats(const Spec& S, const Rows& R, Walk& w, int j) {
     const int o0 = lvl_off(j);
@@ -292,22 +318,33 @@ MG_HD void parent_stats(const Spec& S, const Rows& R, Walk& w, int j) {
     w.ps_lvl = j;
 }
 
-// The per-thread DFS.  Starts at depth d0 (w holds opt[<d0], blocks of level d0);
-// stop < k: emit every surviving node of depth `stop` (frontier expansion);
-// stop == k: run to the leaves.  Returns 1 on a FIRST hit, 2 on abort, 0 when done.
+// The per-thread DFS from a loaded cursor at depth d0 (see Cont).  Returns 1 on a
+// FIRST hit, 2 when abandoned (a better FIRST hit exists / MIN restart), 3 when the
+// step budget ran out and the remaining work was handed back as cursors
+// (h.split), 0 when the subtree is exhausted.
 template <class H>
-MG_HD int dfs(const Spec& S, const Rows& R, Walk& w, int d0, int stop, H& h) {
+MG_HD int dfs(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
     const int k = S.k;
     const int GL = S.G * S.L;
     int j = d0;
-    w.ph[j] = 0;
-    w.oc[j] = -1;
+    int floor_lvl = d0;  // levels below this were handed to other threads
     w.ps_lvl = -1;
-    while (j >= d0) {
+    while (j >= floor_lvl) {
         const int o0 = lvl_off(j);
         const int nb = w.nb[j];
         if (w.ph[j] == 0) {
-            if (h.abort()) return 2;
+            h.level(j);
+            int ab = h.abort();
+            if (ab == 1) {
+                h.split(w, floor_lvl, j);
+                return 3;
+            }
+            if (ab == 2) return 2;
+            if (ab == 3) {
+                // hand the shallowest level that still has untried work to an idle thread
+                while (floor_lvl < j && !level_has_rest(S, R, w, floor_lvl)) ++floor_lvl;
+                if (floor_lvl < j && h.donate(w, floor_lvl)) ++floor_lvl;
+            }
             const double thr = h.thr(S);
             const int n = S.lvl_n[j], off = S.lvl_off[j];
             int o = w.oc[j] + 1;
@@ -555,10 +592,6 @@ MG_HD int dfs(const Spec& S, const Rows& R, Walk& w, int d0, int stop, H& h) {
             if (!ok) prune = true;
         }
         if (prune) continue;
-        if (j + 1 == stop) {
-            h.emit(w, j + 1);
-            continue;
-        }
         ++j;
         w.ph[j] = 0;
         w.oc[j] = -1;
@@ -566,26 +599,115 @@ MG_HD int dfs(const Spec& S, const Rows& R, Walk& w, int d0, int stop, H& h) {
     return 0;
 }
 
-// Load a frontier node into a walk.
-MG_HD void load_node(const Node& nd, Walk& w) {
-    int dep = nd.depth;
-    for (int l = 0; l < dep; ++l) w.opt[l] = nd.opt[l];
-    int o = lvl_off(dep);
-    w.nb[dep] = nd.nb;
-    for (int b = 0; b < nd.nb; ++b) {
-        w.bsz[o + b] = nd.bsz[b];
-        w.bmk[o + b] = nd.bmk[b];
+// Load a cursor into a walk.
+MG_HD void load_cont(const Cont& c, Walk& w) {
+    const int dep = c.depth;
+    for (int l = 0; l < dep; ++l) w.opt[l] = c.opt[l];
+    const int o = lvl_off(dep);
+    w.nb[dep] = c.nb;
+    w.used[dep] = c.used;
+    w.ph[dep] = (uint8_t)c.ph;
+    w.oc[dep] = c.oc;
+    if (c.ph) w.opt[dep] = (uint16_t)c.oc;
+    for (int b = 0; b < c.nb; ++b) {
+        w.bsz[o + b] = c.bsz[b];
+        w.bmk[o + b] = c.bmk[b];
+        if (c.ph) {
+            w.x[o + b] = c.x[b];
+            w.lo[o + b] = c.lo[b];
+            w.hi[o + b] = c.hi[b];
+        }
+    }
+    // Rebuild the blocks and compositions of every ancestor level: level l+1 lists each
+    // parent block as (taken part, rest part), adjacent, with masks differing in bit l.
+    for (int l = dep - 1; l >= 0; --l) {
+        const int oc1 = lvl_off(l + 1), ol = lvl_off(l);
+        const unsigned bit = 1u << l;
+        int nbl = 0;
+        for (int b = 0; b < w.nb[l + 1];) {
+            const unsigned key = w.bmk[oc1 + b] & ~bit;
+            int size = 0, taken = 0;
+            while (b < w.nb[l + 1] && (w.bmk[oc1 + b] & ~bit) == key) {
+                size += w.bsz[oc1 + b];
+                if (w.bmk[oc1 + b] & bit) taken += w.bsz[oc1 + b];
+                ++b;
+            }
+            w.bsz[ol + nbl] = (uint16_t)size;
+            w.bmk[ol + nbl] = (uint16_t)key;
+            w.x[ol + nbl] = (uint16_t)taken;
+            ++nbl;
+        }
+        w.nb[l] = (uint16_t)nbl;
     }
 }
 
-MG_HD void store_node(const Walk& w, int dep, Node& nd) {
-    for (int l = 0; l < MAXK; ++l) nd.opt[l] = l < dep ? w.opt[l] : 0;
-    nd.depth = (uint16_t)dep;
-    int o = lvl_off(dep);
-    nd.nb = w.nb[dep];
-    for (int b = 0; b < nd.nb; ++b) {
-        nd.bsz[b] = w.bsz[o + b];
-        nd.bmk[b] = w.bmk[o + b];
+// Position of a FIRST hit in the reference DFS order: (option, composition) per level.
+struct HitPath {
+    uint16_t opt[MAXK];
+    uint16_t nb[MAXK];
+    uint16_t x[MAXK][MAXB];
+};
+
+// -1: path H precedes the walk's leaf path (levels 0..j), +1 follows it, 0 equal.
+template <class HP>
+MG_HD int path_cmp(const HP* H, const Walk& w, int j) {
+    for (int l = 0; l <= j; ++l) {
+        int ho = H->opt[l];
+        if (ho != w.opt[l]) return ho < w.opt[l] ? -1 : 1;
+        const int o0 = lvl_off(l);
+        for (int b = 0; b < w.nb[l]; ++b) {
+            int hx = H->x[l][b], wx = w.x[o0 + b];
+            if (hx != wx) return hx > wx ? -1 : 1;  // larger count first
+        }
+    }
+    return 0;
+}
+
+// Does H precede every leaf the walk can still reach?  Levels < j are fixed at their
+// current (option, composition); at level j only the options after oc[j] remain.
+template <class HP>
+MG_HD bool path_precedes_rest(const HP* H, const Walk& w, int j) {
+    for (int l = 0; l < j; ++l) {
+        int ho = H->opt[l];
+        if (ho != w.opt[l]) return ho < w.opt[l];
+        const int o0 = lvl_off(l);
+        for (int b = 0; b < w.nb[l]; ++b) {
+            int hx = H->x[l][b], wx = w.x[o0 + b];
+            if (hx != wx) return hx > wx;
+        }
+    }
+    return (int)H->opt[j] <= w.oc[j];
+}
+
+template <class HP>
+MG_HD void path_store(HP* H, const Walk& w, int j) {
+    for (int l = 0; l <= j; ++l) {
+        H->opt[l] = w.opt[l];
+        H->nb[l] = w.nb[l];
+        const int o0 = lvl_off(l);
+        for (int b = 0; b < w.nb[l]; ++b) H->x[l][b] = w.x[o0 + b];
+    }
+}
+
+// Cursor for "the rest of level l": options after oc[l] (ph 0) or compositions after
+// the current x (ph 1).
+MG_HD void store_cont(const Walk& w, int l, int ph, unsigned long long key, Cont& c) {
+    c.key = key;
+    for (int i = 0; i < MAXK; ++i) c.opt[i] = i < l ? w.opt[i] : 0;
+    c.depth = (uint16_t)l;
+    c.nb = w.nb[l];
+    c.ph = (uint16_t)ph;
+    c.oc = ph ? (int16_t)w.opt[l] : w.oc[l];
+    c.used = w.used[l];
+    const int o = lvl_off(l);
+    for (int b = 0; b < c.nb; ++b) {
+        c.bsz[b] = w.bsz[o + b];
+        c.bmk[b] = w.bmk[o + b];
+        if (ph) {
+            c.x[b] = w.x[o + b];
+            c.lo[b] = w.lo[o + b];
+            c.hi[b] = w.hi[o + b];
+        }
     }
 }
 

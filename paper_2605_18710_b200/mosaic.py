@@ -121,7 +121,7 @@ EXPORTS = [
     "mosaic_gpu_merge_records", "mosaic_gpu_launch_count", "mosaic_gpu_search_ms",
     "mosaic_gpu_reset_counters", "mosaic_gpu_synth_problem", "mosaic_gpu_free_problem",
     "mosaic_gpu_own_launches", "mosaic_gpu_ksearch_ms", "mosaic_gpu_ksearch_launches",
-    "mosaic_gpu_h2d_bytes", "mosaic_gpu_d2h_bytes", "mosaic_gpu_mark", "mosaic_gpu_marked_ms",
+    "mosaic_gpu_h2d_bytes", "mosaic_gpu_d2h_bytes", "mosaic_gpu_mark", "mosaic_gpu_marked_ms", "mosaic_gpu_alg_bytes",
 ]
 
 _lib = None
@@ -174,6 +174,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "mosaic_gpu_d2h_bytes": (C.c_int64, [vp]),
         "mosaic_gpu_mark": (None, [vp, C.c_int]),
         "mosaic_gpu_marked_ms": (C.c_double, [vp]),
+        "mosaic_gpu_alg_bytes": (C.c_int64, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -500,7 +501,8 @@ class Planner:
                 "ksearch_launches": L.mosaic_gpu_ksearch_launches(self._ctx),
                 "h2d_bytes": L.mosaic_gpu_h2d_bytes(self._ctx),
                 "d2h_bytes": L.mosaic_gpu_d2h_bytes(self._ctx),
-                "device_ms": L.mosaic_gpu_search_ms(self._ctx)}
+                "device_ms": L.mosaic_gpu_search_ms(self._ctx),
+                "alg_bytes": L.mosaic_gpu_alg_bytes(self._ctx)}
 
     def mark(self, which: int) -> None:
         load_library().mosaic_gpu_mark(self._ctx, which)
