@@ -21,6 +21,7 @@
 
 #include "engine.hpp"
 #include "search_core.cuh"
+#include "search_warp.cuh"
 
 namespace mg {
 
@@ -50,7 +51,9 @@ struct Ctl {
     alignas(128) unsigned long long nodes, leaves;
 };
 
-struct DevHooks {
+// Hooks of one walker (a warp).  Everything that steers control flow is decided by
+// lane 0 and broadcast, so the warp stays converged.
+struct WarpHooks {
     Ctl* ctl;
     int mode;
     long long steps;
@@ -64,26 +67,7 @@ struct DevHooks {
     const Walk* w;
     int cur_level;
 
-    // 0 continue, 2 abandon (MIN restart, or a FIRST hit precedes everything left here),
-    // 3 idle threads are waiting: donate shallow work
-    __device__ int abort() {
-        ++steps;
-        if (*(volatile int*)&ctl->abort) return 2;
-        if ((steps & 15) == 0) {
-            if (mode == MODE_FIRST && *(volatile int*)&ctl->has_hit && hit_precedes()) return 2;
-            unsigned int idle = *(volatile unsigned int*)&ctl->idle;
-            if (idle) {
-                unsigned long long qn = *(volatile unsigned long long*)&ctl->q_tail -
-                                        *(volatile unsigned long long*)&ctl->q_head;
-                if (qn < idle) return 3;
-            }
-        }
-        return 0;
-    }
-    // does the published hit come before every leaf this thread can still reach?
-    // Walk state: levels < cur_level fixed at (opt, x); at cur_level the options after
-    // oc[cur_level] remain.
-    __device__ bool hit_precedes() {
+    __device__ bool hit_precedes() {  // lane 0 only
         int v0 = *(volatile int*)&ctl->ver;
         if (v0 & 1) return false;
         __threadfence();
@@ -92,126 +76,186 @@ struct DevHooks {
         int v1 = *(volatile int*)&ctl->ver;
         return v0 == v1 && before;
     }
-    // publish a FIRST hit at the last level if it precedes the current best
-    __device__ void hit(const Walk& wk, int j, double v) {
-        while (atomicCAS(&ctl->lock, 0, 1) != 0) __nanosleep(64);
-        __threadfence();
-        bool better = !*(volatile int*)&ctl->has_hit ||
-                      path_cmp((const volatile HitPath*)best, wk, j) > 0;
-        if (better) {
-            atomicAdd(&ctl->ver, 1);
-            __threadfence();
-            path_store((volatile HitPath*)best, wk, j);
-            store_leaf(wk, j, v, *leaf_out);
-            ctl->has_hit = 1;
-            __threadfence();
-            atomicAdd(&ctl->ver, 1);
+    // 0 continue, 2 abandon (MIN restart, or a FIRST hit precedes all that is left),
+    // 3 idle walkers are waiting: donate shallow work
+    __device__ int abort() {
+        ++steps;
+        int code = 0;
+        if (lane_id() == 0) {
+            if (*(volatile int*)&ctl->abort) {
+                code = 2;
+            } else if ((steps & 7) == 0) {
+                if (mode == MODE_FIRST && *(volatile int*)&ctl->has_hit && hit_precedes()) {
+                    code = 2;
+                } else {
+                    unsigned int idle = *(volatile unsigned int*)&ctl->idle;
+                    if (idle) {
+                        unsigned long long qn = *(volatile unsigned long long*)&ctl->q_tail -
+                                                *(volatile unsigned long long*)&ctl->q_head;
+                        if (qn < idle) code = 3;
+                    }
+                }
+            }
         }
-        __threadfence();
-        atomicExch(&ctl->lock, 0);
+        return __shfl_sync(FULLW, code, 0);
     }
-    __device__ void split(const Walk&, int, int) {}
+    __device__ void hit(const Walk& wk, int j, double v) {
+        if (lane_id() == 0) {
+            while (atomicCAS(&ctl->lock, 0, 1) != 0) __nanosleep(64);
+            __threadfence();
+            bool better = !*(volatile int*)&ctl->has_hit ||
+                          path_cmp((const volatile HitPath*)best, wk, j) > 0;
+            if (better) {
+                atomicAdd(&ctl->ver, 1);
+                __threadfence();
+                path_store((volatile HitPath*)best, wk, j);
+                store_leaf(wk, j, v, *leaf_out);
+                ctl->has_hit = 1;
+                __threadfence();
+                atomicAdd(&ctl->ver, 1);
+            }
+            __threadfence();
+            atomicExch(&ctl->lock, 0);
+        }
+        __syncwarp();
+    }
     // push the cursor "rest of level l" onto the ring queue (ticket t -> slot t % cap,
     // published by writing ready[slot] = t + 1)
     __device__ bool donate(const Walk& wk, int l) {
-        unsigned long long t = *(volatile unsigned long long*)&ctl->q_tail;
-        while (true) {
-            unsigned long long head = *(volatile unsigned long long*)&ctl->q_head;
-            if (t + 1 - head > ctl->q_cap) return false;  // ring full
-            unsigned long long old = atomicCAS(&ctl->q_tail, t, t + 1);
-            if (old == t) break;
-            t = old;
+        long long slot = -1;
+        unsigned long long t = 0;
+        if (lane_id() == 0) {
+            t = *(volatile unsigned long long*)&ctl->q_tail;
+            while (true) {
+                unsigned long long head = *(volatile unsigned long long*)&ctl->q_head;
+                if (t + 1 - head > ctl->q_cap) break;  // ring full
+                unsigned long long old = atomicCAS(&ctl->q_tail, t, t + 1);
+                if (old == t) {
+                    slot = (long long)(t % ctl->q_cap);
+                    atomicAdd(&ctl->outstanding, 1ULL);
+                    break;
+                }
+                t = old;
+            }
         }
-        atomicAdd(&ctl->outstanding, 1ULL);
-        const unsigned long long slot = t % ctl->q_cap;
-        store_cont(wk, l, 1, 0, q[slot]);
-        __threadfence();
-        atomicExch(&ready[slot], (int)(t + 1));
+        slot = __shfl_sync(FULLW, slot, 0);
+        if (slot < 0) return false;
+        store_cont_warp(wk, l, 1, q[slot]);
+        __threadfence();  // every lane's part of the cursor is visible ...
+        __syncwarp();
+        if (lane_id() == 0) {
+            __threadfence();
+            atomicExch(&ready[slot], (int)(t + 1));  // ... before it is published
+        }
+        __syncwarp();
         return true;
     }
-    __device__ double load_inc() {
-        return __longlong_as_double(*(volatile long long*)&ctl->inc);
+    __device__ double bcast_inc() {
+        double I = 0.0;
+        if (lane_id() == 0) I = __longlong_as_double(*(volatile long long*)&ctl->inc);
+        return __shfl_sync(FULLW, I, 0);
     }
     __device__ double thr(const Spec& S) {
         if (mode != MODE_MIN) return S.thp;
         if ((refresh++ & 15) == 0) {
-            double I = load_inc();
+            double I = bcast_inc();
             inc_cache = I < inc_cache ? I : inc_cache;
         }
         double t = inc_cache >= POS_INF ? POS_INF : inc_cache * (1.0 - TIE_EPS);
         return t < S.thp ? t : S.thp;
     }
     __device__ double incumbent() {
-        double I = load_inc();
+        double I = bcast_inc();
         inc_cache = I < inc_cache ? I : inc_cache;
         return inc_cache;
     }
     __device__ void improve(double v) {
-        atomicMin(&ctl->inc, (unsigned long long)__double_as_longlong(v));
+        if (lane_id() == 0) {
+            atomicMin(&ctl->inc, (unsigned long long)__double_as_longlong(v));
+            if (v < ctl->abort_below) atomicExch(&ctl->abort, 1);
+        }
         if (v < inc_cache) inc_cache = v;
-        if (v < ctl->abort_below) atomicExch(&ctl->abort, 1);
+        __syncwarp();
     }
     __device__ void count_node() { ++nodes; }
     __device__ void count_leaf() { ++leaves; }
     __device__ void overflow() {
-        atomicExch(&ctl->overflow, 1);
-        atomicExch(&ctl->abort, 1);
+        if (lane_id() == 0) {
+            atomicExch(&ctl->overflow, 1);
+            atomicExch(&ctl->abort, 1);
+        }
     }
     __device__ void level(int j) { cur_level = j; }
 };
 
-__device__ __forceinline__ void load_spec(const Spec* g, Spec* s) {
-    const int n = sizeof(Spec) / 4;
-    const int* src = reinterpret_cast<const int*>(g);
-    int* dst = reinterpret_cast<int*>(s);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
-    __syncthreads();
-}
+constexpr int WPC = 2;  // walkers (warps) per CTA
 
-// One resident persistent grid per search with a shared cursor queue.  Threads pop
-// cursors; a busy thread that sees idle threads and a short queue donates the untried
-// siblings of every level above its current one and keeps the current level.
-// `outstanding` counts queued + in-flight cursors; all threads exit when it reaches 0.
+__host__ __device__ constexpr size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+constexpr size_t SMEM_SPEC = align_up(sizeof(Spec), 16);
+constexpr size_t SMEM_WALK = align_up(sizeof(Walk), 16);
+constexpr size_t SMEM_SCR = align_up(sizeof(WScratch), 16);
+constexpr size_t SMEM_BYTES = SMEM_SPEC + WPC * (SMEM_WALK + SMEM_SCR);
+
+// One resident persistent grid per stage search.  Each warp is a walker: it pops a
+// cursor from the shared ring queue and runs the warp-cooperative DFS on it; a busy
+// walker that sees idle ones and a short queue donates its shallowest untried level.
+// `outstanding` counts queued + in-flight cursors; every walker exits when it hits 0.
 //   MIN:   shared incumbent (atomicMin on the fp64 bits), tie band TIE_EPS.
 //   FIRST: hits are ordered by their reference-DFS path; the earliest is kept under a
 //          seqlock, and work that lies after it is abandoned.
-__global__ void __launch_bounds__(128) k_search(const Spec* Sg, Rows R, Cont* Q, int* ready,
-                                                Ctl* ctl, HitPath* best, Leaf* leaf_out) {
-    __shared__ Spec S;
-    load_spec(Sg, &S);
-    Walk w;
+__global__ void __launch_bounds__(32 * WPC) k_search(const Spec* Sg, Rows R, Cont* Q, int* ready,
+                                                     Ctl* ctl, HitPath* best, Leaf* leaf_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    Spec& S = *reinterpret_cast<Spec*>(smem);
+    {
+        const int n = sizeof(Spec) / 4;
+        const int* src = reinterpret_cast<const int*>(Sg);
+        int* dst = reinterpret_cast<int*>(smem);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+        __syncthreads();
+    }
+    const int wid = threadIdx.x >> 5;
+    const int lane = lane_id();
+    Walk& w = *reinterpret_cast<Walk*>(smem + SMEM_SPEC + wid * SMEM_WALK);
+    WScratch& sc = *reinterpret_cast<WScratch*>(smem + SMEM_SPEC + WPC * SMEM_WALK + wid * SMEM_SCR);
     unsigned long long nodes = 0, leaves = 0;
     while (true) {
-        long long slot = -1;
-        bool idle = false;
-        unsigned backoff = 128;
-        while (true) {
-            if (*(volatile int*)&ctl->abort) break;
-            unsigned long long h = *(volatile unsigned long long*)&ctl->q_head;
-            unsigned long long t = *(volatile unsigned long long*)&ctl->q_tail;
-            if (h < t) {
-                if (atomicCAS(&ctl->q_head, h, h + 1) == h) {
-                    slot = (long long)h;
-                    break;
+        long long ticket = -1;
+        if (lane == 0) {
+            bool idle = false;
+            unsigned backoff = 128;
+            while (true) {
+                if (*(volatile int*)&ctl->abort) break;
+                unsigned long long h = *(volatile unsigned long long*)&ctl->q_head;
+                unsigned long long t = *(volatile unsigned long long*)&ctl->q_tail;
+                if (h < t) {
+                    if (atomicCAS(&ctl->q_head, h, h + 1) == h) {
+                        ticket = (long long)h;
+                        break;
+                    }
+                    continue;
                 }
-                continue;
+                if (*(volatile unsigned long long*)&ctl->outstanding == 0) break;
+                if (!idle) {
+                    atomicAdd(&ctl->idle, 1u);
+                    idle = true;
+                }
+                __nanosleep(backoff);
+                backoff = backoff < 4096 ? backoff * 2 : 4096;
             }
-            if (*(volatile unsigned long long*)&ctl->outstanding == 0) break;
-            if (!idle) {
-                atomicAdd(&ctl->idle, 1u);
-                idle = true;
+            if (idle) atomicSub(&ctl->idle, 1u);
+            if (ticket >= 0) {
+                const long long slot = (long long)((unsigned long long)ticket % ctl->q_cap);
+                while (*(volatile int*)&ready[slot] != (int)(ticket + 1)) __nanosleep(32);
+                __threadfence();
             }
-            __nanosleep(backoff);
-            backoff = backoff < 4096 ? backoff * 2 : 4096;
         }
-        if (idle) atomicSub(&ctl->idle, 1u);
-        if (slot < 0) break;
-        const long long ticket = slot;
-        slot = (long long)((unsigned long long)ticket % ctl->q_cap);
-        while (*(volatile int*)&ready[slot] != (int)(ticket + 1)) __nanosleep(32);
+        ticket = __shfl_sync(FULLW, ticket, 0);
+        if (ticket < 0) break;
+        const long long slot = (long long)((unsigned long long)ticket % ctl->q_cap);
         __threadfence();
-        load_cont(Q[slot], w);
-        DevHooks h;
+        load_cont_warp(Q[slot], w);
+        WarpHooks h;
         h.ctl = ctl;
         h.mode = S.mode;
         h.steps = 0;
@@ -223,17 +267,23 @@ __global__ void __launch_bounds__(128) k_search(const Spec* Sg, Rows R, Cont* Q,
         h.nodes = 0;
         h.leaves = 0;
         h.w = &w;
-        h.cur_level = Q[slot].depth;
+        h.cur_level = 0;
         h.inc_cache = POS_INF;
-        h.inc_cache = h.load_inc();
-        dfs(S, R, w, Q[slot].depth, h);
+        h.inc_cache = h.bcast_inc();
+        const int d0 = Q[slot].depth;
+        dfs_warp(S, R, w, sc, d0, h);
         nodes += h.nodes;
         leaves += h.leaves;
-        __threadfence();
-        atomicAdd(&ctl->outstanding, ~0ULL);  // -1
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicAdd(&ctl->outstanding, ~0ULL);  // -1
+        }
     }
-    atomicAdd(&ctl->nodes, nodes);
-    atomicAdd(&ctl->leaves, leaves);
+    if (lane == 0) {
+        atomicAdd(&ctl->nodes, nodes);
+        atomicAdd(&ctl->leaves, leaves);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -451,15 +501,18 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     CK(cudaMemcpyAsync(d_ready_, hone, sizeof(int), cudaMemcpyHostToDevice, s));
     h2d_ += sizeof(Spec) + sizeof(Ctl) + sizeof(Cont) + sizeof(int);
     if (grid_ == 0) {
+        CK(cudaFuncSetAttribute(k_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)SMEM_BYTES));
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search, 128, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search, 32 * WPC, SMEM_BYTES));
         int sms = 148;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
         grid_ = std::max(1, per_sm) * sms;  // all resident: spin-waiting needs it
     }
     CK(cudaEventRecord((cudaEvent_t)evk0_, s));
-    k_search<<<(unsigned)grid_, 128, 0, s>>>((const Spec*)d_spec_, R, Q, d_ready_,
-                                             (Ctl*)d_ctl_, (HitPath*)d_best_, (Leaf*)d_leaf_);
+    k_search<<<(unsigned)grid_, 32 * WPC, SMEM_BYTES, s>>>((const Spec*)d_spec_, R, Q, d_ready_,
+                                                           (Ctl*)d_ctl_, (HitPath*)d_best_,
+                                                           (Leaf*)d_leaf_);
     CK(cudaEventRecord((cudaEvent_t)evk1_, s));
     ++launches_;
     ++own_launches_;

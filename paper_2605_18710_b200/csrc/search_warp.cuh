@@ -1,0 +1,544 @@
+// search_warp.cuh — warp-cooperative version of the canonical-block DFS (sm_100a).
+//
+// One warp is one walker.  Its Walk lives in shared memory; the DFS control flow is
+// warp-uniform (every lane runs the same scalar code on the same shared state, and
+// every value read from global memory that steers control flow is read by lane 0 and
+// broadcast).  The per-GPU-block work — block statistics, admissible take intervals,
+// composition stepping (prefix scans), child construction, look-ahead counts and the
+// closed-form last level — is spread over the 32 lanes, so irregular trees run
+// without intra-warp divergence.  Semantics are exactly those of search_core.cuh.
+#pragma once
+#include "search_core.cuh"
+
+namespace mg {
+
+constexpr unsigned FULLW = 0xffffffffu;
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int wsum(int v) { return __reduce_add_sync(FULLW, v); }
+__device__ __forceinline__ int wmaxi(int v) { return __reduce_max_sync(FULLW, v); }
+__device__ __forceinline__ bool wany(bool p) { return __any_sync(FULLW, p); }
+__device__ __forceinline__ double wmaxd(double v) {
+    for (int o = 16; o; o >>= 1) {
+        double t = __shfl_xor_sync(FULLW, v, o);
+        v = t > v ? t : v;
+    }
+    return v;
+}
+__device__ __forceinline__ int wscan_incl(int v) {
+    const int lane = lane_id();
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(FULLW, v, o);
+        if (lane >= o) v += y;
+    }
+    return v;
+}
+
+struct WScratch {  // per-walker scratch for prefix sums
+    int sa[MAXB];
+    int sb[MAXB];
+};
+
+__device__ __forceinline__ void parent_stats_warp(const Spec& S, const Rows& R, Walk& w, int j) {
+    const int o0 = lvl_off(j);
+    for (int b = lane_id(); b < w.nb[j]; b += 32)
+        block_stats(S, R, w.opt, w.bmk[o0 + b], j, w.pu[b], w.pm[b], w.psum[b], w.pmb[b], w.pP[b],
+                    w.pmx[b]);
+    __syncwarp();
+}
+
+// x_b = lo_b + min(room_b, max(0, R - sum_{t<b} room_t)),  R = d - sum lo
+__device__ __forceinline__ bool first_comp_warp(Walk& w, int o0, int nb, int d) {
+    const int lane = lane_id();
+    int mylo = 0;
+    for (int b = lane; b < nb; b += 32) mylo += w.lo[o0 + b];
+    const int R = d - wsum(mylo);
+    if (R < 0) return false;
+    int carry = 0;
+    for (int c = 0; c < nb; c += 32) {
+        const int b = c + lane;
+        const int room = b < nb ? (int)w.hi[o0 + b] - (int)w.lo[o0 + b] : 0;
+        const int inc = wscan_incl(room);
+        const int ex = carry + inc - room;
+        if (b < nb) {
+            int left = R - ex;
+            left = left > 0 ? left : 0;
+            w.x[o0 + b] = (uint16_t)(w.lo[o0 + b] + (room < left ? room : left));
+        }
+        carry += __shfl_sync(FULLW, inc, 31);
+    }
+    __syncwarp();
+    return carry >= R;
+}
+
+// next composition in descending lexicographic order within [lo, hi]
+__device__ __forceinline__ bool next_comp_warp(Walk& w, WScratch& sc, int o0, int nb) {
+    if (nb < 2) return false;
+    const int lane = lane_id();
+    // inclusive prefix of slack_t = hi_t - x_t and extra_t = x_t - lo_t
+    int cs = 0, ce = 0;
+    for (int c = 0; c < nb; c += 32) {
+        const int b = c + lane;
+        const int sl = b < nb ? (int)w.hi[o0 + b] - (int)w.x[o0 + b] : 0;
+        const int ex = b < nb ? (int)w.x[o0 + b] - (int)w.lo[o0 + b] : 0;
+        const int is = wscan_incl(sl), ie = wscan_incl(ex);
+        if (b < nb) {
+            sc.sa[b] = cs + is;
+            sc.sb[b] = ce + ie;
+        }
+        cs += __shfl_sync(FULLW, is, 31);
+        ce += __shfl_sync(FULLW, ie, 31);
+    }
+    __syncwarp();
+    // rightmost i <= nb-2 with x_i > lo_i and slack to its right
+    int best = -1;
+    for (int i = lane; i < nb - 1; i += 32)
+        if (w.x[o0 + i] > w.lo[o0 + i] && cs - sc.sa[i] >= 1) best = i;
+    const int is = wmaxi(best);
+    if (is < 0) return false;
+    const int R = (ce - sc.sb[is]) + 1;  // extra to the right of i*, plus the one unit
+    __syncwarp();
+    if (lane == 0) w.x[o0 + is] -= 1;
+    int carry = 0;
+    for (int c = 0; c < nb; c += 32) {
+        const int b = c + lane;
+        const bool mine = b < nb && b > is;
+        const int room = mine ? (int)w.hi[o0 + b] - (int)w.lo[o0 + b] : 0;
+        const int inc = wscan_incl(room);
+        const int ex = carry + inc - room;
+        if (mine) {
+            int left = R - ex;
+            left = left > 0 ? left : 0;
+            w.x[o0 + b] = (uint16_t)(w.lo[o0 + b] + (room < left ? room : left));
+        }
+        carry += __shfl_sync(FULLW, inc, 31);
+    }
+    __syncwarp();
+    return true;
+}
+
+// Last level: admissible intervals at threshold t (le: <=, else <); feasibility of d.
+__device__ __forceinline__ bool last_feasible_warp(const Walk& w, int o0, int nb, int d, double t,
+                                                   bool le, const double* rest,
+                                                   const double* take) {
+    int lo = 0, hi = 0;
+    bool dead = false;
+    for (int b = lane_id(); b < nb; b += 32) {
+        const int s = w.bsz[o0 + b];
+        const bool rok = le ? rest[b] <= t : rest[b] < t;
+        const bool tok = w.hi[o0 + b] && (le ? take[b] <= t : take[b] < t);
+        if (rok && tok) {
+            hi += s;
+        } else if (rok) {
+        } else if (tok) {
+            lo += s;
+            hi += s;
+        } else {
+            dead = true;
+        }
+    }
+    const int L = wsum(lo), H = wsum(hi);
+    return !wany(dead) && L <= d && d <= H;
+}
+
+__device__ __forceinline__ bool level_has_rest_warp(const Spec& S, const Walk& w, WScratch& sc,
+                                                    int l) {
+    if (w.opt[l] + 1 < S.lvl_n[l]) return true;
+    const int lane = lane_id();
+    const int o0 = lvl_off(l);
+    const int nb = w.nb[l];
+    int cs = 0;
+    for (int c = 0; c < nb; c += 32) {
+        const int b = c + lane;
+        const int sl = b < nb ? (int)w.hi[o0 + b] - (int)w.x[o0 + b] : 0;
+        const int is = wscan_incl(sl);
+        if (b < nb) sc.sa[b] = cs + is;
+        cs += __shfl_sync(FULLW, is, 31);
+    }
+    __syncwarp();
+    bool any = false;
+    for (int i = lane; i < nb - 1; i += 32)
+        if (w.x[o0 + i] > w.lo[o0 + i] && cs - sc.sa[i] >= 1) any = true;
+    const bool r = wany(any);
+    __syncwarp();
+    return r;
+}
+
+template <class H>
+__device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, WScratch& sc, int d0, H& h) {
+    const int lane = lane_id();
+    const int k = S.k;
+    const int GL = S.G * S.L;
+    int j = d0;
+    int floor_lvl = d0;
+    int ps_lvl = -1;
+    while (j >= floor_lvl) {
+        const int o0 = lvl_off(j);
+        const int nb = w.nb[j];
+        if (w.ph[j] == 0) {
+            h.level(j);
+            const int ab = h.abort();
+            if (ab == 2) return 2;
+            if (ab == 3) {
+                while (floor_lvl < j && !level_has_rest_warp(S, w, sc, floor_lvl)) ++floor_lvl;
+                if (floor_lvl < j && h.donate(w, floor_lvl)) ++floor_lvl;
+            }
+            const double thr = h.thr(S);
+            const int n = S.lvl_n[j], off = S.lvl_off[j];
+            int o = w.oc[j] + 1;
+            bool got = false;
+            for (; o < n; ++o) {
+                const int r = off + o;
+                const int t = opt_test(S, R, r, thr);
+                if (t == 2) break;
+                if (t == 1) continue;
+                if (w.used[j] + R.d[r] * R.u[r] + S.suffix_min[j + 1] > GL) continue;
+                got = true;
+                break;
+            }
+            __syncwarp();
+            if (!got) {
+                --j;
+                continue;
+            }
+            if (lane == 0) {
+                w.oc[j] = (int16_t)o;
+                w.opt[j] = (uint16_t)o;
+            }
+            __syncwarp();
+            const int r = off + o;
+            const int dd = R.d[r], uu = R.u[r];
+            const double ff = R.fp[r], bo = R.B[r], ba = R.base[r];
+            const bool last = j == k - 1;
+            if (ps_lvl != j) {
+                parent_stats_warp(S, R, w, j);
+                ps_lvl = j;
+                if (last) {
+                    for (int b = lane; b < nb; b += 32)
+                        w.cm[b] = w.bmk[o0 + b] ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] +
+                                                      (S.additive ? 0.0 : S.e3 * w.pP[b])
+                                                : NEG_INF;
+                    __syncwarp();
+                }
+            }
+            // per-block admissible take interval
+            int mylo = 0, myhi = 0;
+            bool mydead = false;
+            for (int b = lane; b < nb; b += 32) {
+                const int s = w.bsz[o0 + b];
+                const bool el = w.pu[b] + uu <= S.L && !(w.pm[b] + ff > S.cap_slack);
+                bool tok = el, rok = true;
+                if (!last && S.nonneg) {
+                    if (el) {
+                        double lbt;
+                        if (S.include_self) {
+                            const double mb = w.pmb[b] > ba ? w.pmb[b] : ba;
+                            lbt = mb + S.e1 + S.e2 * (w.psum[b] + bo) +
+                                  envelope(S, j + 1, w.pP[b] * bo);
+                        } else {
+                            const double bx = ba - S.e2 * bo;
+                            const double mx = w.pmx[b] > bx ? w.pmx[b] : bx;
+                            lbt = mx + S.e1 + S.e2 * (w.psum[b] + bo) + envelope(S, j + 1, 0.0);
+                        }
+                        tok = !(lbt > thr);
+                    }
+                    if (w.bmk[o0 + b]) {
+                        const double lbr = S.include_self
+                                               ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] +
+                                                     envelope(S, j + 1, w.pP[b])
+                                               : w.pmx[b] + S.e1 + S.e2 * w.psum[b] +
+                                                     envelope(S, j + 1, 0.0);
+                        rok = !(lbr > thr);
+                    }
+                }
+                int l, hg;
+                if (rok) {
+                    l = 0;
+                    hg = tok ? s : 0;
+                } else if (tok) {
+                    l = s;
+                    hg = s;
+                } else {
+                    l = 0;
+                    hg = 0;
+                    mydead = true;
+                }
+                w.lo[o0 + b] = (uint16_t)l;
+                w.hi[o0 + b] = (uint16_t)hg;
+                mylo += l;
+                myhi += hg;
+            }
+            const int sumlo = wsum(mylo), sumhi = wsum(myhi);
+            const bool dead = wany(mydead);
+            __syncwarp();
+            if (dead || sumlo > dd || sumhi < dd) continue;
+            if (last) {
+                h.count_leaf();
+                const bool fm = S.mode == MODE_FIRST;
+                if (S.include_self) {
+                    const double tx = fm ? S.theta * (1.0 + 1e-12) : h.incumbent() * (1.0 - TIE_EPS);
+                    int flo = 0, fhi = 0;
+                    bool fdead = false;
+                    for (int b = lane; b < nb; b += 32) {
+                        const int s = w.bsz[o0 + b];
+                        const bool rok = fm ? w.cm[b] <= tx : w.cm[b] < tx;
+                        bool tok = false;
+                        if (w.hi[o0 + b]) {
+                            const double mb = w.pmb[b] > ba ? w.pmb[b] : ba;
+                            const double tv = mb + S.e1 + S.e2 * (w.psum[b] + bo) +
+                                              (S.additive ? 0.0 : S.e3 * (w.pP[b] * bo));
+                            tok = fm ? tv <= tx : tv < tx;
+                        }
+                        if (rok) {
+                            fhi += tok ? s : 0;
+                        } else if (tok) {
+                            flo += s;
+                            fhi += s;
+                        } else {
+                            fdead = true;
+                        }
+                    }
+                    const int FL = wsum(flo), FH = wsum(fhi);
+                    if (wany(fdead) || FL > dd || FH < dd) continue;
+                }
+                double* rest = w.cs;
+                double* take = w.cb;
+                for (int b = lane; b < nb; b += 32) {
+                    const unsigned m = w.bmk[o0 + b];
+                    rest[b] = contrib(S, R, w.opt, m);
+                    take[b] = w.hi[o0 + b] ? contrib(S, R, w.opt, m | (1u << j)) : POS_INF;
+                }
+                __syncwarp();
+                if (fm) {
+                    if (!(0.0 <= S.theta)) continue;
+                    if (!last_feasible_warp(w, o0, nb, dd, S.theta, true, rest, take)) continue;
+                    int mylo2 = 0;
+                    for (int b = lane; b < nb; b += 32)
+                        mylo2 += (rest[b] <= S.theta) ? 0 : w.bsz[o0 + b];
+                    const int rem0 = dd - wsum(mylo2);
+                    int carry = 0;
+                    double v = 0.0;
+                    for (int c = 0; c < nb; c += 32) {
+                        const int b = c + lane;
+                        int l = 0, room = 0;
+                        if (b < nb) {
+                            const int s = w.bsz[o0 + b];
+                            const bool rok = rest[b] <= S.theta;
+                            const bool tok = w.hi[o0 + b] && take[b] <= S.theta;
+                            l = rok ? 0 : s;
+                            room = (tok ? s : 0) - l;
+                        }
+                        const int inc = wscan_incl(room);
+                        const int ex = carry + inc - room;
+                        if (b < nb) {
+                            int left = rem0 - ex;
+                            left = left > 0 ? left : 0;
+                            const int xb = l + (room < left ? room : left);
+                            w.x[o0 + b] = (uint16_t)xb;
+                            const int s = w.bsz[o0 + b];
+                            if (xb > 0 && take[b] > v) v = take[b];
+                            if (xb < s && rest[b] > v) v = rest[b];
+                        }
+                        carry += __shfl_sync(FULLW, inc, 31);
+                    }
+                    v = wmaxd(v);
+                    __syncwarp();
+                    h.hit(w, j, v);
+                    return 1;
+                } else {
+                    const double I = h.incumbent();
+                    const double Ie = I * (1.0 - TIE_EPS);
+                    if (!last_feasible_warp(w, o0, nb, dd, Ie, false, rest, take)) continue;
+                    double hiv = Ie;
+                    while (true) {
+                        double c = NEG_INF;
+                        for (int b = lane; b < nb; b += 32) {
+                            if (rest[b] < hiv && rest[b] > c) c = rest[b];
+                            if (w.hi[o0 + b] && take[b] < hiv && take[b] > c) c = take[b];
+                        }
+                        c = wmaxd(c);
+                        if (c <= NEG_INF) break;
+                        if (last_feasible_warp(w, o0, nb, dd, c, true, rest, take))
+                            hiv = c;
+                        else
+                            break;
+                    }
+                    const double v = hiv > 0.0 ? hiv : 0.0;
+                    if (v < I) h.improve(v);
+                }
+                continue;
+            }
+            if (!first_comp_warp(w, o0, nb, dd)) continue;
+            if (lane == 0) w.ph[j] = 1;
+            __syncwarp();
+        } else {
+            if (!next_comp_warp(w, sc, o0, nb)) {
+                if (lane == 0) w.ph[j] = 0;
+                __syncwarp();
+                continue;
+            }
+        }
+        // ---- build the child (level j+1 blocks + their stats) ----
+        h.count_node();
+        if (ps_lvl != j) {
+            parent_stats_warp(S, R, w, j);
+            ps_lvl = j;
+        }
+        const int o1 = lvl_off(j + 1);
+        const int c1 = lvl_cap(j + 1);
+        const int r = S.lvl_off[j] + w.opt[j];
+        const int uu = R.u[r];
+        const double ff = R.fp[r], bo = R.B[r], ba = R.base[r];
+        int carry = 0;
+        for (int c = 0; c < nb; c += 32) {
+            const int b = c + lane;
+            int xb = 0, s = 0, cnt = 0;
+            if (b < nb) {
+                xb = w.x[o0 + b];
+                s = w.bsz[o0 + b];
+                cnt = (xb > 0) + (xb < s);
+            }
+            const int inc = wscan_incl(cnt);
+            int pos = carry + inc - cnt;
+            if (b < nb) {
+                const unsigned mk = w.bmk[o0 + b];
+                if (xb > 0 && pos < c1) {
+                    w.bsz[o1 + pos] = (uint16_t)xb;
+                    w.bmk[o1 + pos] = (uint16_t)(mk | (1u << j));
+                    w.cu[pos] = w.pu[b] + uu;
+                    w.cm[pos] = w.pm[b] + ff;
+                    w.cs[pos] = w.psum[b] + bo;
+                    w.cb[pos] = w.pmb[b] > ba ? w.pmb[b] : ba;
+                    ++pos;
+                } else if (xb > 0) {
+                    ++pos;
+                }
+                if (xb < s && pos < c1) {
+                    w.bsz[o1 + pos] = (uint16_t)(s - xb);
+                    w.bmk[o1 + pos] = (uint16_t)mk;
+                    w.cu[pos] = w.pu[b];
+                    w.cm[pos] = w.pm[b];
+                    w.cs[pos] = w.psum[b];
+                    w.cb[pos] = w.pmb[b];
+                }
+            }
+            carry += __shfl_sync(FULLW, inc, 31);
+        }
+        const int m = carry;
+        if (m > c1) {
+            h.overflow();
+            return 2;
+        }
+        if (lane == 0) {
+            w.nb[j + 1] = (uint16_t)m;
+            w.used[j + 1] = w.used[j] + R.d[r] * R.u[r];
+        }
+        __syncwarp();
+        const double thr = h.thr(S);
+        bool prune = false;
+        for (int l = j + 1; l < k && !prune; ++l) {
+            const int n = S.lvl_n[l], off = S.lvl_off[l];
+            bool ok = false;
+            for (int o = 0; o < n && !ok; ++o) {
+                const int rr = off + o;
+                const int t = opt_test(S, R, rr, thr);
+                if (t == 2) break;
+                if (t == 1) continue;
+                const int d2 = R.d[rr], u2 = R.u[rr];
+                const double f2 = R.fp[rr], b2 = R.B[rr], a2 = R.base[rr];
+                int cnt = 0;
+                for (int b = lane; b < m; b += 32) {
+                    if (w.cu[b] + u2 > S.L) continue;
+                    if (w.cm[b] + f2 > S.cap_slack) continue;
+                    if (S.nonneg && S.include_self) {
+                        const double mb = w.cb[b] > a2 ? w.cb[b] : a2;
+                        if (mb + S.e1 + S.e2 * (w.cs[b] + b2) > thr) continue;
+                    }
+                    cnt += w.bsz[o1 + b];
+                }
+                ok = wsum(cnt) >= d2;
+            }
+            if (!ok) prune = true;
+        }
+        if (prune) continue;
+        ++j;
+        if (lane == 0) {
+            w.ph[j] = 0;
+            w.oc[j] = -1;
+        }
+        __syncwarp();
+    }
+    return 0;
+}
+
+// ---- cursor load / store by a whole warp ----
+__device__ __forceinline__ void load_cont_warp(const Cont& c, Walk& w) {
+    const int lane = lane_id();
+    const int dep = c.depth;
+    const int o = lvl_off(dep);
+    for (int b = lane; b < c.nb; b += 32) {
+        w.bsz[o + b] = c.bsz[b];
+        w.bmk[o + b] = c.bmk[b];
+        if (c.ph) {
+            w.x[o + b] = c.x[b];
+            w.lo[o + b] = c.lo[b];
+            w.hi[o + b] = c.hi[b];
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        for (int l = 0; l < dep; ++l) w.opt[l] = c.opt[l];
+        w.nb[dep] = c.nb;
+        w.used[dep] = c.used;
+        w.ph[dep] = (uint8_t)c.ph;
+        w.oc[dep] = c.oc;
+        if (c.ph) w.opt[dep] = (uint16_t)c.oc;
+        for (int l = dep - 1; l >= 0; --l) {
+            const int oc1 = lvl_off(l + 1), ol = lvl_off(l);
+            const unsigned bit = 1u << l;
+            int nbl = 0;
+            for (int b = 0; b < w.nb[l + 1];) {
+                const unsigned key = w.bmk[oc1 + b] & ~bit;
+                int size = 0, taken = 0;
+                while (b < w.nb[l + 1] && (w.bmk[oc1 + b] & ~bit) == key) {
+                    size += w.bsz[oc1 + b];
+                    if (w.bmk[oc1 + b] & bit) taken += w.bsz[oc1 + b];
+                    ++b;
+                }
+                w.bsz[ol + nbl] = (uint16_t)size;
+                w.bmk[ol + nbl] = (uint16_t)key;
+                w.x[ol + nbl] = (uint16_t)taken;
+                ++nbl;
+            }
+            w.nb[l] = (uint16_t)nbl;
+        }
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void store_cont_warp(const Walk& w, int l, int ph, Cont& c) {
+    const int lane = lane_id();
+    const int o = lvl_off(l);
+    const int nb = w.nb[l];
+    for (int b = lane; b < nb; b += 32) {
+        c.bsz[b] = w.bsz[o + b];
+        c.bmk[b] = w.bmk[o + b];
+        if (ph) {
+            c.x[b] = w.x[o + b];
+            c.lo[b] = w.lo[o + b];
+            c.hi[b] = w.hi[o + b];
+        }
+    }
+    if (lane == 0) {
+        c.key = 0;
+        for (int i = 0; i < MAXK; ++i) c.opt[i] = i < l ? w.opt[i] : 0;
+        c.depth = (uint16_t)l;
+        c.nb = (uint16_t)nb;
+        c.ph = (uint16_t)ph;
+        c.oc = ph ? (int16_t)w.opt[l] : w.oc[l];
+        c.used = w.used[l];
+    }
+    __syncwarp();
+}
+
+}  // namespace mg

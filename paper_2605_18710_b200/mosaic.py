@@ -300,9 +300,10 @@ class Planner:
 
     def __init__(self, problem: C.POINTER(ProblemC), device: int = 0, _owned=None):
         L = load_library()
-        self._owned = _owned
+        self._owned = None
         self._ctx = C.c_void_p()
         _raise(L.mosaic_gpu_create(problem, device, C.byref(self._ctx)))
+        self._owned = _owned  # freed by close() only once the context exists
         p = problem.contents
         self.n_modules = p.n_modules
         self.gpu_count = p.gpu_count
