@@ -473,6 +473,8 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     Cont* hr = reinterpret_cast<Cont*>(pin + pin_off(3));
     int* hone = reinterpret_cast<int*>(pin + pin_off(4));
     *hs = S;
+    hs->shard_rank = rank_;
+    hs->shard_world = world_;
     std::memset(hc, 0, sizeof(Ctl));
     union {
         double d;
@@ -528,6 +530,7 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
         res.found = true;
         res.leaf = *hl;
     }
+    if (world_ > 1) merge_ranks(S, hc, res);
     CK(cudaEventRecord((cudaEvent_t)ev1_, s));
     CK(cudaEventSynchronize((cudaEvent_t)ev1_));
     float kms = 0, ms = 0;
@@ -613,6 +616,69 @@ void Engine::evaluate(const std::vector<EvalEntry>& ent, const std::vector<int>&
     cudaFreeAsync(dst, s);
     cudaFreeAsync(drect, s);
     CK(cudaStreamSynchronize(s));
+}
+
+// One all-gather per search (NCCL through the caller's callback): every rank contributes
+// its outcome; MIN takes the smallest incumbent and restarts everywhere if any rank
+// restarted, FIRST takes the hit that is earliest in reference DFS order.
+struct RankRecord {
+    int has_hit, aborted, overflow, pad;
+    double inc;
+    unsigned long long nodes, leaves;
+    HitPath path;
+    Leaf leaf;
+};
+
+static int host_path_cmp(const HitPath& a, const HitPath& b, int k) {
+    for (int l = 0; l < k; ++l) {
+        if (a.opt[l] != b.opt[l]) return a.opt[l] < b.opt[l] ? -1 : 1;
+        for (int i = 0; i < a.nb[l]; ++i)
+            if (a.x[l][i] != b.x[l][i]) return a.x[l][i] > b.x[l][i] ? -1 : 1;
+    }
+    return 0;
+}
+
+void Engine::merge_ranks(const Spec& S, const void* ctl_host, SearchResult& res) {
+    const Ctl* hc = reinterpret_cast<const Ctl*>(ctl_host);
+    if (!ag_) throw std::runtime_error("multi-GPU search without an all-gather");
+    std::vector<RankRecord> all(world_);
+    RankRecord mine;
+    std::memset(&mine, 0, sizeof mine);
+    mine.has_hit = res.found ? 1 : 0;
+    mine.aborted = res.aborted ? 1 : 0;
+    mine.overflow = res.overflow ? 1 : 0;
+    union {
+        unsigned long long u;
+        double d;
+    } w;
+    w.u = hc->inc;
+    mine.inc = w.d;
+    mine.nodes = hc->nodes;
+    mine.leaves = hc->leaves;
+    if (res.found) {
+        CK(cudaMemcpy(&mine.path, d_best_, sizeof(HitPath), cudaMemcpyDeviceToHost));
+        mine.leaf = res.leaf;
+    }
+    if (ag_(ag_user_, &mine, all.data(), sizeof(RankRecord)) != 0)
+        throw std::runtime_error("all-gather failed");
+    int win = -1;
+    double best = POS_INF;
+    bool aborted = false, overflow = false;
+    for (int r = 0; r < world_; ++r) {
+        const RankRecord& x = all[r];
+        aborted |= x.aborted != 0;
+        overflow |= x.overflow != 0;
+        if (x.inc < best) best = x.inc;
+        if (x.has_hit && (win < 0 || host_path_cmp(x.path, all[win].path, S.k) < 0)) win = r;
+    }
+    res.overflow = overflow;
+    if (S.mode == MODE_MIN) {
+        res.aborted = aborted;
+        res.value = best;
+    } else {
+        res.found = win >= 0;
+        if (win >= 0) res.leaf = all[win].leaf;
+    }
 }
 
 void Engine::mark(int which) {

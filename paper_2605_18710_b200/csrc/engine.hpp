@@ -78,6 +78,7 @@ class Engine {
 
   private:
     void ensure_front(long long n);
+    void merge_ranks(const Spec& S, const void* ctl_host, SearchResult& res);
     int device_;
     int rank_ = 0, world_ = 1;
     AllGatherFn ag_ = nullptr;

@@ -65,6 +65,7 @@ struct Spec {
     int lvl_off[MAXK];             // row offset of each level's options
     int pos_lvl[MAXK];             // module-index position -> level
     int suffix_min[MAXK + 1];      // min quota demand d*u over levels >= j
+    int shard_rank, shard_world;   // multi-GPU: this rank takes level-0 options o % world == rank
     int env_n[MAXK + 1];           // product-term envelope over unplaced levels >= j
     double env_a[MAXK + 1][MAXENV];
     double env_b[MAXK + 1][MAXENV];

@@ -192,6 +192,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, WScratch& sc, int
                 const int t = opt_test(S, R, r, thr);
                 if (t == 2) break;
                 if (t == 1) continue;
+                if (j == 0 && S.shard_world > 1 && o % S.shard_world != S.shard_rank) continue;
                 if (w.used[j] + R.d[r] * R.u[r] + S.suffix_min[j + 1] > GL) continue;
                 got = true;
                 break;

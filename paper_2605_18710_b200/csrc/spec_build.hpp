@@ -59,6 +59,8 @@ inline bool build_spec(const Model& M, const SearchReq& q, Spec& S) {
     S.include_self = M.include_self;
     S.additive = M.additive;
     S.use_filter = q.use_filter;
+    S.shard_rank = 0;
+    S.shard_world = 1;
     S.e1 = M.e1;
     S.e2 = M.e2;
     S.e3 = M.e3;
