@@ -34,6 +34,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOAD = "cfg5"
+DESCR = {
+    "cfg1": "cfg1: CLIP ViT-L/14 + text encoder, 8 modeled GPUs, exhaustive-size stage search",
+    "cfg2": "cfg2: LLaVA ViT + projector + 7B LLM, 16 modeled GPUs, quota 1/8, GAHC",
+    "cfg3": "cfg3: Qwen3-VL vision + text + deepstack + LLM, 32 modeled GPUs, GAHC",
+    "cfg4": "cfg4: omni-6 (3 encoders -> LLM -> 2 decoders), 64 modeled GPUs, GAHC",
+    "cfg5": "cfg5: omni-modal 8-module MM, 128 modeled GPUs, quota 1/32, GAHC to best plan",
+}
 METRIC = "candidate plans evaluated/sec (cfg5 GAHC solve to best plan)"
 UNIT = "plans/s"
 REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver_instr")
@@ -203,6 +210,11 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="cfg5", help="cfg1..cfg5 (default cfg5)")
+    ap.add_argument("--dist-backend", default="nccl",
+                    help="nccl (default); gloo lets several ranks share one GPU for testing")
+    ap.add_argument("--same-device", action="store_true",
+                    help="every rank uses cuda:0 (sharding test on a single GPU)")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)
@@ -211,13 +223,18 @@ def main() -> None:
     import torch
     import torch.distributed as dist
 
+    global WORKLOAD
+    WORKLOAD = args.workload
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if args.same_device else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
 
     from paper_2605_18710_b200 import mosaic
 
@@ -226,14 +243,17 @@ def main() -> None:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    comm_dev = dev if args.dist_backend == "nccl" else torch.device("cpu")
+
     def allgather_bytes(b: bytes) -> list[bytes]:
-        t = torch.frombuffer(bytearray(b), dtype=torch.uint8).to(dev)
+        t = torch.frombuffer(bytearray(b), dtype=torch.uint8).to(comm_dev)
         outs = [torch.empty_like(t) for _ in range(world)]
         dist.all_gather(outs, t)
         return [bytes(o.cpu().numpy().tobytes()) for o in outs]
 
     # ---- device-resident run: tables already in HBM, time the solve only ----
     pl = mosaic.Planner.from_spec(WORKLOAD, device=local)
+    res_g, res_l, res_n = pl.gpu_count, pl.quota_levels, pl.n_modules
     if world > 1:
         pl.set_shard(rank, world, allgather_bytes)
     for _ in range(args.warmup):
@@ -255,11 +275,12 @@ def main() -> None:
     ctr = pl.counters()
     t_local = sum(dev_ms)
     if world > 1:
-        tt = torch.tensor([t_local, float(leaves)], dtype=torch.float64, device=dev)
-        mx = tt.clone()
-        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
-        t_max, leaves_all = float(mx[0]), float(tt[1])
+        tt = torch.tensor([t_local, float(leaves)], dtype=torch.float64, device=comm_dev)
+        mx = tt[:1].clone()
+        sm = tt[1:].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        t_max, leaves_all = float(mx[0]), float(sm[0])
     else:
         t_max, leaves_all = t_local, float(leaves)
     value = leaves_all / (t_max / 1000.0) if t_max > 0 else 0.0
@@ -313,9 +334,9 @@ def main() -> None:
         "warmup": args.warmup, "ms_per_step": t_max / max(1, args.steps),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "cfg5: omni-modal 8-module MM, 128 modeled GPUs, quota 1/32, "
-                               "GAHC to best plan", "modeled_gpus": 128, "quota_levels": 32,
-                   "modules": 8, "l2": "flushed between steps (256 MiB write)",
+        "config": {"workload": DESCR.get(WORKLOAD, WORKLOAD), "modeled_gpus": res_g,
+                   "quota_levels": res_l, "modules": res_n,
+                   "l2": "flushed between steps (256 MiB write)",
                    "parallelism": f"frontier+round sharding over {world} GPU(s)"},
         "time_to_best_plan_s": t_max / 1000.0 / max(1, args.steps),
         "best_plan_iteration_time": plans[-1],

@@ -47,7 +47,8 @@ struct Ctl {
     alignas(128) unsigned int idle;
     alignas(128) int lock;  // FIRST: best hit, published under a seqlock
     int ver;
-    int has_hit;
+    int has_hit;            // FIRST: a hit is published; MIN: an argmin leaf is stored
+    double leaf_val;
     alignas(128) unsigned long long nodes, leaves;
 };
 
@@ -121,7 +122,8 @@ struct WarpHooks {
     }
     // push the cursor "rest of level l" onto the ring queue (ticket t -> slot t % cap,
     // published by writing ready[slot] = t + 1)
-    __device__ bool donate(const Walk& wk, int l) {
+    // ph 1: "rest of level l" (after the current composition); ph 0: options from mid on
+    __device__ bool donate(const Walk& wk, int l, int ph, int mid) {
         long long slot = -1;
         unsigned long long t = 0;
         if (lane_id() == 0) {
@@ -140,7 +142,7 @@ struct WarpHooks {
         }
         slot = __shfl_sync(FULLW, slot, 0);
         if (slot < 0) return false;
-        store_cont_warp(wk, l, 1, q[slot]);
+        store_cont_warp(wk, l, ph, q[slot], mid - 1);
         __threadfence();  // every lane's part of the cursor is visible ...
         __syncwarp();
         if (lane_id() == 0) {
@@ -177,8 +179,27 @@ struct WarpHooks {
         if (v < inc_cache) inc_cache = v;
         __syncwarp();
     }
+    // MIN: lower the incumbent and keep the allocation that reached it
+    __device__ void improve_leaf(const Walk& wk, int j, double v) {
+        if (lane_id() == 0) {
+            atomicMin(&ctl->inc, (unsigned long long)__double_as_longlong(v));
+            if (v < ctl->abort_below) atomicExch(&ctl->abort, 1);
+            while (atomicCAS(&ctl->lock, 0, 1) != 0) __nanosleep(64);
+            __threadfence();
+            if (!ctl->has_hit || v < ctl->leaf_val) {
+                store_leaf(wk, j, v, *leaf_out);
+                ctl->leaf_val = v;
+                ctl->has_hit = 1;
+            }
+            __threadfence();
+            atomicExch(&ctl->lock, 0);
+        }
+        if (v < inc_cache) inc_cache = v;
+        __syncwarp();
+    }
     __device__ void count_node() { ++nodes; }
     __device__ void count_leaf() { ++leaves; }
+    __device__ void count_leaves(int n) { leaves += (unsigned long long)n; }
     __device__ void overflow() {
         if (lane_id() == 0) {
             atomicExch(&ctl->overflow, 1);
@@ -458,7 +479,8 @@ void Engine::ensure_front(long long n) {
     front_cap_ = cap;
 }
 
-SearchResult Engine::search(const Spec& S, double ub, double abort_below, SearchStats& st) {
+SearchResult Engine::search(const Spec& S, double ub, double abort_below, SearchStats& st,
+                            const HitPath* seed_path, const Leaf* seed_leaf) {
     CK(cudaSetDevice(device_));
     cudaStream_t s = S_(stream_);
     SearchResult res;
@@ -475,6 +497,7 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     *hs = S;
     hs->shard_rank = rank_;
     hs->shard_world = world_;
+    hs->shard_level = S.k >= 2 ? 1 : 0;  // (o_0, o_1) pairs: fine enough to balance 8 ranks
     std::memset(hc, 0, sizeof(Ctl));
     union {
         double d;
@@ -492,10 +515,19 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     hr->nb = 1;
     hr->ph = 0;
     hr->oc = -1;
+    hr->oe = (int16_t)S.lvl_n[0];
     hr->bsz[0] = (uint16_t)S.G;
     *hone = 1;
     Cont* Q = reinterpret_cast<Cont*>(d_front_[0]);
     CK(cudaEventRecord((cudaEvent_t)ev0_, s));
+    if (S.mode == MODE_FIRST && seed_path && seed_leaf) {
+        // a known leaf <= theta: the search only has to look at what precedes it
+        hc->has_hit = 1;
+        CK(cudaMemcpyAsync(d_best_, seed_path, sizeof(HitPath), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d_leaf_, seed_leaf, sizeof(Leaf), cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        h2d_ += sizeof(HitPath) + sizeof(Leaf);
+    }
     CK(cudaMemcpyAsync(d_spec_, hs, sizeof(Spec), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(d_ctl_, hc, sizeof(Ctl), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(Q, hr, sizeof(Cont), cudaMemcpyHostToDevice, s));
@@ -523,7 +555,7 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     d2h_ += sizeof(Ctl);
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
-    if (S.mode == MODE_FIRST && hc->has_hit && !hc->overflow) {
+    if (hc->has_hit && !hc->overflow) {
         CK(cudaMemcpyAsync(hl, d_leaf_, sizeof(Leaf), cudaMemcpyDeviceToHost, s));
         d2h_ += sizeof(Leaf);
         CK(cudaStreamSynchronize(s));

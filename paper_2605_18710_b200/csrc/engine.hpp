@@ -15,8 +15,8 @@ struct SearchStats {
 };
 
 struct SearchResult {
-    bool found = false;  // FIRST: a leaf with value <= theta exists (in filter order)
-    Leaf leaf{};         // FIRST: that leaf
+    bool found = false;  // FIRST: a leaf with value <= theta exists; MIN: argmin leaf kept
+    Leaf leaf{};         // FIRST: the first such leaf; MIN: an allocation reaching `value`
     double value = POS_INF;  // MIN: best value found (< ub), else ub
     bool aborted = false;    // MIN: incumbent fell below abort_below
     bool overflow = false;   // a level needed more than MAXB blocks
@@ -38,7 +38,9 @@ class Engine {
     Engine& operator=(const Engine&) = delete;
 
     void upload_rows(const Model& M);
-    SearchResult search(const Spec& S, double ub, double abort_below, SearchStats& st);
+    // seed (FIRST only): a leaf known to satisfy theta, as a path in this search's order
+    SearchResult search(const Spec& S, double ub, double abort_below, SearchStats& st,
+                        const HitPath* seed_path = nullptr, const Leaf* seed_leaf = nullptr);
     // Batched stage_time (K1): per allocation, entries [off[i], off[i+1]).
     void evaluate(const std::vector<EvalEntry>& ent, const std::vector<int>& gpus,
                   const std::vector<long long>& off, const std::vector<double>& base,

@@ -7,6 +7,9 @@
 #include <cmath>
 #include <functional>
 #include <limits>
+#include <cstring>
+#include <cstdio>
+#include <cstdlib>
 
 namespace mosaic_b200 {
 
@@ -66,8 +69,76 @@ void Planner::check_rows(int m) const {
     if (!opt_err_[m].empty()) throw Error(RANGE, opt_err_[m]);
 }
 
+// Canonical form of a known allocation in the DFS order `order`: sort GPUs by their
+// membership vector (level 0 most significant, descending); then at every level each
+// module holds a prefix of every block.  Yields the hit path + leaf the FIRST search
+// would report for it, or false if it is not a leaf of that search (filter, capacity).
+bool Planner::make_seed(const std::vector<Entry>& ents, const std::vector<int>& order,
+                        bool filter, double theta, double value, mg::HitPath& hp,
+                        Leaf& lf) const {
+    const int k = (int)order.size(), G = P_.gpu_count;
+    if (!(value <= theta) || k > mg::MAXK) return false;
+    std::vector<uint32_t> key(G, 0);
+    std::vector<int> row(k, -1);
+    for (int l = 0; l < k; ++l) {
+        const Entry* e = nullptr;
+        for (const auto& x : ents)
+            if (x.module == order[l]) e = &x;
+        if (!e) return false;
+        const auto& rows = M_.rows[order[l]];
+        for (int i = 0; i < (int)rows.size(); ++i)
+            if (rows[i].d == e->d && rows[i].u == e->units) row[l] = i;
+        if (row[l] < 0) return false;
+        if (filter && rows[row[l]].bound > theta) return false;
+        for (int g : e->gpus) key[g] |= 1u << (k - 1 - l);
+    }
+    std::vector<uint32_t> ks(key);
+    std::sort(ks.begin(), ks.end(), std::greater<uint32_t>());
+    struct Blk { int start, size; uint32_t mask; };
+    std::vector<Blk> blocks{{0, G, 0}};
+    std::memset(&hp, 0, sizeof hp);
+    for (int l = 0; l < k; ++l) {
+        if ((int)blocks.size() > mg::MAXB) return false;
+        const mg::OptRow& r = M_.rows[order[l]][row[l]];
+        hp.opt[l] = (uint16_t)row[l];
+        hp.nb[l] = (uint16_t)blocks.size();
+        std::vector<Blk> next;
+        const uint32_t bit = 1u << (k - 1 - l);
+        for (size_t b = 0; b < blocks.size(); ++b) {
+            const Blk& B = blocks[b];
+            int taken = 0;
+            while (taken < B.size && (ks[B.start + taken] & bit)) ++taken;
+            hp.x[l][b] = (uint16_t)taken;
+            if (taken > 0) {
+                int units = 0;
+                double mem = 0.0;
+                for (int t = 0; t < l; ++t)
+                    if (B.mask >> t & 1u) {
+                        units += M_.rows[order[t]][row[t]].u;
+                        mem = mem + M_.rows[order[t]][row[t]].fp;
+                    }
+                if (units + r.u > M_.L || mem + r.fp > M_.cap * (1.0 + 1e-12)) return false;
+                next.push_back({B.start, taken, B.mask | (1u << l)});
+            }
+            if (taken < B.size) next.push_back({B.start + taken, B.size - taken, B.mask});
+        }
+        blocks.swap(next);
+    }
+    if ((int)blocks.size() > 2 * mg::MAXB) return false;
+    std::memset(&lf, 0, sizeof lf);
+    lf.value = value;
+    for (int l = 0; l < k; ++l) lf.opt[l] = (uint16_t)row[l];
+    lf.nb = (int)blocks.size();
+    for (size_t b = 0; b < blocks.size(); ++b) {
+        lf.bsz[b] = (uint16_t)blocks[b].size;
+        lf.bmk[b] = (uint16_t)blocks[b].mask;
+    }
+    return true;
+}
+
 bool Planner::first_leaf(const std::vector<int>& order, bool filter, double theta, Leaf& leaf,
-                         mg::SearchStats& st) {
+                         mg::SearchStats& st, const std::vector<Entry>* seed,
+                         double seed_value) {
     mg::SearchReq q;
     q.mode = MODE_FIRST;
     q.use_filter = filter;
@@ -75,7 +146,14 @@ bool Planner::first_leaf(const std::vector<int>& order, bool filter, double thet
     q.level_module = order;
     mg::Spec S;
     if (!mg::build_spec(M_, q, S)) return false;
-    mg::SearchResult r = eng_->search(S, POS_INF, 0.0, st);
+    mg::HitPath hp;
+    Leaf sl;
+    const bool seeded = seed && make_seed(*seed, order, filter, theta, seed_value, hp, sl);
+    if (seed && std::getenv("MOSAIC_TRACE"))
+        std::fprintf(stderr, "[mosaic] FIRST seed %s (theta=%.17g value=%.17g)\n",
+                     seeded ? "applied" : "rejected", theta, seed_value);
+    mg::SearchResult r = eng_->search(S, POS_INF, 0.0, st, seeded ? &hp : nullptr,
+                                      seeded ? &sl : nullptr);
     if (r.overflow) throw Error(TOO_LARGE, "stage needs more than 128 GPU blocks");
     if (r.found) leaf = r.leaf;
     return r.found;
@@ -83,7 +161,8 @@ bool Planner::first_leaf(const std::vector<int>& order, bool filter, double thet
 
 // Exact minimum stage_time over every capacity/memory-feasible leaf (T*), restarting
 // with tighter static bounds whenever the incumbent drops well below the last bound.
-double Planner::min_value(const std::vector<int>& mods, double ub, mg::SearchStats& st) {
+double Planner::min_value(const std::vector<int>& mods, double ub, mg::SearchStats& st,
+                          std::vector<Entry>* argmin) {
     while (true) {
         // fail-first: fewest viable options first (any order is valid for MIN)
         const double thp = ub >= POS_INF ? POS_INF : ub * (1.0 - mg::TIE_EPS);
@@ -110,6 +189,7 @@ double Planner::min_value(const std::vector<int>& mods, double ub, mg::SearchSta
         double ab = ub >= POS_INF ? POS_INF : ub * (1.0 - 1e-4);
         mg::SearchResult r = eng_->search(S, ub, ab, st);
         if (r.overflow) throw Error(TOO_LARGE, "stage needs more than 128 GPU blocks");
+        if (argmin && r.found && r.leaf.nb > 0) *argmin = leaf_entries(q.level_module, r.leaf);
         if (r.aborted) {
             ub = r.value;
             continue;
@@ -169,6 +249,7 @@ StageResult Planner::stage_eval(uint64_t mask) {
     }
     bool have_T = false;
     double Tstar = POS_INF;
+    std::vector<Entry> argmin;  // an allocation reaching Tstar
     long long probes = 0;
     // FeasibilitySearch::run(tau) replayed: first leaf in fail-first DFS order.
     auto run = [&](double tau, Leaf& leaf, std::vector<int>& order) -> bool {
@@ -188,7 +269,9 @@ StageResult Planner::stage_eval(uint64_t mask) {
         std::stable_sort(cnt.begin(), cnt.end());
         order.clear();
         for (auto& [c, m] : cnt) order.push_back(m);
-        return first_leaf(order, true, th, leaf, res.st);
+        // seed with the argmin allocation when it is known to satisfy this probe
+        const bool seed = nonneg && have_T && !argmin.empty() && Tstar <= th;
+        return first_leaf(order, true, th, leaf, res.st, seed ? &argmin : nullptr, Tstar);
     };
     Leaf best, cur;
     std::vector<int> best_order, cur_order;
@@ -204,7 +287,8 @@ StageResult Planner::stage_eval(uint64_t mask) {
     }
     double t_best = best.value;
     if (nonneg) {
-        Tstar = min_value(mods, t_best, res.st);
+        argmin = leaf_entries(best_order, best);
+        Tstar = min_value(mods, t_best, res.st, &argmin);
         have_T = true;
     }
     double lo = std::min(tau_lo, t_best);

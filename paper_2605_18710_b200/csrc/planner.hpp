@@ -88,8 +88,12 @@ class Planner {
   private:
     void check_rows(int m) const;
     bool first_leaf(const std::vector<int>& order, bool filter, double theta, mg::Leaf& leaf,
-                    mg::SearchStats& st);
-    double min_value(const std::vector<int>& mods, double ub, mg::SearchStats& st);
+                    mg::SearchStats& st, const std::vector<Entry>* seed = nullptr,
+                    double seed_value = 0.0);
+    double min_value(const std::vector<int>& mods, double ub, mg::SearchStats& st,
+                     std::vector<Entry>* argmin = nullptr);
+    bool make_seed(const std::vector<Entry>& ents, const std::vector<int>& order, bool filter,
+                   double theta, double value, mg::HitPath& hp, mg::Leaf& lf) const;
     std::vector<Entry> leaf_entries(const std::vector<int>& order, const mg::Leaf& lf) const;
     std::optional<StageResult> evaluate_cached(uint64_t mask, bool* hit, PlanResult& pr);
 

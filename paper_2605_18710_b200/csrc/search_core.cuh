@@ -65,7 +65,8 @@ struct Spec {
     int lvl_off[MAXK];             // row offset of each level's options
     int pos_lvl[MAXK];             // module-index position -> level
     int suffix_min[MAXK + 1];      // min quota demand d*u over levels >= j
-    int shard_rank, shard_world;   // multi-GPU: this rank takes level-0 options o % world == rank
+    int shard_rank, shard_world;   // multi-GPU: this rank takes the option prefixes
+    int shard_level;               //   (o_0..o_L) with shard_hash % world == rank, L = shard_level
     int env_n[MAXK + 1];           // product-term envelope over unplaced levels >= j
     double env_a[MAXK + 1][MAXENV];
     double env_b[MAXK + 1][MAXENV];
@@ -89,12 +90,21 @@ struct alignas(16) Cont {
     uint16_t opt[MAXK];
     uint16_t depth, nb, ph;
     int16_t oc;
+    int16_t oe;  // options at `depth` stop before oe (range split by work donation)
+    int16_t pad16;
     int used;
     uint16_t bsz[MAXB];
     uint16_t bmk[MAXB];
     uint16_t x[MAXB];
     uint16_t lo[MAXB];
     uint16_t hi[MAXB];
+};
+
+// Position of a FIRST hit in the reference DFS order: (option, composition) per level.
+struct HitPath {
+    uint16_t opt[MAXK];
+    uint16_t nb[MAXK];
+    uint16_t x[MAXK][MAXB];
 };
 
 // Leaf: options of every level plus the final block list (sizes, level masks).
@@ -121,6 +131,7 @@ constexpr int WALK_SLOTS = 255 + (MAXK + 1 - 8) * MAXB;  // sum_{j<=MAXK} lvl_ca
 struct Walk {
     uint16_t opt[MAXK];
     int16_t oc[MAXK];
+    int16_t oe[MAXK];  // option range end per level (exclusive)
     uint8_t ph[MAXK];
     uint16_t nb[MAXK + 1];
     int used[MAXK + 1];
@@ -189,6 +200,60 @@ MG_HD double contrib(const Spec& S, const Rows& R, const uint16_t* opt, unsigned
         best = v > best ? v : best;
     }
     return best;
+}
+
+// contrib() with the option of level `jl` replaced by `ol` (lanes evaluating different
+// last-level options against the same shared walk).
+MG_HD double contrib_o(const Spec& S, const Rows& R, const uint16_t* opt, unsigned mask, int jl,
+                       int ol) {
+    if (!mask) return NEG_INF;
+    if (S.include_self) {
+        double s = 0.0, p = 1.0, mb = NEG_INF;
+        for (int pos = 0; pos < S.k; ++pos) {
+            int l = S.pos_lvl[pos];
+            if (!(mask >> l & 1u)) continue;
+            int r = S.lvl_off[l] + (l == jl ? ol : opt[l]);
+            double b = R.B[r];
+            s = s + b;
+            p = p * b;
+            double ba = R.base[r];
+            mb = ba > mb ? ba : mb;
+        }
+        double dl = S.e1 + S.e2 * s;
+        dl = dl + (S.additive ? 0.0 : S.e3 * p);
+        return mb + dl;
+    }
+    double best = NEG_INF;
+    for (int pos = 0; pos < S.k; ++pos) {
+        int l = S.pos_lvl[pos];
+        if (!(mask >> l & 1u)) continue;
+        double s = 0.0, p = 1.0;
+        int n = 0;
+        for (int pos2 = 0; pos2 < S.k; ++pos2) {
+            int l2 = S.pos_lvl[pos2];
+            if (l2 == l || !(mask >> l2 & 1u)) continue;
+            double b = R.B[S.lvl_off[l2] + (l2 == jl ? ol : opt[l2])];
+            s = s + b;
+            p = p * b;
+            ++n;
+        }
+        if (n == 0) p = 0.0;
+        double dl = S.e1 + S.e2 * s;
+        dl = dl + (S.additive ? 0.0 : S.e3 * p);
+        double v = R.base[S.lvl_off[l] + (l == jl ? ol : opt[l])] + dl;
+        best = v > best ? v : best;
+    }
+    return best;
+}
+
+// Owner rank of an option prefix (levels 0..j with level j's option o).
+MG_HD unsigned shard_hash(const uint16_t* opt, int j, int o) {
+    unsigned h = 2166136261u;
+    for (int l = 0; l <= j; ++l) {
+        h ^= (unsigned)(l == j ? o : opt[l]) + 0x9e37u * (unsigned)(l + 1);
+        h *= 16777619u;
+    }
+    return h;
 }
 
 // 0 accept, 1 skip, 2 stop the option loop (all later options fail too).
@@ -642,12 +707,6 @@ MG_HD void load_cont(const Cont& c, Walk& w) {
     }
 }
 
-// Position of a FIRST hit in the reference DFS order: (option, composition) per level.
-struct HitPath {
-    uint16_t opt[MAXK];
-    uint16_t nb[MAXK];
-    uint16_t x[MAXK][MAXB];
-};
 
 // -1: path H precedes the walk's leaf path (levels 0..j), +1 follows it, 0 equal.
 template <class HP>

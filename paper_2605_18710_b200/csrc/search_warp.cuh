@@ -164,6 +164,220 @@ __device__ __forceinline__ bool level_has_rest_warp(const Spec& S, const Walk& w
     return r;
 }
 
+// Descending-lexicographic first composition whose present parts all have contribution
+// <= t (rest/take per block); writes w.x at level j and returns the allocation's value.
+__device__ __forceinline__ double greedy_fill_warp(Walk& w, int o0, int nb, int dd, double t,
+                                                   const double* rest, const double* take) {
+    const int lane = lane_id();
+    int mylo = 0;
+    for (int b = lane; b < nb; b += 32) mylo += (rest[b] <= t) ? 0 : w.bsz[o0 + b];
+    const int rem0 = dd - wsum(mylo);
+    int carry = 0;
+    double v = 0.0;
+    for (int c = 0; c < nb; c += 32) {
+        const int b = c + lane;
+        int l = 0, room = 0;
+        if (b < nb) {
+            const int s = w.bsz[o0 + b];
+            const bool rok = rest[b] <= t;
+            const bool tok = w.hi[o0 + b] && take[b] <= t;
+            l = rok ? 0 : s;
+            room = (tok ? s : 0) - l;
+        }
+        const int inc = wscan_incl(room);
+        const int ex = carry + inc - room;
+        if (b < nb) {
+            int left = rem0 - ex;
+            left = left > 0 ? left : 0;
+            const int xb = l + (room < left ? room : left);
+            w.x[o0 + b] = (uint16_t)xb;
+            const int s = w.bsz[o0 + b];
+            if (xb > 0 && take[b] > v) v = take[b];
+            if (xb < s && rest[b] > v) v = rest[b];
+        }
+        carry += __shfl_sync(FULLW, inc, 31);
+    }
+    v = wmaxd(v);
+    __syncwarp();
+    return v;
+}
+
+// Per-lane exact check of last-level option `o` at threshold t (le: <=, else <).
+__device__ __forceinline__ bool lane_last_feasible(const Spec& S, const Rows& R, const Walk& w,
+                                                   int j, int o0, int nb, int o, int uu,
+                                                   double ff, int dd, double t, bool le) {
+    int lo = 0, hi = 0;
+    for (int b = 0; b < nb; ++b) {
+        const int s = w.bsz[o0 + b];
+        const double rv = w.cs[b];
+        const bool rok = le ? rv <= t : rv < t;
+        bool tok = false;
+        if (w.pu[b] + uu <= S.L && !(w.pm[b] + ff > S.cap_slack)) {
+            const double tv = contrib_o(S, R, w.opt, w.bmk[o0 + b] | (1u << j), j, o);
+            tok = le ? tv <= t : tv < t;
+        }
+        if (rok) {
+            if (tok) hi += s;
+        } else if (tok) {
+            lo += s;
+            hi += s;
+        } else {
+            return false;
+        }
+    }
+    return lo <= dd && dd <= hi;
+}
+
+// The last level with lanes over OPTIONS: every lane screens its own candidate option
+// against all blocks (no per-option warp reductions), then the winner — first feasible
+// option (FIRST) or smallest value (MIN) — is materialised block-parallel.  Returns true
+// when a FIRST hit was published.
+template <class H>
+__device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, int& ps_lvl, H& h) {
+    const int lane = lane_id();
+    const int o0 = lvl_off(j), nb = w.nb[j];
+    const int GL = S.G * S.L;
+    if (ps_lvl != j) {
+        parent_stats_warp(S, R, w, j);
+        ps_lvl = j;
+    }
+    // per block: approximate (fast filter) and exact rest contributions
+    for (int b = lane; b < nb; b += 32) {
+        const unsigned m = w.bmk[o0 + b];
+        w.cm[b] = m ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] + (S.additive ? 0.0 : S.e3 * w.pP[b])
+                    : NEG_INF;
+        w.cs[b] = contrib(S, R, w.opt, m);
+    }
+    __syncwarp();
+    const bool fm = S.mode == MODE_FIRST;
+    const int n = S.lvl_n[j] < w.oe[j] ? S.lvl_n[j] : w.oe[j];
+    const int off = S.lvl_off[j];
+    const double thr = h.thr(S);
+    for (int start = w.oc[j] + 1; start < n; start += 32) {
+        const int o = start + lane;
+        const int t = o < n ? opt_test(S, R, off + o, thr) : 2;
+        const unsigned brk = __ballot_sync(FULLW, t == 2);
+        const int first_brk = brk ? __ffs(brk) - 1 : 32;
+        bool valid = t == 0 && lane < first_brk;
+        if (valid && j == S.shard_level && S.shard_world > 1 &&
+            shard_hash(w.opt, j, o) % (unsigned)S.shard_world != (unsigned)S.shard_rank)
+            valid = false;
+        int dd = 0, uu = 0;
+        double ff = 0.0, bo = 0.0, ba = 0.0;
+        if (valid) {
+            const int r = off + o;
+            dd = R.d[r];
+            uu = R.u[r];
+            ff = R.fp[r];
+            bo = R.B[r];
+            ba = R.base[r];
+            if (w.used[j] + dd * uu > GL) valid = false;
+        }
+        h.count_leaves(__popc(__ballot_sync(FULLW, valid)));
+        const double I = fm ? 0.0 : h.incumbent();
+        const double Ie = I * (1.0 - TIE_EPS);
+        bool feas = false;
+        double val = POS_INF;
+        if (valid) {
+            // fast filter (approximate contributions, sound 1e-12 slack)
+            bool pass = true;
+            if (S.include_self) {
+                const double tx = fm ? S.theta * (1.0 + 1e-12) : Ie;
+                int lo = 0, hi = 0;
+                for (int b = 0; b < nb && pass; ++b) {
+                    const int s = w.bsz[o0 + b];
+                    const bool el = w.pu[b] + uu <= S.L && !(w.pm[b] + ff > S.cap_slack);
+                    const bool rok = fm ? w.cm[b] <= tx : w.cm[b] < tx;
+                    bool tok = false;
+                    if (el) {
+                        const double mb = w.pmb[b] > ba ? w.pmb[b] : ba;
+                        const double tv = mb + S.e1 + S.e2 * (w.psum[b] + bo) +
+                                          (S.additive ? 0.0 : S.e3 * (w.pP[b] * bo));
+                        tok = fm ? tv <= tx : tv < tx;
+                    }
+                    if (rok) {
+                        if (tok) hi += s;
+                    } else if (tok) {
+                        lo += s;
+                        hi += s;
+                    } else {
+                        pass = false;
+                    }
+                }
+                pass = pass && lo <= dd && dd <= hi;
+            }
+            if (pass) {
+                if (fm) {
+                    feas = 0.0 <= S.theta &&
+                           lane_last_feasible(S, R, w, j, o0, nb, o, uu, ff, dd, S.theta, true);
+                } else if (lane_last_feasible(S, R, w, j, o0, nb, o, uu, ff, dd, Ie, false)) {
+                    // smallest feasible threshold: descend through candidate values
+                    double hiv = Ie;
+                    while (true) {
+                        double c = NEG_INF;
+                        for (int b = 0; b < nb; ++b) {
+                            const double rv = w.cs[b];
+                            if (rv < hiv && rv > c) c = rv;
+                            if (w.pu[b] + uu <= S.L && !(w.pm[b] + ff > S.cap_slack)) {
+                                const double tv =
+                                    contrib_o(S, R, w.opt, w.bmk[o0 + b] | (1u << j), j, o);
+                                if (tv < hiv && tv > c) c = tv;
+                            }
+                        }
+                        if (c <= NEG_INF) break;
+                        if (lane_last_feasible(S, R, w, j, o0, nb, o, uu, ff, dd, c, true))
+                            hiv = c;
+                        else
+                            break;
+                    }
+                    val = hiv > 0.0 ? hiv : 0.0;
+                    feas = val < I;
+                }
+            }
+        }
+        const unsigned fb = __ballot_sync(FULLW, feas);
+        if (fb) {
+            int win;
+            double v;
+            if (fm) {
+                win = __ffs(fb) - 1;
+            } else {
+                double mv = val;
+                for (int of = 16; of; of >>= 1) {
+                    double x = __shfl_xor_sync(FULLW, mv, of);
+                    mv = x < mv ? x : mv;
+                }
+                win = __ffs(__ballot_sync(FULLW, feas && val == mv)) - 1;
+            }
+            const int ow = start + win;
+            const int r = off + ow;
+            const int dd2 = R.d[r], uu2 = R.u[r];
+            const double ff2 = R.fp[r];
+            if (lane == 0) {
+                w.opt[j] = (uint16_t)ow;
+                w.oc[j] = (int16_t)ow;
+            }
+            __syncwarp();
+            // block-parallel materialisation of the winner: take contributions + greedy fill
+            for (int b = lane; b < nb; b += 32) {
+                const bool el = w.pu[b] + uu2 <= S.L && !(w.pm[b] + ff2 > S.cap_slack);
+                w.hi[o0 + b] = el ? w.bsz[o0 + b] : 0;
+                w.cb[b] = el ? contrib(S, R, w.opt, w.bmk[o0 + b] | (1u << j)) : POS_INF;
+            }
+            __syncwarp();
+            const double tfill = fm ? S.theta : __shfl_sync(FULLW, val, win);
+            v = greedy_fill_warp(w, o0, nb, dd2, tfill, w.cs, w.cb);
+            if (fm) {
+                h.hit(w, j, v);
+                return true;
+            }
+            h.improve_leaf(w, j, v);
+        }
+        if (first_brk < 32) break;
+    }
+    return false;
+}
+
 template <class H>
 __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, WScratch& sc, int d0, H& h) {
     const int lane = lane_id();
@@ -181,10 +395,25 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, WScratch& sc, int
             if (ab == 2) return 2;
             if (ab == 3) {
                 while (floor_lvl < j && !level_has_rest_warp(S, w, sc, floor_lvl)) ++floor_lvl;
-                if (floor_lvl < j && h.donate(w, floor_lvl)) ++floor_lvl;
+                if (floor_lvl < j) {
+                    if (h.donate(w, floor_lvl, 1, -1)) ++floor_lvl;
+                } else if (j < k - 1) {
+                    // all that is left is this level's option range: hand over its upper half
+                    const int a = w.oc[j] + 1, e = w.oe[j];
+                    if (e - a >= 2) {
+                        const int mid = a + (e - a) / 2;
+                        if (h.donate(w, j, 0, mid) && lane == 0) w.oe[j] = (int16_t)mid;
+                        __syncwarp();
+                    }
+                }
+            }
+            if (j == k - 1 && S.nonneg) {
+                if (last_level_batch(S, R, w, j, ps_lvl, h)) return 1;
+                --j;
+                continue;
             }
             const double thr = h.thr(S);
-            const int n = S.lvl_n[j], off = S.lvl_off[j];
+            const int n = S.lvl_n[j] < w.oe[j] ? S.lvl_n[j] : w.oe[j], off = S.lvl_off[j];
             int o = w.oc[j] + 1;
             bool got = false;
             for (; o < n; ++o) {
@@ -192,7 +421,9 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, WScratch& sc, int
                 const int t = opt_test(S, R, r, thr);
                 if (t == 2) break;
                 if (t == 1) continue;
-                if (j == 0 && S.shard_world > 1 && o % S.shard_world != S.shard_rank) continue;
+                if (j == S.shard_level && S.shard_world > 1 &&
+                    shard_hash(w.opt, j, o) % (unsigned)S.shard_world != (unsigned)S.shard_rank)
+                    continue;
                 if (w.used[j] + R.d[r] * R.u[r] + S.suffix_min[j + 1] > GL) continue;
                 got = true;
                 break;
@@ -365,7 +596,36 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, WScratch& sc, int
                             break;
                     }
                     const double v = hiv > 0.0 ? hiv : 0.0;
-                    if (v < I) h.improve(v);
+                    if (v < I) {
+                        // materialise one allocation reaching v (greedy fill at hiv) so the
+                        // planner can seed later FIRST probes with the argmin
+                        int mylo3 = 0;
+                        for (int b = lane; b < nb; b += 32)
+                            mylo3 += (rest[b] <= hiv) ? 0 : w.bsz[o0 + b];
+                        const int rem0 = dd - wsum(mylo3);
+                        int carry = 0;
+                        for (int c = 0; c < nb; c += 32) {
+                            const int b = c + lane;
+                            int l = 0, room = 0;
+                            if (b < nb) {
+                                const int s = w.bsz[o0 + b];
+                                const bool rok = rest[b] <= hiv;
+                                const bool tok = w.hi[o0 + b] && take[b] <= hiv;
+                                l = rok ? 0 : s;
+                                room = (tok ? s : 0) - l;
+                            }
+                            const int inc = wscan_incl(room);
+                            const int ex = carry + inc - room;
+                            if (b < nb) {
+                                int left = rem0 - ex;
+                                left = left > 0 ? left : 0;
+                                w.x[o0 + b] = (uint16_t)(l + (room < left ? room : left));
+                            }
+                            carry += __shfl_sync(FULLW, inc, 31);
+                        }
+                        __syncwarp();
+                        h.improve_leaf(w, j, v);
+                    }
                 }
                 continue;
             }
@@ -466,6 +726,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, WScratch& sc, int
         if (lane == 0) {
             w.ph[j] = 0;
             w.oc[j] = -1;
+            w.oe[j] = (int16_t)S.lvl_n[j];
         }
         __syncwarp();
     }
@@ -493,6 +754,7 @@ __device__ __forceinline__ void load_cont_warp(const Cont& c, Walk& w) {
         w.used[dep] = c.used;
         w.ph[dep] = (uint8_t)c.ph;
         w.oc[dep] = c.oc;
+        w.oe[dep] = c.oe;
         if (c.ph) w.opt[dep] = (uint16_t)c.oc;
         for (int l = dep - 1; l >= 0; --l) {
             const int oc1 = lvl_off(l + 1), ol = lvl_off(l);
@@ -517,7 +779,10 @@ __device__ __forceinline__ void load_cont_warp(const Cont& c, Walk& w) {
     __syncwarp();
 }
 
-__device__ __forceinline__ void store_cont_warp(const Walk& w, int l, int ph, Cont& c) {
+// Cursor for the rest of level l: ph 1 = compositions after the current x of opt[l], then
+// the options after it up to oe[l]; ph 0 = options oc_from+1 .. oe[l]-1 (range split).
+__device__ __forceinline__ void store_cont_warp(const Walk& w, int l, int ph, Cont& c,
+                                                int oc_from = -1) {
     const int lane = lane_id();
     const int o = lvl_off(l);
     const int nb = w.nb[l];
@@ -536,7 +801,8 @@ __device__ __forceinline__ void store_cont_warp(const Walk& w, int l, int ph, Co
         c.depth = (uint16_t)l;
         c.nb = (uint16_t)nb;
         c.ph = (uint16_t)ph;
-        c.oc = ph ? (int16_t)w.opt[l] : w.oc[l];
+        c.oc = ph ? (int16_t)w.opt[l] : (int16_t)oc_from;
+        c.oe = w.oe[l];
         c.used = w.used[l];
     }
     __syncwarp();

@@ -61,6 +61,7 @@ inline bool build_spec(const Model& M, const SearchReq& q, Spec& S) {
     S.use_filter = q.use_filter;
     S.shard_rank = 0;
     S.shard_world = 1;
+    S.shard_level = 0;
     S.e1 = M.e1;
     S.e2 = M.e2;
     S.e3 = M.e3;
