@@ -67,6 +67,7 @@ struct WarpHooks {
     unsigned long long nodes, leaves;
     const Walk* w;
     int cur_level;
+    int don_period;
 
     __device__ bool hit_precedes() {  // lane 0 only
         int v0 = *(volatile int*)&ctl->ver;
@@ -85,7 +86,7 @@ struct WarpHooks {
         if (lane_id() == 0) {
             if (*(volatile int*)&ctl->abort) {
                 code = 2;
-            } else if ((steps & 7) == 0) {
+            } else if ((steps & (unsigned)(don_period - 1)) == 0) {
                 if (mode == MODE_FIRST && *(volatile int*)&ctl->has_hit && hit_precedes()) {
                     code = 2;
                 } else {
@@ -93,7 +94,7 @@ struct WarpHooks {
                     if (idle) {
                         unsigned long long qn = *(volatile unsigned long long*)&ctl->q_tail -
                                                 *(volatile unsigned long long*)&ctl->q_head;
-                        if (qn < idle) code = 3;
+                        if (qn == 0) code = 3;  // queue drained and walkers waiting
                     }
                 }
             }
@@ -211,11 +212,10 @@ struct WarpHooks {
 
 constexpr int WPC = 2;  // walkers (warps) per CTA
 
-__host__ __device__ constexpr size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-constexpr size_t SMEM_SPEC = align_up(sizeof(Spec), 16);
-constexpr size_t SMEM_WALK = align_up(sizeof(Walk), 16);
-constexpr size_t SMEM_SCR = align_up(sizeof(WScratch), 16);
-constexpr size_t SMEM_BYTES = SMEM_SPEC + WPC * (SMEM_WALK + SMEM_SCR);
+constexpr size_t SMEM_SPEC = (sizeof(Spec) + 15) & ~size_t(15);
+
+// dynamic shared memory of one CTA for a stage of k modules over G GPUs
+static size_t smem_bytes(int G, int k) { return SMEM_SPEC + WPC * walk_layout(G, k).bytes; }
 
 // One resident persistent grid per stage search.  Each warp is a walker: it pops a
 // cursor from the shared ring queue and runs the warp-cooperative DFS on it; a busy
@@ -237,8 +237,11 @@ __global__ void __launch_bounds__(32 * WPC) k_search(const Spec* Sg, Rows R, Con
     }
     const int wid = threadIdx.x >> 5;
     const int lane = lane_id();
-    Walk& w = *reinterpret_cast<Walk*>(smem + SMEM_SPEC + wid * SMEM_WALK);
-    WScratch& sc = *reinterpret_cast<WScratch*>(smem + SMEM_SPEC + WPC * SMEM_WALK + wid * SMEM_SCR);
+    const size_t wbytes = walk_layout(S.G, S.k).bytes;
+    unsigned char* wbase = smem + SMEM_SPEC + wid * wbytes;
+    Walk& w = *reinterpret_cast<Walk*>(wbase);
+    if (lane == 0) walk_carve(w, wbase, S.G, S.k);
+    __syncwarp();
     unsigned long long nodes = 0, leaves = 0;
     while (true) {
         long long ticket = -1;
@@ -262,7 +265,7 @@ __global__ void __launch_bounds__(32 * WPC) k_search(const Spec* Sg, Rows R, Con
                     idle = true;
                 }
                 __nanosleep(backoff);
-                backoff = backoff < 4096 ? backoff * 2 : 4096;
+                backoff = backoff < 8192 ? backoff * 2 : 8192;
             }
             if (idle) atomicSub(&ctl->idle, 1u);
             if (ticket >= 0) {
@@ -289,10 +292,11 @@ __global__ void __launch_bounds__(32 * WPC) k_search(const Spec* Sg, Rows R, Con
         h.leaves = 0;
         h.w = &w;
         h.cur_level = 0;
+        h.don_period = S.don_period;
         h.inc_cache = POS_INF;
         h.inc_cache = h.bcast_inc();
         const int d0 = Q[slot].depth;
-        dfs_warp(S, R, w, sc, d0, h);
+        dfs_warp(S, R, w, d0, h);
         nodes += h.nodes;
         leaves += h.leaves;
         __syncwarp();
@@ -382,6 +386,8 @@ static inline size_t pin_off(int i) {
 
 Engine::Engine(int device) : device_(device) {
     trace_ = std::getenv("MOSAIC_TRACE") != nullptr;
+    if (const char* e = std::getenv("MOSAIC_DON_DEPTH")) don_depth_ = std::atoi(e);
+    if (const char* e = std::getenv("MOSAIC_DON_PERIOD")) don_period_ = std::atoi(e);
     CK(cudaSetDevice(device));
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -498,6 +504,9 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     hs->shard_rank = rank_;
     hs->shard_world = world_;
     hs->shard_level = S.k >= 2 ? 1 : 0;  // (o_0, o_1) pairs: fine enough to balance 8 ranks
+    // donation policy: hand over only shallow levels, when the queue has run dry
+    hs->don_max_level = S.k >= 6 ? S.k - 1 - don_depth_ : S.k - 3;
+    hs->don_period = don_period_;
     std::memset(hc, 0, sizeof(Ctl));
     union {
         double d;
@@ -534,19 +543,24 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     CK(cudaMemsetAsync(d_ready_, 0, cap * sizeof(int), s));
     CK(cudaMemcpyAsync(d_ready_, hone, sizeof(int), cudaMemcpyHostToDevice, s));
     h2d_ += sizeof(Spec) + sizeof(Ctl) + sizeof(Cont) + sizeof(int);
-    if (grid_ == 0) {
-        CK(cudaFuncSetAttribute(k_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)SMEM_BYTES));
+    const size_t smem = smem_bytes(S.G, S.k);
+    if (smem != grid_smem_) {
+        if (smem > smem_attr_) {
+            CK(cudaFuncSetAttribute(k_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+            smem_attr_ = smem;
+        }
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search, 32 * WPC, SMEM_BYTES));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search, 32 * WPC, smem));
         int sms = 148;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
         grid_ = std::max(1, per_sm) * sms;  // all resident: spin-waiting needs it
+        grid_smem_ = smem;
     }
     CK(cudaEventRecord((cudaEvent_t)evk0_, s));
-    k_search<<<(unsigned)grid_, 32 * WPC, SMEM_BYTES, s>>>((const Spec*)d_spec_, R, Q, d_ready_,
-                                                           (Ctl*)d_ctl_, (HitPath*)d_best_,
-                                                           (Leaf*)d_leaf_);
+    k_search<<<(unsigned)grid_, 32 * WPC, smem, s>>>((const Spec*)d_spec_, R, Q, d_ready_,
+                                                     (Ctl*)d_ctl_, (HitPath*)d_best_,
+                                                     (Leaf*)d_leaf_);
     CK(cudaEventRecord((cudaEvent_t)evk1_, s));
     ++launches_;
     ++own_launches_;

@@ -99,7 +99,10 @@ class Engine {
     int* d_ready_ = nullptr;
     void* d_best_ = nullptr;
     long long grid_ = 0;
+    size_t grid_smem_ = 0, smem_attr_ = 0;
     bool trace_ = false;
+    int don_depth_ = 3;    // donate levels <= k-1-don_depth (measured best on cfg5)
+    int don_period_ = 32;  // power of two
     long long front_cap_ = 0;
     void* h_pin_ = nullptr;
     long long launches_ = 0;

@@ -67,6 +67,8 @@ struct Spec {
     int suffix_min[MAXK + 1];      // min quota demand d*u over levels >= j
     int shard_rank, shard_world;   // multi-GPU: this rank takes the option prefixes
     int shard_level;               //   (o_0..o_L) with shard_hash % world == rank, L = shard_level
+    int don_max_level;             // work donation: only levels <= this are handed over
+    int don_period;                // check for idle walkers every don_period option steps (2^n)
     int env_n[MAXK + 1];           // product-term envelope over unplaced levels >= j
     double env_a[MAXK + 1][MAXENV];
     double env_b[MAXK + 1][MAXENV];
@@ -118,16 +120,29 @@ struct Leaf {
 };
 
 // Block storage offsets: level j holds at most min(2^j, MAXB) blocks.
-#ifdef MG_DEVICE_CODE
-MG_HD int lvl_cap(int j) { return j >= 7 ? MAXB : (1 << j); }
-MG_HD int lvl_off(int j) {
-    int off = 0;
-    for (int i = 0; i < j; ++i) off += lvl_cap(i);
-    return off;
-}
+#if defined(__CUDACC__)
+#define MG_HX __host__ __device__ inline
+#else
+#define MG_HX inline
 #endif
-constexpr int WALK_SLOTS = 255 + (MAXK + 1 - 8) * MAXB;  // sum_{j<=MAXK} lvl_cap(j)
 
+// Blocks at level j: at most min(2^j, G) (each level splits every block in two), capped
+// at MAXB.  The walker only stores levels 0..k-1 (the last level is closed-form).
+MG_HX int lvl_capacity(int j, int G) {
+    int c = j >= 7 ? MAXB : (1 << j);
+    c = c < G ? c : G;
+    return c < MAXB ? c : MAXB;
+}
+
+// Shared-memory footprint of one walker for a stage of k modules over G GPUs.
+struct WalkLayout {
+    int slots;    // sum of level capacities
+    int nblk;     // max blocks at any stored level
+    size_t bytes; // header + arrays, 16-B aligned
+};
+
+// DFS state of one walker.  The header is fixed; the arrays it points to are carved
+// from shared memory right behind it, sized for the stage at hand (walk_layout).
 struct Walk {
     uint16_t opt[MAXK];
     int16_t oc[MAXK];
@@ -135,19 +150,63 @@ struct Walk {
     uint8_t ph[MAXK];
     uint16_t nb[MAXK + 1];
     int used[MAXK + 1];
-    uint16_t bsz[WALK_SLOTS];
-    uint16_t bmk[WALK_SLOTS];
-    uint16_t x[WALK_SLOTS];
-    uint16_t lo[WALK_SLOTS];   // admissible take count per block: [lo, hi]
-    uint16_t hi[WALK_SLOTS];
-    // parent-block stats of level `ps_lvl` (recomputed when a deeper level overwrote them)
+    int loff[MAXK + 1];  // slot offset of each level's block arrays
+    int lcap[MAXK + 1];  // block capacity of each level
     int ps_lvl;
-    int pu[MAXB];
-    double pm[MAXB], psum[MAXB], pmb[MAXB], pP[MAXB], pmx[MAXB];
-    // child-block stats (look-ahead) / last-level contributions
-    int cu[MAXB];
-    double cm[MAXB], cs[MAXB], cb[MAXB];
+    uint16_t *bsz, *bmk, *x, *lo, *hi;           // per level (loff-indexed)
+    int *pu, *cu, *sa, *sb;                      // per block of the current / child level
+    double *pm, *psum, *pmb, *pP, *pmx, *cm, *cs, *cb;
 };
+
+MG_HX size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+MG_HX WalkLayout walk_layout(int G, int k) {
+    WalkLayout L;
+    L.slots = 0;
+    L.nblk = 1;
+    for (int j = 0; j < k; ++j) {
+        const int c = lvl_capacity(j, G);
+        L.slots += c;
+        L.nblk = c > L.nblk ? c : L.nblk;
+    }
+    L.bytes = align16(sizeof(Walk)) + align16(8 * 8 * (size_t)L.nblk) +
+              align16(4 * 4 * (size_t)L.nblk) + align16(5 * 2 * (size_t)L.slots);
+    return L;
+}
+
+// Point a walker's arrays into the shared-memory region right behind its header.
+MG_HX void walk_carve(Walk& w, unsigned char* base, int G, int k) {
+    const WalkLayout L = walk_layout(G, k);
+    unsigned char* p = base + align16(sizeof(Walk));
+    double* d = reinterpret_cast<double*>(p);
+    w.pm = d;
+    w.psum = d + L.nblk;
+    w.pmb = d + 2 * L.nblk;
+    w.pP = d + 3 * L.nblk;
+    w.pmx = d + 4 * L.nblk;
+    w.cm = d + 5 * L.nblk;
+    w.cs = d + 6 * L.nblk;
+    w.cb = d + 7 * L.nblk;
+    p += align16(8 * 8 * (size_t)L.nblk);
+    int* i = reinterpret_cast<int*>(p);
+    w.pu = i;
+    w.cu = i + L.nblk;
+    w.sa = i + 2 * L.nblk;
+    w.sb = i + 3 * L.nblk;
+    p += align16(4 * 4 * (size_t)L.nblk);
+    uint16_t* u = reinterpret_cast<uint16_t*>(p);
+    w.bsz = u;
+    w.bmk = u + L.slots;
+    w.x = u + 2 * L.slots;
+    w.lo = u + 3 * L.slots;
+    w.hi = u + 4 * L.slots;
+    int off = 0;
+    for (int j = 0; j <= MAXK; ++j) {
+        w.loff[j] = off;
+        w.lcap[j] = j < k ? lvl_capacity(j, G) : 0;
+        off += w.lcap[j];
+    }
+}
 
 #ifdef MG_DEVICE_CODE
 MG_HD double envelope(const Spec& S, int j, double P) {
@@ -298,423 +357,13 @@ MG_HD void block_stats(const Spec& S, const Rows& R, const uint16_t* opt, unsign
     }
 }
 
-MG_HD int hi_minus_x(const Walk& w, int i) { return (int)w.hi[i] - (int)w.x[i]; }
-
-// First composition in descending lexicographic order with x_b in [lo_b, hi_b].
-MG_HD bool first_comp(const uint16_t* lo, const uint16_t* hi, uint16_t* x, int nb, int d) {
-    int R = d;
-    for (int b = 0; b < nb; ++b) R -= lo[b];
-    if (R < 0) return false;
-    for (int b = 0; b < nb; ++b) {
-        int room = hi[b] - lo[b];
-        int e = room < R ? room : R;
-        x[b] = (uint16_t)(lo[b] + e);
-        R -= e;
-    }
-    return R == 0;
-}
-
-MG_HD bool next_comp(const uint16_t* lo, const uint16_t* hi, uint16_t* x, int nb) {
-    if (nb < 2) return false;
-    int slack = hi[nb - 1] - x[nb - 1];
-    int extra = x[nb - 1] - lo[nb - 1];
-    int i = nb - 2;
-    for (; i >= 0; --i) {
-        if (x[i] > lo[i] && slack >= 1) break;
-        slack += hi[i] - x[i];
-        extra += x[i] - lo[i];
-    }
-    if (i < 0) return false;
-    x[i] -= 1;
-    int R = extra + 1;
-    for (int b = i + 1; b < nb; ++b) {
-        int room = hi[b] - lo[b];
-        int e = room < R ? room : R;
-        x[b] = (uint16_t)(lo[b] + e);
-        R -= e;
-    }
-    return true;
-}
-
-// Admissible take-count interval of every block at the last level for threshold t
-// (le: contribution <= t, else < t).  Returns false if some block has none or the
-// degree is unreachable.
-MG_HD bool last_intervals(const Walk& w, int o0, int nb, int d, double t, bool le,
-                          const double* rest, const double* take, int& sumlo, int& sumhi) {
-    sumlo = 0;
-    sumhi = 0;
-    for (int b = 0; b < nb; ++b) {
-        int s = w.bsz[o0 + b];
-        bool rok = le ? rest[b] <= t : rest[b] < t;
-        bool tok = w.hi[o0 + b] && (le ? take[b] <= t : take[b] < t);
-        if (rok && tok) {
-            sumhi += s;
-        } else if (rok) {
-        } else if (tok) {
-            sumlo += s;
-            sumhi += s;
-        } else {
-            return false;
-        }
-    }
-    return sumlo <= d && d <= sumhi;
-}
-
-// Does level l (at ph 1: current composition x of option opt[l]) have untried work:
-// another composition of this option, or a later option?
-MG_HD bool level_has_rest(const Spec& S, const Rows& R, const Walk& w, int l) {
-    if (w.opt[l] + 1 < S.lvl_n[l]) return true;
-    const int o0 = lvl_off(l);
-    const int nb = w.nb[l];
-    // next_comp succeeds iff some x_i > lo_i has slack to its right
-    int slack = hi_minus_x(w, o0 + nb - 1);
-    for (int i = nb - 2; i >= 0; --i) {
-        if (w.x[o0 + i] > w.lo[o0 + i] && slack >= 1) return true;
-        slack += hi_minus_x(w, o0 + i);
-    }
-    return false;
-}
-
-// Stats of the blocks of level j into the parent scratch.
-MG_HD void parent_stats(const Spec& S, const Rows& R, Walk& w, int j) {
-    const int o0 = lvl_off(j);
-    for (int b = 0; b < w.nb[j]; ++b)
-        block_stats(S, R, w.opt, w.bmk[o0 + b], j, w.pu[b], w.pm[b], w.psum[b], w.pmb[b], w.pP[b],
-                    w.pmx[b]);
-    w.ps_lvl = j;
-}
-
-// The per-thread DFS from a loaded cursor at depth d0 (see Cont).  Returns 1 on a
-// FIRST hit, 2 when abandoned (a better FIRST hit exists / MIN restart), 3 when the
-// step budget ran out and the remaining work was handed back as cursors
-// (h.split), 0 when the subtree is exhausted.
-template <class H>
-MG_HD int dfs(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
-    const int k = S.k;
-    const int GL = S.G * S.L;
-    int j = d0;
-    int floor_lvl = d0;  // levels below this were handed to other threads
-    w.ps_lvl = -1;
-    while (j >= floor_lvl) {
-        const int o0 = lvl_off(j);
-        const int nb = w.nb[j];
-        if (w.ph[j] == 0) {
-            h.level(j);
-            int ab = h.abort();
-            if (ab == 1) {
-                h.split(w, floor_lvl, j);
-                return 3;
-            }
-            if (ab == 2) return 2;
-            if (ab == 3) {
-                // hand the shallowest level that still has untried work to an idle thread
-                while (floor_lvl < j && !level_has_rest(S, R, w, floor_lvl)) ++floor_lvl;
-                if (floor_lvl < j && h.donate(w, floor_lvl)) ++floor_lvl;
-            }
-            const double thr = h.thr(S);
-            const int n = S.lvl_n[j], off = S.lvl_off[j];
-            int o = w.oc[j] + 1;
-            bool got = false;
-            for (; o < n; ++o) {
-                int r = off + o;
-                int t = opt_test(S, R, r, thr);
-                if (t == 2) break;
-                if (t == 1) continue;
-                if (w.used[j] + R.d[r] * R.u[r] + S.suffix_min[j + 1] > GL) continue;
-                got = true;
-                break;
-            }
-            if (!got) {
-                --j;
-                continue;
-            }
-            w.oc[j] = (int16_t)o;
-            w.opt[j] = (uint16_t)o;
-            const int r = off + o;
-            const int dd = R.d[r], uu = R.u[r];
-            const double ff = R.fp[r], bo = R.B[r], ba = R.base[r];
-            const bool last = j == k - 1;
-            if (w.ps_lvl != j) {
-                parent_stats(S, R, w, j);
-                if (last) {
-                    // approximate rest contributions (any summation order) for the fast filter
-                    for (int b = 0; b < nb; ++b)
-                        w.cm[b] = w.bmk[o0 + b] ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] +
-                                                      (S.additive ? 0.0 : S.e3 * w.pP[b])
-                                                : NEG_INF;
-                }
-            }
-            // per-block admissible take interval: capacity, memory, and (non-negative
-            // models) the interference bound of the taken and the remaining part
-            int sumlo = 0, sumhi = 0;
-            bool dead = false;
-            for (int b = 0; b < nb; ++b) {
-                const int s = w.bsz[o0 + b];
-                bool el = w.pu[b] + uu <= S.L && !(w.pm[b] + ff > S.cap_slack);
-                bool tok = el, rok = true;
-                if (!last && S.nonneg) {
-                    if (el) {
-                        double lbt;
-                        if (S.include_self) {
-                            double mb = w.pmb[b] > ba ? w.pmb[b] : ba;
-                            lbt = mb + S.e1 + S.e2 * (w.psum[b] + bo) +
-                                  envelope(S, j + 1, w.pP[b] * bo);
-                        } else {
-                            double bx = ba - S.e2 * bo;
-                            double mx = w.pmx[b] > bx ? w.pmx[b] : bx;
-                            lbt = mx + S.e1 + S.e2 * (w.psum[b] + bo) + envelope(S, j + 1, 0.0);
-                        }
-                        tok = !(lbt > thr);
-                    }
-                    if (w.bmk[o0 + b]) {
-                        double lbr = S.include_self
-                                         ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] +
-                                               envelope(S, j + 1, w.pP[b])
-                                         : w.pmx[b] + S.e1 + S.e2 * w.psum[b] +
-                                               envelope(S, j + 1, 0.0);
-                        rok = !(lbr > thr);
-                    }
-                }
-                int l, hgh;
-                if (rok) {
-                    l = 0;
-                    hgh = tok ? s : 0;
-                } else if (tok) {
-                    l = s;
-                    hgh = s;
-                } else {
-                    dead = true;
-                    break;
-                }
-                w.lo[o0 + b] = (uint16_t)l;
-                w.hi[o0 + b] = (uint16_t)hgh;
-                sumlo += l;
-                sumhi += hgh;
-            }
-            if (dead || sumlo > dd || sumhi < dd) continue;
-            if (last) {
-                // ---- last level: closed form over blocks ----
-                h.count_leaf();
-                if (S.include_self) {
-                    // fast filter with approximate contributions and a 1e-12 slack: exact
-                    // values differ by a few ulps, so a rejection here is always sound
-                    // MIN rejects ties with the incumbent (and anything within TIE_EPS
-                    // below it): the planner only ever needs T* to that precision.
-                    const bool fm = S.mode == MODE_FIRST;
-                    const double tx = fm ? S.theta * (1.0 + 1e-12) : h.incumbent() * (1.0 - TIE_EPS);
-                    int flo = 0, fhi = 0;
-                    bool fdead = false;
-                    for (int b = 0; b < nb; ++b) {
-                        const int s = w.bsz[o0 + b];
-                        bool rok = fm ? w.cm[b] <= tx : w.cm[b] < tx;
-                        bool tok = false;
-                        if (w.hi[o0 + b]) {
-                            double mb = w.pmb[b] > ba ? w.pmb[b] : ba;
-                            double tv = mb + S.e1 + S.e2 * (w.psum[b] + bo) +
-                                        (S.additive ? 0.0 : S.e3 * (w.pP[b] * bo));
-                            tok = fm ? tv <= tx : tv < tx;
-                        }
-                        if (rok) {
-                            fhi += tok ? s : 0;
-                        } else if (tok) {
-                            flo += s;
-                            fhi += s;
-                        } else {
-                            fdead = true;
-                            break;
-                        }
-                    }
-                    if (fdead || flo > dd || fhi < dd) continue;
-                }
-                double* rest = w.cs;
-                double* take = w.cb;
-                for (int b = 0; b < nb; ++b) {
-                    unsigned m = w.bmk[o0 + b];
-                    rest[b] = contrib(S, R, w.opt, m);
-                    take[b] = w.hi[o0 + b] ? contrib(S, R, w.opt, m | (1u << j)) : POS_INF;
-                }
-                if (S.mode == MODE_FIRST) {
-                    int lo, hi;
-                    if (!(0.0 <= S.theta)) continue;
-                    if (!last_intervals(w, o0, nb, dd, S.theta, true, rest, take, lo, hi)) continue;
-                    // greedy first composition (descending lexicographic)
-                    int rem = dd - lo;
-                    for (int b = 0; b < nb; ++b) {
-                        int s = w.bsz[o0 + b];
-                        bool rok = rest[b] <= S.theta;
-                        bool tok = w.hi[o0 + b] && take[b] <= S.theta;
-                        int l = (!rok) ? s : 0;
-                        int hgh = tok ? s : 0;
-                        int e = hgh - l < rem ? hgh - l : rem;
-                        w.x[o0 + b] = (uint16_t)(l + e);
-                        rem -= e;
-                    }
-                    double v = 0.0;
-                    for (int b = 0; b < nb; ++b) {
-                        int xb = w.x[o0 + b], s = w.bsz[o0 + b];
-                        if (xb > 0 && take[b] > v) v = take[b];
-                        if (xb < s && rest[b] > v) v = rest[b];
-                    }
-                    h.hit(w, j, v);
-                    return 1;
-                } else {
-                    double I = h.incumbent();
-                    double Ie = I * (1.0 - TIE_EPS);
-                    int lo, hi;
-                    if (!last_intervals(w, o0, nb, dd, Ie, false, rest, take, lo, hi)) continue;
-                    double hiv = Ie;
-                    while (true) {
-                        double c = NEG_INF;
-                        for (int b = 0; b < nb; ++b) {
-                            if (rest[b] < hiv && rest[b] > c) c = rest[b];
-                            if (w.hi[o0 + b] && take[b] < hiv && take[b] > c) c = take[b];
-                        }
-                        if (c <= NEG_INF) break;
-                        if (last_intervals(w, o0, nb, dd, c, true, rest, take, lo, hi)) {
-                            hiv = c;
-                        } else {
-                            break;
-                        }
-                    }
-                    double v = hiv > 0.0 ? hiv : 0.0;
-                    if (v < I) h.improve(v);
-                }
-                continue;
-            }
-            if (!first_comp(w.lo + o0, w.hi + o0, w.x + o0, nb, dd)) continue;
-            w.ph[j] = 1;
-        } else {
-            if (!next_comp(w.lo + o0, w.hi + o0, w.x + o0, nb)) {
-                w.ph[j] = 0;
-                continue;
-            }
-        }
-        // ---- build the child (level j+1 blocks + their stats) ----
-        h.count_node();
-        if (w.ps_lvl != j) parent_stats(S, R, w, j);
-        const int o1 = lvl_off(j + 1);
-        const int c1 = lvl_cap(j + 1);
-        const int r = S.lvl_off[j] + w.opt[j];
-        const int uu = R.u[r];
-        const double ff = R.fp[r], bo = R.B[r], ba = R.base[r];
-        int m = 0;
-        bool overflow = false;
-        for (int b = 0; b < nb; ++b) {
-            int xb = w.x[o0 + b], s = w.bsz[o0 + b];
-            unsigned mk = w.bmk[o0 + b];
-            if (xb > 0) {
-                if (m >= c1) { overflow = true; break; }
-                w.bsz[o1 + m] = (uint16_t)xb;
-                w.bmk[o1 + m] = (uint16_t)(mk | (1u << j));
-                w.cu[m] = w.pu[b] + uu;
-                w.cm[m] = w.pm[b] + ff;
-                w.cs[m] = w.psum[b] + bo;
-                w.cb[m] = w.pmb[b] > ba ? w.pmb[b] : ba;
-                ++m;
-            }
-            if (xb < s) {
-                if (m >= c1) { overflow = true; break; }
-                w.bsz[o1 + m] = (uint16_t)(s - xb);
-                w.bmk[o1 + m] = (uint16_t)mk;
-                w.cu[m] = w.pu[b];
-                w.cm[m] = w.pm[b];
-                w.cs[m] = w.psum[b];
-                w.cb[m] = w.pmb[b];
-                ++m;
-            }
-        }
-        if (overflow) {
-            h.overflow();
-            return 2;
-        }
-        w.nb[j + 1] = (uint16_t)m;
-        w.used[j + 1] = w.used[j] + R.d[r] * R.u[r];
-        const double thr = h.thr(S);
-        bool prune = false;
-        // look-ahead: every unplaced level keeps an option that fits somewhere
-        for (int l = j + 1; l < k && !prune; ++l) {
-            const int n = S.lvl_n[l], off = S.lvl_off[l];
-            bool ok = false;
-            for (int o = 0; o < n && !ok; ++o) {
-                int rr = off + o;
-                int t = opt_test(S, R, rr, thr);
-                if (t == 2) break;
-                if (t == 1) continue;
-                const int dd = R.d[rr], u2 = R.u[rr];
-                const double f2 = R.fp[rr], b2 = R.B[rr], a2 = R.base[rr];
-                int cnt = 0;
-                for (int b = 0; b < m; ++b) {
-                    if (w.cu[b] + u2 > S.L) continue;
-                    if (w.cm[b] + f2 > S.cap_slack) continue;
-                    if (S.nonneg && S.include_self) {
-                        double mb = w.cb[b] > a2 ? w.cb[b] : a2;
-                        if (mb + S.e1 + S.e2 * (w.cs[b] + b2) > thr) continue;
-                    }
-                    cnt += w.bsz[o1 + b];
-                    if (cnt >= dd) break;
-                }
-                ok = cnt >= dd;
-            }
-            if (!ok) prune = true;
-        }
-        if (prune) continue;
-        ++j;
-        w.ph[j] = 0;
-        w.oc[j] = -1;
-    }
-    return 0;
-}
-
-// Load a cursor into a walk.
-MG_HD void load_cont(const Cont& c, Walk& w) {
-    const int dep = c.depth;
-    for (int l = 0; l < dep; ++l) w.opt[l] = c.opt[l];
-    const int o = lvl_off(dep);
-    w.nb[dep] = c.nb;
-    w.used[dep] = c.used;
-    w.ph[dep] = (uint8_t)c.ph;
-    w.oc[dep] = c.oc;
-    if (c.ph) w.opt[dep] = (uint16_t)c.oc;
-    for (int b = 0; b < c.nb; ++b) {
-        w.bsz[o + b] = c.bsz[b];
-        w.bmk[o + b] = c.bmk[b];
-        if (c.ph) {
-            w.x[o + b] = c.x[b];
-            w.lo[o + b] = c.lo[b];
-            w.hi[o + b] = c.hi[b];
-        }
-    }
-    // Rebuild the blocks and compositions of every ancestor level: level l+1 lists each
-    // parent block as (taken part, rest part), adjacent, with masks differing in bit l.
-    for (int l = dep - 1; l >= 0; --l) {
-        const int oc1 = lvl_off(l + 1), ol = lvl_off(l);
-        const unsigned bit = 1u << l;
-        int nbl = 0;
-        for (int b = 0; b < w.nb[l + 1];) {
-            const unsigned key = w.bmk[oc1 + b] & ~bit;
-            int size = 0, taken = 0;
-            while (b < w.nb[l + 1] && (w.bmk[oc1 + b] & ~bit) == key) {
-                size += w.bsz[oc1 + b];
-                if (w.bmk[oc1 + b] & bit) taken += w.bsz[oc1 + b];
-                ++b;
-            }
-            w.bsz[ol + nbl] = (uint16_t)size;
-            w.bmk[ol + nbl] = (uint16_t)key;
-            w.x[ol + nbl] = (uint16_t)taken;
-            ++nbl;
-        }
-        w.nb[l] = (uint16_t)nbl;
-    }
-}
-
-
 // -1: path H precedes the walk's leaf path (levels 0..j), +1 follows it, 0 equal.
 template <class HP>
 MG_HD int path_cmp(const HP* H, const Walk& w, int j) {
     for (int l = 0; l <= j; ++l) {
         int ho = H->opt[l];
         if (ho != w.opt[l]) return ho < w.opt[l] ? -1 : 1;
-        const int o0 = lvl_off(l);
+        const int o0 = w.loff[l];
         for (int b = 0; b < w.nb[l]; ++b) {
             int hx = H->x[l][b], wx = w.x[o0 + b];
             if (hx != wx) return hx > wx ? -1 : 1;  // larger count first
@@ -730,7 +379,7 @@ MG_HD bool path_precedes_rest(const HP* H, const Walk& w, int j) {
     for (int l = 0; l < j; ++l) {
         int ho = H->opt[l];
         if (ho != w.opt[l]) return ho < w.opt[l];
-        const int o0 = lvl_off(l);
+        const int o0 = w.loff[l];
         for (int b = 0; b < w.nb[l]; ++b) {
             int hx = H->x[l][b], wx = w.x[o0 + b];
             if (hx != wx) return hx > wx;
@@ -744,30 +393,8 @@ MG_HD void path_store(HP* H, const Walk& w, int j) {
     for (int l = 0; l <= j; ++l) {
         H->opt[l] = w.opt[l];
         H->nb[l] = w.nb[l];
-        const int o0 = lvl_off(l);
+        const int o0 = w.loff[l];
         for (int b = 0; b < w.nb[l]; ++b) H->x[l][b] = w.x[o0 + b];
-    }
-}
-
-// Cursor for "the rest of level l": options after oc[l] (ph 0) or compositions after
-// the current x (ph 1).
-MG_HD void store_cont(const Walk& w, int l, int ph, unsigned long long key, Cont& c) {
-    c.key = key;
-    for (int i = 0; i < MAXK; ++i) c.opt[i] = i < l ? w.opt[i] : 0;
-    c.depth = (uint16_t)l;
-    c.nb = w.nb[l];
-    c.ph = (uint16_t)ph;
-    c.oc = ph ? (int16_t)w.opt[l] : w.oc[l];
-    c.used = w.used[l];
-    const int o = lvl_off(l);
-    for (int b = 0; b < c.nb; ++b) {
-        c.bsz[b] = w.bsz[o + b];
-        c.bmk[b] = w.bmk[o + b];
-        if (ph) {
-            c.x[b] = w.x[o + b];
-            c.lo[b] = w.lo[o + b];
-            c.hi[b] = w.hi[o + b];
-        }
     }
 }
 
@@ -775,7 +402,7 @@ MG_HD void store_cont(const Walk& w, int l, int ph, unsigned long long key, Cont
 MG_HD void store_leaf(const Walk& w, int j, double v, Leaf& lf) {
     lf.value = v;
     for (int l = 0; l <= j; ++l) lf.opt[l] = w.opt[l];
-    int o0 = lvl_off(j);
+    int o0 = w.loff[j];
     int m = 0;
     for (int b = 0; b < w.nb[j]; ++b) {
         int xb = w.x[o0 + b], s = w.bsz[o0 + b];

@@ -34,13 +34,9 @@ __device__ __forceinline__ int wscan_incl(int v) {
     return v;
 }
 
-struct WScratch {  // per-walker scratch for prefix sums
-    int sa[MAXB];
-    int sb[MAXB];
-};
 
 __device__ __forceinline__ void parent_stats_warp(const Spec& S, const Rows& R, Walk& w, int j) {
-    const int o0 = lvl_off(j);
+    const int o0 = w.loff[j];
     for (int b = lane_id(); b < w.nb[j]; b += 32)
         block_stats(S, R, w.opt, w.bmk[o0 + b], j, w.pu[b], w.pm[b], w.psum[b], w.pmb[b], w.pP[b],
                     w.pmx[b]);
@@ -72,7 +68,7 @@ __device__ __forceinline__ bool first_comp_warp(Walk& w, int o0, int nb, int d) 
 }
 
 // next composition in descending lexicographic order within [lo, hi]
-__device__ __forceinline__ bool next_comp_warp(Walk& w, WScratch& sc, int o0, int nb) {
+__device__ __forceinline__ bool next_comp_warp(Walk& w, int o0, int nb) {
     if (nb < 2) return false;
     const int lane = lane_id();
     // inclusive prefix of slack_t = hi_t - x_t and extra_t = x_t - lo_t
@@ -83,8 +79,8 @@ __device__ __forceinline__ bool next_comp_warp(Walk& w, WScratch& sc, int o0, in
         const int ex = b < nb ? (int)w.x[o0 + b] - (int)w.lo[o0 + b] : 0;
         const int is = wscan_incl(sl), ie = wscan_incl(ex);
         if (b < nb) {
-            sc.sa[b] = cs + is;
-            sc.sb[b] = ce + ie;
+            w.sa[b] = cs + is;
+            w.sb[b] = ce + ie;
         }
         cs += __shfl_sync(FULLW, is, 31);
         ce += __shfl_sync(FULLW, ie, 31);
@@ -93,10 +89,10 @@ __device__ __forceinline__ bool next_comp_warp(Walk& w, WScratch& sc, int o0, in
     // rightmost i <= nb-2 with x_i > lo_i and slack to its right
     int best = -1;
     for (int i = lane; i < nb - 1; i += 32)
-        if (w.x[o0 + i] > w.lo[o0 + i] && cs - sc.sa[i] >= 1) best = i;
+        if (w.x[o0 + i] > w.lo[o0 + i] && cs - w.sa[i] >= 1) best = i;
     const int is = wmaxi(best);
     if (is < 0) return false;
-    const int R = (ce - sc.sb[is]) + 1;  // extra to the right of i*, plus the one unit
+    const int R = (ce - w.sb[is]) + 1;  // extra to the right of i*, plus the one unit
     __syncwarp();
     if (lane == 0) w.x[o0 + is] -= 1;
     int carry = 0;
@@ -141,24 +137,24 @@ __device__ __forceinline__ bool last_feasible_warp(const Walk& w, int o0, int nb
     return !wany(dead) && L <= d && d <= H;
 }
 
-__device__ __forceinline__ bool level_has_rest_warp(const Spec& S, const Walk& w, WScratch& sc,
+__device__ __forceinline__ bool level_has_rest_warp(const Spec& S, const Walk& w,
                                                     int l) {
     if (w.opt[l] + 1 < S.lvl_n[l]) return true;
     const int lane = lane_id();
-    const int o0 = lvl_off(l);
+    const int o0 = w.loff[l];
     const int nb = w.nb[l];
     int cs = 0;
     for (int c = 0; c < nb; c += 32) {
         const int b = c + lane;
         const int sl = b < nb ? (int)w.hi[o0 + b] - (int)w.x[o0 + b] : 0;
         const int is = wscan_incl(sl);
-        if (b < nb) sc.sa[b] = cs + is;
+        if (b < nb) w.sa[b] = cs + is;
         cs += __shfl_sync(FULLW, is, 31);
     }
     __syncwarp();
     bool any = false;
     for (int i = lane; i < nb - 1; i += 32)
-        if (w.x[o0 + i] > w.lo[o0 + i] && cs - sc.sa[i] >= 1) any = true;
+        if (w.x[o0 + i] > w.lo[o0 + i] && cs - w.sa[i] >= 1) any = true;
     const bool r = wany(any);
     __syncwarp();
     return r;
@@ -235,7 +231,7 @@ __device__ __forceinline__ bool lane_last_feasible(const Spec& S, const Rows& R,
 template <class H>
 __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, int& ps_lvl, H& h) {
     const int lane = lane_id();
-    const int o0 = lvl_off(j), nb = w.nb[j];
+    const int o0 = w.loff[j], nb = w.nb[j];
     const int GL = S.G * S.L;
     if (ps_lvl != j) {
         parent_stats_warp(S, R, w, j);
@@ -379,7 +375,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
 }
 
 template <class H>
-__device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, WScratch& sc, int d0, H& h) {
+__device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
     const int lane = lane_id();
     const int k = S.k;
     const int GL = S.G * S.L;
@@ -387,17 +383,18 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, WScratch& sc, int
     int floor_lvl = d0;
     int ps_lvl = -1;
     while (j >= floor_lvl) {
-        const int o0 = lvl_off(j);
+        const int o0 = w.loff[j];
         const int nb = w.nb[j];
         if (w.ph[j] == 0) {
             h.level(j);
             const int ab = h.abort();
             if (ab == 2) return 2;
             if (ab == 3) {
-                while (floor_lvl < j && !level_has_rest_warp(S, w, sc, floor_lvl)) ++floor_lvl;
-                if (floor_lvl < j) {
+                // only shallow work is worth a hand-over (cursor traffic beats tiny subtrees)
+                while (floor_lvl < j && !level_has_rest_warp(S, w, floor_lvl)) ++floor_lvl;
+                if (floor_lvl < j && floor_lvl <= S.don_max_level) {
                     if (h.donate(w, floor_lvl, 1, -1)) ++floor_lvl;
-                } else if (j < k - 1) {
+                } else if (floor_lvl == j && j <= S.don_max_level) {
                     // all that is left is this level's option range: hand over its upper half
                     const int a = w.oc[j] + 1, e = w.oe[j];
                     if (e - a >= 2) {
@@ -633,7 +630,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, WScratch& sc, int
             if (lane == 0) w.ph[j] = 1;
             __syncwarp();
         } else {
-            if (!next_comp_warp(w, sc, o0, nb)) {
+            if (!next_comp_warp(w, o0, nb)) {
                 if (lane == 0) w.ph[j] = 0;
                 __syncwarp();
                 continue;
@@ -645,8 +642,8 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, WScratch& sc, int
             parent_stats_warp(S, R, w, j);
             ps_lvl = j;
         }
-        const int o1 = lvl_off(j + 1);
-        const int c1 = lvl_cap(j + 1);
+        const int o1 = w.loff[j + 1];
+        const int c1 = w.lcap[j + 1];
         const int r = S.lvl_off[j] + w.opt[j];
         const int uu = R.u[r];
         const double ff = R.fp[r], bo = R.B[r], ba = R.base[r];
@@ -737,7 +734,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, WScratch& sc, int
 __device__ __forceinline__ void load_cont_warp(const Cont& c, Walk& w) {
     const int lane = lane_id();
     const int dep = c.depth;
-    const int o = lvl_off(dep);
+    const int o = w.loff[dep];
     for (int b = lane; b < c.nb; b += 32) {
         w.bsz[o + b] = c.bsz[b];
         w.bmk[o + b] = c.bmk[b];
@@ -757,7 +754,7 @@ __device__ __forceinline__ void load_cont_warp(const Cont& c, Walk& w) {
         w.oe[dep] = c.oe;
         if (c.ph) w.opt[dep] = (uint16_t)c.oc;
         for (int l = dep - 1; l >= 0; --l) {
-            const int oc1 = lvl_off(l + 1), ol = lvl_off(l);
+            const int oc1 = w.loff[l + 1], ol = w.loff[l];
             const unsigned bit = 1u << l;
             int nbl = 0;
             for (int b = 0; b < w.nb[l + 1];) {
@@ -784,7 +781,7 @@ __device__ __forceinline__ void load_cont_warp(const Cont& c, Walk& w) {
 __device__ __forceinline__ void store_cont_warp(const Walk& w, int l, int ph, Cont& c,
                                                 int oc_from = -1) {
     const int lane = lane_id();
-    const int o = lvl_off(l);
+    const int o = w.loff[l];
     const int nb = w.nb[l];
     for (int b = lane; b < nb; b += 32) {
         c.bsz[b] = w.bsz[o + b];
