@@ -37,6 +37,9 @@ inline std::vector<int> probe_ok;
 #endif
 
 #include "mosaic/bench.hpp"
+#ifdef MOSAIC_WITH_IO
+#include "mosaic/io.hpp"
+#endif
 #include "mosaic/oracle.hpp"
 #include "mosaic/profiler.hpp"
 #include "mosaic/solver.hpp"
@@ -383,6 +386,19 @@ int main(int argc, char** argv) {
                 p = q + 1;
             }
             pd("t", stage_time(in.ctx, al), false);
+#ifdef MOSAIC_WITH_IO
+        } else if (op == "json") {
+            // reference JSON v1 files for this instance (io.hpp) + the plan solve() returns
+            SolveConfig cfg{L, 1e-3, prune, cache};
+            auto r = solve(in.ctx, in.cluster, cfg);
+            nlohmann::json j;
+            j["model"] = to_json(in.graph);
+            j["cluster"] = to_json(in.cluster);
+            j["profile"] = to_json(in.surfaces);
+            j["interference"] = to_json(in.im);
+            j["plan"] = to_json(r.plan, in.graph);
+            std::printf("\"files\":%s", j.dump().c_str());
+#endif
         } else if (op == "partitions") {
             auto parts = enumerate_partitions(in.graph);
             std::printf("\"count\":%zu", parts.size());

@@ -83,31 +83,6 @@ Sample Surface::lookup(int d, double a) const {
                   blend(&Point::sm_active)};
 }
 
-std::vector<Cand> candidate_options(const Problem& P, int m, int levels) {
-    const Module& mod = P.modules.at(m);
-    const Surface& s = mod.surface;
-    std::vector<Cand> out;
-    for (double dv : s.d_values()) {
-        int d = (int)dv;
-        if (d > P.gpu_count) continue;
-        for (int units = 1; units <= levels; ++units) {
-            double a = (double)units / levels;
-            if (a < s.min_a() - kTol || a > s.max_a() + kTol) continue;
-            double fp = s.lookup(d, a).memory + mod.memory_base;
-            if (fp > P.memory_capacity) continue;
-            Sample smp = s.lookup(d, a);
-            double B = s.lookup(1, a).bandwidth_util;
-            out.push_back(Cand{d, units, smp.latency, B, fp});
-        }
-    }
-    std::sort(out.begin(), out.end(), [](const Cand& x, const Cand& y) {
-        if (x.base != y.base) return x.base < y.base;
-        if (x.d != y.d) return x.d < y.d;
-        return x.units < y.units;
-    });
-    return out;
-}
-
 std::string validate_graph(const Problem& P) {
     std::set<std::string> seen;
     for (const auto& m : P.modules)

@@ -6,7 +6,7 @@
 // from the reference so the packed tables are bit-identical (compile with
 // -ffp-contract=off, no -march=native):
 //   ScalingSurface ctor/lookup/bracket   perf_model.hpp:57-79, 124-147, 155-194
-//   candidate_options                    stage_eval.hpp:68-93
+//   candidate_options                    stage_eval.hpp:68-93 (on the device: pack.cu)
 //   evaluate_workload/generate_surfaces  profiler.hpp:57-111
 //   make_workload/make_spec/presets      profiler.hpp:185-285
 //   random_instance                      profiler.hpp:304-338
@@ -38,6 +38,8 @@ class Surface {
     Surface(std::string id, const std::vector<Point>& pts);
     Sample lookup(int d, double a) const;
     const std::vector<double>& d_values() const { return dv_; }
+    const std::vector<double>& a_values() const { return av_; }
+    const std::vector<Point>& grid() const { return grid_; }  // [di * |a| + ai]
     double min_a() const { return av_.front(); }
     double max_a() const { return av_.back(); }
     int min_d() const { return (int)dv_.front(); }
@@ -81,8 +83,6 @@ struct Cand {  // CandidateOption (stage_eval.hpp:58-63)
     double base, B, fp;
 };
 
-// candidate_options for module m (stage_eval.hpp:68-93); throws RangeError like lookup.
-std::vector<Cand> candidate_options(const Problem& P, int m, int levels);
 
 // core.hpp helpers
 std::string validate_graph(const Problem& P);  // "" when valid

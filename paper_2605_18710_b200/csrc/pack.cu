@@ -1,0 +1,220 @@
+// pack.cu — candidate-option tables built on the device.
+//
+// k_pack_options: one CTA per module.  Threads enumerate (d, units) over the profiled d
+// axis and the quota lattice, evaluate the surface lookup (perf_model.hpp:124-147,
+// bracket :174-192, restated operation for operation; -fmad=false), apply the hull and
+// memory filters of candidate_options (stage_eval.hpp:68-85), then the CTA sorts the rows
+// by (base latency, d, units) (stage_eval.hpp:87-91) with a bitonic sort in shared memory
+// and writes the flat SoA table the search kernels read.  The host only ships the raw
+// surface grids.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "pack.hpp"
+
+namespace mg {
+
+#define CKP(x)                                                                         \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess)                                                         \
+            throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e_) + \
+                                     " at " #x);                                       \
+    } while (0)
+
+constexpr int PK_THREADS = 256;
+constexpr int PK_MAXROWS = 1024;  // d values x quota levels per module (32 KB of smem)
+constexpr double PK_TOL = 1e-12;  // kAxisTolerance, perf_model.hpp:50
+
+struct PackSurf {  // one module's grid, SoA, axes ascending
+    int nd, na;
+    int goff;      // offset of its grid in the flat arrays (nd*na points)
+    double membase;
+    double dv[PACK_MAXD], av[PACK_MAXA];
+};
+
+__device__ void bracket_dev(const double* ax, int n, double v, bool lg, int& lo, int& hi,
+                            double& w) {
+    for (int i = 0; i < n; ++i) {
+        double av = fabs(v) > 1.0 ? fabs(v) : 1.0;
+        if (fabs(ax[i] - v) <= PK_TOL * av) {
+            lo = hi = i;
+            w = 0.0;
+            return;
+        }
+    }
+    int h = 0;
+    while (h < n && !(v < ax[h])) ++h;
+    int l = h - 1;
+    double sv = lg ? log2(v) : v, sl = lg ? log2(ax[l]) : ax[l], sh = lg ? log2(ax[h]) : ax[h];
+    lo = l;
+    hi = h;
+    w = (sv - sl) / (sh - sl);
+}
+
+// ScalingSurface::lookup: field 0 latency, 1 bandwidth_util, 2 memory
+__device__ double lookup_dev(const PackSurf& s, const double* g0, const double* g1,
+                             const double* g2, int d, double a, int field) {
+    int dl, dh, al, ah;
+    double wd, wa;
+    bracket_dev(s.dv, s.nd, (double)d, true, dl, dh, wd);
+    bracket_dev(s.av, s.na, a, false, al, ah, wa);
+    const double* g = field == 0 ? g0 : (field == 1 ? g1 : g2);
+    g += s.goff;
+    if (dl == dh && al == ah) return g[dl * s.na + al];
+    double v00 = g[dl * s.na + al], v01 = g[dl * s.na + ah];
+    double v10 = g[dh * s.na + al], v11 = g[dh * s.na + ah];
+    double lo = v00 + (v01 - v00) * wa;
+    double hi = v10 + (v11 - v10) * wa;
+    return lo + (hi - lo) * wd;
+}
+
+struct PRow {
+    double base, B, fp;
+    int d, u;
+};
+
+__device__ bool row_less(const PRow& x, const PRow& y) {
+    if (x.base != y.base) return x.base < y.base;
+    if (x.d != y.d) return x.d < y.d;
+    return x.u < y.u;
+}
+
+__global__ void __launch_bounds__(PK_THREADS)
+    k_pack_options(const PackSurf* surfs, const double* glat, const double* gbw,
+                   const double* gmem, int G, int L, double cap, int* counts, int* errs,
+                   PRow* out) {
+    __shared__ PRow rows[PK_MAXROWS];
+    __shared__ int n;
+    const PackSurf& s = surfs[blockIdx.x];
+    if (threadIdx.x == 0) n = 0;
+    __syncthreads();
+    const double amin = s.av[0], amax = s.av[s.na - 1];
+    const bool has_d1 = (int)s.dv[0] <= 1 && 1 <= (int)s.dv[s.nd - 1];
+    for (int c = threadIdx.x; c < s.nd * L; c += blockDim.x) {
+        const int di = c / L, units = c % L + 1;
+        const int d = (int)s.dv[di];
+        if (d > G) continue;
+        const double a = (double)units / L;
+        if (a < amin - PK_TOL || a > amax + PK_TOL) continue;
+        if (!has_d1) {  // solo_bandwidth looks up d = 1 (perf_model.hpp:420-422)
+            errs[blockIdx.x] = 1;
+            continue;
+        }
+        const double fp = lookup_dev(s, glat, gbw, gmem, d, a, 2) + s.membase;
+        if (fp > cap) continue;
+        PRow r;
+        r.base = lookup_dev(s, glat, gbw, gmem, d, a, 0);
+        r.B = lookup_dev(s, glat, gbw, gmem, 1, a, 1);
+        r.fp = fp;
+        r.d = d;
+        r.u = units;
+        int slot = atomicAdd(&n, 1);
+        if (slot < PK_MAXROWS) rows[slot] = r;
+    }
+    __syncthreads();
+    const int cnt = n < PK_MAXROWS ? n : PK_MAXROWS;
+    int pw = 1;
+    while (pw < cnt) pw <<= 1;
+    for (int i = cnt + threadIdx.x; i < pw; i += blockDim.x) {
+        rows[i].base = 1e308;  // padding sorts last
+        rows[i].d = 1 << 30;
+        rows[i].u = 1 << 30;
+    }
+    __syncthreads();
+    // bitonic sort by (base, d, units)
+    for (int k = 2; k <= pw; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < pw; i += blockDim.x) {
+                int p = i ^ j;
+                if (p > i) {
+                    bool up = (i & k) == 0;
+                    PRow x = rows[i], y = rows[p];
+                    if (up ? row_less(y, x) : row_less(x, y)) {
+                        rows[i] = y;
+                        rows[p] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) out[blockIdx.x * PK_MAXROWS + i] = rows[i];
+    if (threadIdx.x == 0) counts[blockIdx.x] = n > PK_MAXROWS ? -1 : n;
+}
+
+std::vector<std::vector<PackedRow>> pack_options_device(const std::vector<PackInput>& mods, int G,
+                                                        int L, double cap, int device,
+                                                        long long* h2d_bytes,
+                                                        std::vector<int>* range_err) {
+    CKP(cudaSetDevice(device));
+    const int M = (int)mods.size();
+    std::vector<std::vector<PackedRow>> res(M);
+    if (M == 0) return res;
+    std::vector<PackSurf> hs(M);
+    std::vector<double> lat, bw, mem;
+    for (int m = 0; m < M; ++m) {
+        const PackInput& in = mods[m];
+        if ((int)in.dv.size() > PACK_MAXD || (int)in.av.size() > PACK_MAXA)
+            throw std::runtime_error("surface grid too large for the packing kernel");
+        PackSurf& s = hs[m];
+        s.nd = (int)in.dv.size();
+        s.na = (int)in.av.size();
+        s.goff = (int)lat.size();
+        s.membase = in.membase;
+        for (int i = 0; i < s.nd; ++i) s.dv[i] = in.dv[i];
+        for (int i = 0; i < s.na; ++i) s.av[i] = in.av[i];
+        lat.insert(lat.end(), in.lat.begin(), in.lat.end());
+        bw.insert(bw.end(), in.bw.begin(), in.bw.end());
+        mem.insert(mem.end(), in.mem.begin(), in.mem.end());
+    }
+    for (const auto& in : mods)
+        if ((long long)L * (long long)in.dv.size() > PK_MAXROWS)
+            throw std::runtime_error("quota_levels x d values exceed the packing kernel");
+    PackSurf* ds;
+    double *dl, *db, *dm;
+    int *dc, *derr;
+    PRow* dout;
+    const size_t npts = std::max<size_t>(1, lat.size());
+    CKP(cudaMalloc(&ds, sizeof(PackSurf) * M));
+    CKP(cudaMalloc(&dl, 8 * npts));
+    CKP(cudaMalloc(&db, 8 * npts));
+    CKP(cudaMalloc(&dm, 8 * npts));
+    CKP(cudaMalloc(&dc, sizeof(int) * M));
+    CKP(cudaMalloc(&derr, sizeof(int) * M));
+    CKP(cudaMalloc(&dout, sizeof(PRow) * PK_MAXROWS * M));
+    CKP(cudaMemcpy(ds, hs.data(), sizeof(PackSurf) * M, cudaMemcpyHostToDevice));
+    CKP(cudaMemcpy(dl, lat.data(), 8 * lat.size(), cudaMemcpyHostToDevice));
+    CKP(cudaMemcpy(db, bw.data(), 8 * bw.size(), cudaMemcpyHostToDevice));
+    CKP(cudaMemcpy(dm, mem.data(), 8 * mem.size(), cudaMemcpyHostToDevice));
+    CKP(cudaMemset(derr, 0, sizeof(int) * M));
+    if (h2d_bytes) *h2d_bytes += (long long)(sizeof(PackSurf) * M + 24 * lat.size());
+    k_pack_options<<<M, PK_THREADS>>>(ds, dl, db, dm, G, L, cap, dc, derr, dout);
+    CKP(cudaGetLastError());
+    std::vector<int> counts(M), errs(M);
+    std::vector<PRow> rows((size_t)PK_MAXROWS * M);
+    CKP(cudaMemcpy(counts.data(), dc, sizeof(int) * M, cudaMemcpyDeviceToHost));
+    CKP(cudaMemcpy(errs.data(), derr, sizeof(int) * M, cudaMemcpyDeviceToHost));
+    CKP(cudaMemcpy(rows.data(), dout, sizeof(PRow) * rows.size(), cudaMemcpyDeviceToHost));
+    cudaFree(ds);
+    cudaFree(dl);
+    cudaFree(db);
+    cudaFree(dm);
+    cudaFree(dc);
+    cudaFree(derr);
+    cudaFree(dout);
+    if (range_err) range_err->assign(errs.begin(), errs.end());
+    for (int m = 0; m < M; ++m) {
+        if (counts[m] < 0) throw std::runtime_error("too many candidate options for one module");
+        for (int i = 0; i < counts[m]; ++i) {
+            const PRow& r = rows[(size_t)m * PK_MAXROWS + i];
+            res[m].push_back(PackedRow{r.d, r.u, r.base, r.B, r.fp});
+        }
+    }
+    return res;
+}
+
+}  // namespace mg

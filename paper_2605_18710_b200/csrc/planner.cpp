@@ -1,5 +1,6 @@
 // planner.cpp — see planner.hpp.  Compiled with -ffp-contract=off.
 #include "planner.hpp"
+#include "pack.hpp"
 
 #include <algorithm>
 #include <bit>
@@ -46,13 +47,29 @@ Planner::Planner(Problem P, int device) : P_(std::move(P)) {
     M_.include_self = P_.include_self;
     opts_.resize(P_.modules.size());
     opt_err_.resize(P_.modules.size());
+    // candidate_options of every module, built on the device (pack.cu)
+    std::vector<mg::PackInput> pin(P_.modules.size());
+    for (size_t m = 0; m < P_.modules.size(); ++m) {
+        const Surface& s = P_.modules[m].surface;
+        pin[m].dv = s.d_values();
+        pin[m].av = s.a_values();
+        for (const auto& p : s.grid()) {
+            pin[m].lat.push_back(p.latency);
+            pin[m].bw.push_back(p.bandwidth_util);
+            pin[m].mem.push_back(p.memory);
+        }
+        pin[m].membase = P_.modules[m].memory_base;
+    }
+    long long packed_bytes = 0;
+    std::vector<int> range_err;
+    auto packed = mg::pack_options_device(pin, P_.gpu_count, P_.quota_levels, P_.memory_capacity,
+                                          device, &packed_bytes, &range_err);
     int off = 0;
     for (size_t m = 0; m < P_.modules.size(); ++m) {
-        try {
-            opts_[m] = candidate_options(P_, (int)m, P_.quota_levels);
-        } catch (const RangeError& e) {
-            opt_err_[m] = e.what();
-        }
+        if (range_err[m])
+            opt_err_[m] = P_.modules[m].id + ": d=1 outside profiled range";
+        else
+            for (const auto& r : packed[m]) opts_[m].push_back(Cand{r.d, r.u, r.base, r.B, r.fp});
         std::vector<mg::OptRow> rows;
         for (const auto& c : opts_[m])
             rows.push_back(mg::OptRow{c.d, c.units, c.base, c.B, c.fp,

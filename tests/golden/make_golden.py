@@ -160,8 +160,20 @@ def stime() -> None:
     dump("stime.json", out)
 
 
+
+
+def io_files() -> None:
+    """Reference JSON v1 files (io.hpp) and the plan solve() writes, for the N3 loaders."""
+    out = {}
+    for inst, extra in [("cfg3", []), ("cfg4", []), ("random:7:5:16", []),
+                        ("preset:ofasys:8:32", ["levels=32"])]:
+        d = ref(inst, "json", *extra)
+        out[inst] = {"args": [inst, "json", *extra], "files": d["files"]}
+    dump("io_files.json", out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["configs", "cfg5_stages", "random_sets", "presets", "variants",
-                             "stime"]
+                             "stime", "io_files"]
     for w in which:
         globals()[w]()
