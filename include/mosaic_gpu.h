@@ -135,6 +135,12 @@ int mosaic_gpu_exact_stage(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_
 int mosaic_gpu_feasible(mosaic_gpu_ctx* ctx, uint64_t mask, double tau,
                         mosaic_gpu_stage_result* out);
 
+/* T* = minimum stage_time over every allocation of the module set that is below `ub`
+ * (returns ub if none is): the quantity stage_eval's probes are decided against.  With
+ * restart = 0 it is exactly one device search (used for profiling). */
+int mosaic_gpu_stage_min(mosaic_gpu_ctx* ctx, uint64_t mask, double ub, int restart,
+                         double* tstar, mosaic_gpu_stage_result* stats);
+
 /* Plan = ordered stages (DeploymentPlan, core.hpp:100-104). */
 #define MOSAIC_GPU_MAX_STAGES 64
 typedef struct {

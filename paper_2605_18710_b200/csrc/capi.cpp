@@ -230,6 +230,18 @@ int mosaic_gpu_feasible(mosaic_gpu_ctx* ctx, uint64_t mask, double tau,
     });
 }
 
+int mosaic_gpu_stage_min(mosaic_gpu_ctx* ctx, uint64_t mask, double ub, int restart,
+                         double* tstar, mosaic_gpu_stage_result* stats) {
+    return guard([&] {
+        StageResult r;
+        *tstar = ctx->pl->stage_min(mask, ub, restart != 0, r.st);
+        r.status = OK;
+        r.stage_time = *tstar;
+        if (stats) fill_stage(r, stats);
+        return MOSAIC_OK;
+    });
+}
+
 int mosaic_gpu_plan_stage(mosaic_gpu_ctx* ctx, int stage, mosaic_gpu_stage_result* out) {
     return guard([&] {
         if (stage < 0 || stage >= (int)ctx->plan.stages.size())

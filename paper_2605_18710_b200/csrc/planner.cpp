@@ -335,6 +335,22 @@ StageResult Planner::stage_eval(uint64_t mask) {
     return res;
 }
 
+double Planner::stage_min(uint64_t mask, double ub, bool restart, mg::SearchStats& st) {
+    const auto mods = mask_modules(mask);
+    if ((int)mods.size() > mg::MAXK) throw Error(TOO_LARGE, "stage larger than 12 modules");
+    for (int m : mods) check_rows(m);
+    if (restart) return min_value(mods, ub, st);
+    mg::SearchReq q;
+    q.mode = MODE_MIN;
+    q.ub = ub;
+    q.level_module = mods;
+    mg::Spec S;
+    if (!mg::build_spec(M_, q, S)) return ub;
+    mg::SearchResult r = eng_->search(S, ub, 0.0, st);
+    if (r.overflow) throw Error(TOO_LARGE, "stage needs more than 128 GPU blocks");
+    return r.value;
+}
+
 StageResult Planner::feasible(uint64_t mask, double tau) {
     StageResult res;
     const auto mods = mask_modules(mask);

@@ -77,6 +77,8 @@ class Planner {
     StageResult exact_stage(uint64_t mask);
     StageResult feasible(uint64_t mask, double tau);
     PlanResult solve();
+    // T* of a module set below `ub` (one MIN search when restart == false)
+    double stage_min(uint64_t mask, double ub, bool restart, mg::SearchStats& st);
     PlanResult brute_force();
     // stage_time of explicit allocations (entries per allocation sorted by module)
     void stage_time(const std::vector<std::vector<Entry>>& allocs, std::vector<double>& st,

@@ -121,7 +121,7 @@ EXPORTS = [
     "mosaic_gpu_merge_records", "mosaic_gpu_launch_count", "mosaic_gpu_search_ms",
     "mosaic_gpu_reset_counters", "mosaic_gpu_synth_problem", "mosaic_gpu_free_problem",
     "mosaic_gpu_own_launches", "mosaic_gpu_ksearch_ms", "mosaic_gpu_ksearch_launches",
-    "mosaic_gpu_h2d_bytes", "mosaic_gpu_d2h_bytes", "mosaic_gpu_mark", "mosaic_gpu_marked_ms", "mosaic_gpu_alg_bytes",
+    "mosaic_gpu_h2d_bytes", "mosaic_gpu_d2h_bytes", "mosaic_gpu_mark", "mosaic_gpu_marked_ms", "mosaic_gpu_alg_bytes", "mosaic_gpu_stage_min",
 ]
 
 _lib = None
@@ -175,6 +175,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "mosaic_gpu_mark": (None, [vp, C.c_int]),
         "mosaic_gpu_marked_ms": (C.c_double, [vp]),
         "mosaic_gpu_alg_bytes": (C.c_int64, [vp]),
+        "mosaic_gpu_stage_min": (C.c_int, [vp, C.c_uint64, C.c_double, C.c_int,
+                                           P(C.c_double), P(StageResultC)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -414,6 +416,16 @@ class Planner:
         r = StageResultC()
         _raise(load_library().mosaic_gpu_exact_stage(self._ctx, self._mask(modules), C.byref(r)))
         return self._stage(r) if r.status == OK else None
+
+    def stage_min(self, modules: Sequence[int], ub: float = float("inf"),
+                  restart: bool = True) -> float:
+        """T* of the module set below ub (one device MIN search when restart=False)."""
+        t = C.c_double()
+        r = StageResultC()
+        _raise(load_library().mosaic_gpu_stage_min(self._ctx, self._mask(modules),
+                                                    min(ub, 1e300), int(restart), C.byref(t),
+                                                    C.byref(r)))
+        return t.value
 
     def feasibility_run(self, modules: Sequence[int], tau: float) -> Optional[StageEvalResult]:
         r = StageResultC()

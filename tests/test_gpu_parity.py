@@ -255,3 +255,26 @@ def test_evaluator_stage_time_bits():
         want = [hexf(r["t"]) for r in rows]
         assert got == want
         pl.close()
+
+
+def test_surface_without_d1_raises_range_error():
+    # candidate_options needs lookup(1, a) for the solo bandwidth (perf_model.hpp:420-422);
+    # a surface profiled only from d=2 makes the reference throw SurfaceRangeError
+    pts = [(d, a / 10, 1.0 / (d * a), 0.5, 1e9, 1.0) for d in (2, 4) for a in range(1, 11)]
+    pl = mosaic.Planner.from_surfaces([{"id": "m", "memory_base": 0.0, "points": pts}], [], 4)
+    with pytest.raises(mosaic.SurfaceRangeError):
+        pl.stage_eval([0])
+
+
+def test_stage_min_equals_stage_eval_time():
+    pl = planner("cfg5")
+    for mods in ([0, 1], [0, 1, 2], [1, 3, 5]):
+        r = pl.stage_eval(mods)
+        assert pl.stage_min(mods) == r.stage_time
+
+
+def test_evaluator_reproduces_searched_allocations():
+    # k_eval on every allocation the search returned must give back its stage time
+    pl = planner("cfg4")
+    res = pl.solve()
+    assert pl.stage_time(res.plan.stages) == res.plan.predicted_stage_times
