@@ -155,7 +155,7 @@ struct Walk {
     int ps_lvl;
     uint16_t *bsz, *bmk, *x, *lo, *hi;           // per level (loff-indexed)
     int *pu, *cu, *sa, *sb;                      // per block of the current / child level
-    double *pm, *psum, *pmb, *pP, *pmx, *cm, *cs, *cb;
+    double *pm, *psum, *pmb, *pP, *pmx, *cm, *cs, *cb, *cP, *cmx;
 };
 
 MG_HX size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -169,7 +169,7 @@ MG_HX WalkLayout walk_layout(int G, int k) {
         L.slots += c;
         L.nblk = c > L.nblk ? c : L.nblk;
     }
-    L.bytes = align16(sizeof(Walk)) + align16(8 * 8 * (size_t)L.nblk) +
+    L.bytes = align16(sizeof(Walk)) + align16(10 * 8 * (size_t)L.nblk) +
               align16(4 * 4 * (size_t)L.nblk) + align16(5 * 2 * (size_t)L.slots);
     return L;
 }
@@ -187,7 +187,9 @@ MG_HX void walk_carve(Walk& w, unsigned char* base, int G, int k) {
     w.cm = d + 5 * L.nblk;
     w.cs = d + 6 * L.nblk;
     w.cb = d + 7 * L.nblk;
-    p += align16(8 * 8 * (size_t)L.nblk);
+    w.cP = d + 8 * L.nblk;
+    w.cmx = d + 9 * L.nblk;
+    p += align16(10 * 8 * (size_t)L.nblk);
     int* i = reinterpret_cast<int*>(p);
     w.pu = i;
     w.cu = i + L.nblk;

@@ -237,14 +237,19 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
         parent_stats_warp(S, R, w, j);
         ps_lvl = j;
     }
-    // per block: approximate (fast filter) and exact rest contributions
+    // per block: approximate rest contribution (fast filter); the exact one is computed
+    // only once some option survives the filter (proof searches rarely need it)
     for (int b = lane; b < nb; b += 32) {
         const unsigned m = w.bmk[o0 + b];
         w.cm[b] = m ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] + (S.additive ? 0.0 : S.e3 * w.pP[b])
                     : NEG_INF;
-        w.cs[b] = contrib(S, R, w.opt, m);
     }
     __syncwarp();
+    bool rest_ready = !S.include_self;
+    if (rest_ready) {
+        for (int b = lane; b < nb; b += 32) w.cs[b] = contrib(S, R, w.opt, w.bmk[o0 + b]);
+        __syncwarp();
+    }
     const bool fm = S.mode == MODE_FIRST;
     const int n = S.lvl_n[j] < w.oe[j] ? S.lvl_n[j] : w.oe[j];
     const int off = S.lvl_off[j];
@@ -274,9 +279,10 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
         const double Ie = I * (1.0 - TIE_EPS);
         bool feas = false;
         double val = POS_INF;
+        bool pass = false;
         if (valid) {
             // fast filter (approximate contributions, sound 1e-12 slack)
-            bool pass = true;
+            pass = true;
             if (S.include_self) {
                 const double tx = fm ? S.theta * (1.0 + 1e-12) : Ie;
                 int lo = 0, hi = 0;
@@ -302,6 +308,13 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
                 }
                 pass = pass && lo <= dd && dd <= hi;
             }
+        }
+        if (!rest_ready && __any_sync(FULLW, valid && pass)) {
+            for (int b = lane; b < nb; b += 32) w.cs[b] = contrib(S, R, w.opt, w.bmk[o0 + b]);
+            __syncwarp();
+            rest_ready = true;
+        }
+        if (valid) {
             if (pass) {
                 if (fm) {
                     feas = 0.0 <= S.theta &&
@@ -667,6 +680,9 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                     w.cm[pos] = w.pm[b] + ff;
                     w.cs[pos] = w.psum[b] + bo;
                     w.cb[pos] = w.pmb[b] > ba ? w.pmb[b] : ba;
+                    w.cP[pos] = w.pP[b] * bo;
+                    const double bx = ba - S.e2 * bo;
+                    w.cmx[pos] = w.pmx[b] > bx ? w.pmx[b] : bx;
                     ++pos;
                 } else if (xb > 0) {
                     ++pos;
@@ -678,6 +694,8 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                     w.cm[pos] = w.pm[b];
                     w.cs[pos] = w.psum[b];
                     w.cb[pos] = w.pmb[b];
+                    w.cP[pos] = w.pP[b];
+                    w.cmx[pos] = w.pmx[b];
                 }
             }
             carry += __shfl_sync(FULLW, inc, 31);
@@ -724,8 +742,18 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
             w.ph[j] = 0;
             w.oc[j] = -1;
             w.oe[j] = (int16_t)S.lvl_n[j];
+            // the child stats are exactly the new level's parent stats (same summation
+            // order as block_stats): swap the buffers instead of recomputing them
+            int* ti = w.pu; w.pu = w.cu; w.cu = ti;
+            double* t;
+            t = w.pm; w.pm = w.cm; w.cm = t;
+            t = w.psum; w.psum = w.cs; w.cs = t;
+            t = w.pmb; w.pmb = w.cb; w.cb = t;
+            t = w.pP; w.pP = w.cP; w.cP = t;
+            t = w.pmx; w.pmx = w.cmx; w.cmx = t;
         }
         __syncwarp();
+        ps_lvl = j;
     }
     return 0;
 }
