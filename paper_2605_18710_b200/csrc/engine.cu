@@ -210,7 +210,7 @@ struct WarpHooks {
     __device__ void level(int j) { cur_level = j; }
 };
 
-constexpr int WPC = 2;  // walkers (warps) per CTA
+constexpr int WPC = 4;  // walkers (warps) per CTA
 
 constexpr size_t SMEM_SPEC = (sizeof(Spec) + 15) & ~size_t(15);
 

@@ -44,7 +44,7 @@ namespace mg {
 
 constexpr int MAXK = 12;   // modules per stage
 constexpr int MAXB = 128;  // blocks per level
-constexpr int MAXENV = 16; // envelope lines per level
+constexpr int MAXENV = 8;  // envelope lines per level
 constexpr int FB = MAXB;   // blocks carried by a frontier node
 constexpr double NEG_INF = -1.0e300;
 constexpr double POS_INF = 1.0e300;
