@@ -201,6 +201,18 @@ double Planner::min_value(const std::vector<int>& mods, double ub, mg::SearchSta
         q.mode = MODE_MIN;
         q.ub = ub;
         for (auto& [c, m] : cnt) q.level_module.push_back(m);
+        if (const char* e = std::getenv("MOSAIC_MIN_ORDER")) {  // experiments: "3,0,1,..."
+            std::vector<int> o;
+            for (const char* p = e; *p;) {
+                o.push_back(std::atoi(p));
+                while (*p && *p != ',') ++p;
+                if (*p == ',') ++p;
+            }
+            std::vector<int> a = o, b = mods;
+            std::sort(a.begin(), a.end());
+            std::sort(b.begin(), b.end());
+            if (a == b) q.level_module = o;
+        }
         mg::Spec S;
         if (!mg::build_spec(M_, q, S)) return ub;
         double ab = ub >= POS_INF ? POS_INF : ub * (1.0 - 1e-4);
@@ -344,6 +356,15 @@ double Planner::stage_min(uint64_t mask, double ub, bool restart, mg::SearchStat
     q.mode = MODE_MIN;
     q.ub = ub;
     q.level_module = mods;
+    if (const char* e = std::getenv("MOSAIC_MIN_ORDER")) {
+        std::vector<int> o;
+        for (const char* p = e; *p;) {
+            o.push_back(std::atoi(p));
+            while (*p && *p != ',') ++p;
+            if (*p == ',') ++p;
+        }
+        if (o.size() == mods.size()) q.level_module = o;
+    }
     mg::Spec S;
     if (!mg::build_spec(M_, q, S)) return ub;
     mg::SearchResult r = eng_->search(S, ub, 0.0, st);

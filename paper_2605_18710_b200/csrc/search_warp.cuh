@@ -712,7 +712,8 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
         __syncwarp();
         const double thr = h.thr(S);
         bool prune = false;
-        for (int l = j + 1; l < k && !prune; ++l) {
+        // (when only the closed-form last level remains, its batch screen subsumes this)
+        for (int l = j + 1; l < k && !prune && !(j + 1 == k - 1 && S.nonneg); ++l) {
             const int n = S.lvl_n[l], off = S.lvl_off[l];
             bool ok = false;
             for (int o = 0; o < n && !ok; ++o) {
