@@ -147,6 +147,9 @@ struct Walk {
     uint16_t opt[MAXK];
     int16_t oc[MAXK];
     int16_t oe[MAXK];  // option range end per level (exclusive)
+    uint32_t vmask[MAXK];  // option pre-screen: viable options in [vbase, vbase + 32)
+    int16_t vbase[MAXK];   //   (-1: not screened at this node yet)
+    uint8_t vstop[MAXK];   //   no option beyond the window can pass
     uint8_t ph[MAXK];
     uint16_t nb[MAXK + 1];
     int used[MAXK + 1];

@@ -387,6 +387,80 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
     return false;
 }
 
+// Lane-parallel pre-screen of the options [start, start + 32) at a non-last level: each
+// lane runs opt_test, the capacity test and the full admissible-interval test of its own
+// option over all blocks (no warp reductions).  Only options whose intervals can reach d
+// survive; they are then processed one by one with the block-parallel code.  The screen
+// uses the current threshold, which only tightens later, so it never drops a leaf.
+__device__ __forceinline__ void screen_options(const Spec& S, const Rows& R, Walk& w, int j,
+                                               int start, int n, double thr) {
+    const int lane = lane_id();
+    const int o = start + lane;
+    const int o0 = w.loff[j], nb = w.nb[j];
+    const int off = S.lvl_off[j];
+    const int t = o < n ? opt_test(S, R, off + o, thr) : 2;
+    const unsigned brk = __ballot_sync(FULLW, t == 2);
+    const int first_brk = brk ? __ffs(brk) - 1 : 32;
+    bool viable = t == 0 && lane < first_brk;
+    if (viable && j == S.shard_level && S.shard_world > 1 &&
+        shard_hash(w.opt, j, o) % (unsigned)S.shard_world != (unsigned)S.shard_rank)
+        viable = false;
+    if (viable) {
+        const int r = off + o;
+        const int dd = R.d[r], uu = R.u[r];
+        const double ff = R.fp[r], bo = R.B[r], ba = R.base[r];
+        if (w.used[j] + dd * uu + S.suffix_min[j + 1] > S.G * S.L) {
+            viable = false;
+        } else {
+            int lo = 0, hi = 0;
+            for (int b = 0; b < nb && viable; ++b) {
+                const int s = w.bsz[o0 + b];
+                const bool el = w.pu[b] + uu <= S.L && !(w.pm[b] + ff > S.cap_slack);
+                bool tok = el, rok = true;
+                if (S.nonneg) {
+                    if (el) {
+                        double lbt;
+                        if (S.include_self) {
+                            const double mb = w.pmb[b] > ba ? w.pmb[b] : ba;
+                            lbt = mb + S.e1 + S.e2 * (w.psum[b] + bo) +
+                                  envelope(S, j + 1, w.pP[b] * bo);
+                        } else {
+                            const double bx = ba - S.e2 * bo;
+                            const double mx = w.pmx[b] > bx ? w.pmx[b] : bx;
+                            lbt = mx + S.e1 + S.e2 * (w.psum[b] + bo) + envelope(S, j + 1, 0.0);
+                        }
+                        tok = !(lbt > thr);
+                    }
+                    if (w.bmk[o0 + b]) {
+                        const double lbr = S.include_self
+                                               ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] +
+                                                     envelope(S, j + 1, w.pP[b])
+                                               : w.pmx[b] + S.e1 + S.e2 * w.psum[b] +
+                                                     envelope(S, j + 1, 0.0);
+                        rok = !(lbr > thr);
+                    }
+                }
+                if (rok) {
+                    if (tok) hi += s;
+                } else if (tok) {
+                    lo += s;
+                    hi += s;
+                } else {
+                    viable = false;
+                }
+            }
+            viable = viable && lo <= dd && dd <= hi;
+        }
+    }
+    const unsigned m = __ballot_sync(FULLW, viable);
+    if (lane == 0) {
+        w.vmask[j] = m;
+        w.vbase[j] = (int16_t)start;
+        w.vstop[j] = first_brk < 32 ? 1 : 0;
+    }
+    __syncwarp();
+}
+
 template <class H>
 __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
     const int lane = lane_id();
@@ -426,17 +500,37 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
             const int n = S.lvl_n[j] < w.oe[j] ? S.lvl_n[j] : w.oe[j], off = S.lvl_off[j];
             int o = w.oc[j] + 1;
             bool got = false;
-            for (; o < n; ++o) {
-                const int r = off + o;
-                const int t = opt_test(S, R, r, thr);
-                if (t == 2) break;
-                if (t == 1) continue;
-                if (j == S.shard_level && S.shard_world > 1 &&
-                    shard_hash(w.opt, j, o) % (unsigned)S.shard_world != (unsigned)S.shard_rank)
-                    continue;
-                if (w.used[j] + R.d[r] * R.u[r] + S.suffix_min[j + 1] > GL) continue;
-                got = true;
-                break;
+            if (j < k - 1) {
+                if (ps_lvl != j) {
+                    parent_stats_warp(S, R, w, j);
+                    ps_lvl = j;
+                }
+                while (o < n) {
+                    if (w.vbase[j] < 0 || o < w.vbase[j] || o >= w.vbase[j] + 32)
+                        screen_options(S, R, w, j, o, n, thr);
+                    const unsigned mk = w.vmask[j] >> (o - w.vbase[j]);
+                    if (mk) {
+                        o += __ffs(mk) - 1;
+                        got = true;
+                        break;
+                    }
+                    if (w.vstop[j]) break;
+                    o = w.vbase[j] + 32;
+                }
+            } else {
+                for (; o < n; ++o) {
+                    const int r = off + o;
+                    const int t = opt_test(S, R, r, thr);
+                    if (t == 2) break;
+                    if (t == 1) continue;
+                    if (j == S.shard_level && S.shard_world > 1 &&
+                        shard_hash(w.opt, j, o) % (unsigned)S.shard_world !=
+                            (unsigned)S.shard_rank)
+                        continue;
+                    if (w.used[j] + R.d[r] * R.u[r] + S.suffix_min[j + 1] > GL) continue;
+                    got = true;
+                    break;
+                }
             }
             __syncwarp();
             if (!got) {
@@ -743,6 +837,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
             w.ph[j] = 0;
             w.oc[j] = -1;
             w.oe[j] = (int16_t)S.lvl_n[j];
+            w.vbase[j] = -1;
             // the child stats are exactly the new level's parent stats (same summation
             // order as block_stats): swap the buffers instead of recomputing them
             int* ti = w.pu; w.pu = w.cu; w.cu = ti;
@@ -781,6 +876,7 @@ __device__ __forceinline__ void load_cont_warp(const Cont& c, Walk& w) {
         w.ph[dep] = (uint8_t)c.ph;
         w.oc[dep] = c.oc;
         w.oe[dep] = c.oe;
+        w.vbase[dep] = -1;
         if (c.ph) w.opt[dep] = (uint16_t)c.oc;
         for (int l = dep - 1; l >= 0; --l) {
             const int oc1 = w.loff[l + 1], ol = w.loff[l];
