@@ -45,6 +45,7 @@ struct Ctl {
     unsigned long long q_cap;
     alignas(128) unsigned long long outstanding;  // queued + in-flight cursors
     alignas(128) unsigned int idle;
+    unsigned int walkers;  // resident walkers of this launch
     alignas(128) int lock;  // FIRST: best hit, published under a seqlock
     int ver;
     int has_hit;            // FIRST: a hit is published; MIN: an argmin leaf is stored
@@ -94,7 +95,8 @@ struct WarpHooks {
                     if (idle) {
                         unsigned long long qn = *(volatile unsigned long long*)&ctl->q_tail -
                                                 *(volatile unsigned long long*)&ctl->q_head;
-                        if (qn == 0) code = 3;  // queue drained and walkers waiting
+                        if (qn == 0)  // queue drained and walkers waiting
+                            code = idle * 4 > ctl->walkers * 3 ? 4 : 3;
                     }
                 }
             }
@@ -248,6 +250,7 @@ __global__ void __launch_bounds__(32 * WPC) k_search(const Spec* Sg, Rows R, Con
         if (lane == 0) {
             bool idle = false;
             unsigned backoff = 128;
+            const unsigned backoff_cap = S.backoff_cap_ns;
             while (true) {
                 if (*(volatile int*)&ctl->abort) break;
                 unsigned long long h = *(volatile unsigned long long*)&ctl->q_head;
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(32 * WPC) k_search(const Spec* Sg, Rows R, Con
                     idle = true;
                 }
                 __nanosleep(backoff);
-                backoff = backoff < 8192 ? backoff * 2 : 8192;
+                backoff = backoff < backoff_cap ? backoff * 2 : backoff_cap;
             }
             if (idle) atomicSub(&ctl->idle, 1u);
             if (ticket >= 0) {
@@ -388,6 +391,7 @@ Engine::Engine(int device) : device_(device) {
     trace_ = std::getenv("MOSAIC_TRACE") != nullptr;
     if (const char* e = std::getenv("MOSAIC_DON_DEPTH")) don_depth_ = std::atoi(e);
     if (const char* e = std::getenv("MOSAIC_DON_PERIOD")) don_period_ = std::atoi(e);
+    if (const char* e = std::getenv("MOSAIC_BACKOFF_NS")) backoff_cap_ = std::atoi(e);
     CK(cudaSetDevice(device));
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -503,10 +507,21 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     *hs = S;
     hs->shard_rank = rank_;
     hs->shard_world = world_;
+    if (const char* e = std::getenv("MOSAIC_SHARD_SIM")) {  // "r/w": measure one rank's share
+        int r = 0, wd = 1;
+        if (std::sscanf(e, "%d/%d", &r, &wd) == 2 && wd >= 1 && r >= 0 && r < wd) {
+            hs->shard_rank = r;
+            hs->shard_world = wd;
+        }
+    }
     hs->shard_level = S.k >= 2 ? 1 : 0;  // (o_0, o_1) pairs: fine enough to balance 8 ranks
     // donation policy: hand over only shallow levels, when the queue has run dry
     hs->don_max_level = S.k >= 6 ? S.k - 1 - don_depth_ : S.k - 3;
+    // Deeper hand-overs in the tail (most walkers idle) measured slower on cfg5 (cursor
+    // rebuild + traffic outweigh the extra parallelism): kept at the normal depth.
+    hs->don_max_level_tail = hs->don_max_level;
     hs->don_period = don_period_;
+    hs->backoff_cap_ns = backoff_cap_;
     std::memset(hc, 0, sizeof(Ctl));
     union {
         double d;
@@ -557,6 +572,9 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
         grid_ = std::max(1, per_sm) * sms;  // all resident: spin-waiting needs it
         grid_smem_ = smem;
     }
+    hc->walkers = (unsigned)(grid_ * WPC);
+    CK(cudaMemcpyAsync(&((Ctl*)d_ctl_)->walkers, &hc->walkers, sizeof(unsigned),
+                       cudaMemcpyHostToDevice, s));
     CK(cudaEventRecord((cudaEvent_t)evk0_, s));
     k_search<<<(unsigned)grid_, 32 * WPC, smem, s>>>((const Spec*)d_spec_, R, Q, d_ready_,
                                                      (Ctl*)d_ctl_, (HitPath*)d_best_,

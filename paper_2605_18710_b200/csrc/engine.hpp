@@ -103,6 +103,7 @@ class Engine {
     bool trace_ = false;
     int don_depth_ = 3;    // donate levels <= k-1-don_depth (measured best on cfg5)
     int don_period_ = 32;  // power of two
+    int backoff_cap_ = 2048;  // ns, idle walkers polling back-off cap (measured)
     long long front_cap_ = 0;
     void* h_pin_ = nullptr;
     long long launches_ = 0;

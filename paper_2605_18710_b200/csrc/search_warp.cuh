@@ -476,12 +476,14 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
             h.level(j);
             const int ab = h.abort();
             if (ab == 2) return 2;
-            if (ab == 3) {
-                // only shallow work is worth a hand-over (cursor traffic beats tiny subtrees)
+            if (ab == 3 || ab == 4) {
+                // only shallow work is worth a hand-over (cursor traffic beats tiny
+                // subtrees) — except in the tail, when most walkers are starving
+                const int maxl = ab == 4 ? S.don_max_level_tail : S.don_max_level;
                 while (floor_lvl < j && !level_has_rest_warp(S, w, floor_lvl)) ++floor_lvl;
-                if (floor_lvl < j && floor_lvl <= S.don_max_level) {
+                if (floor_lvl < j && floor_lvl <= maxl) {
                     if (h.donate(w, floor_lvl, 1, -1)) ++floor_lvl;
-                } else if (floor_lvl == j && j <= S.don_max_level) {
+                } else if (floor_lvl == j && j <= maxl) {
                     // all that is left is this level's option range: hand over its upper half
                     const int a = w.oc[j] + 1, e = w.oe[j];
                     if (e - a >= 2) {
