@@ -392,6 +392,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* e = std::getenv("MOSAIC_DON_DEPTH")) don_depth_ = std::atoi(e);
     if (const char* e = std::getenv("MOSAIC_DON_PERIOD")) don_period_ = std::atoi(e);
     if (const char* e = std::getenv("MOSAIC_BACKOFF_NS")) backoff_cap_ = std::atoi(e);
+    if (const char* e = std::getenv("MOSAIC_SMALL_TREE")) small_tree_ = std::atof(e);
     CK(cudaSetDevice(device));
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -485,6 +486,8 @@ void Engine::ensure_front(long long n) {
     CK(cudaMalloc(&d_front_[0], cap * sizeof(Cont)));
     cudaFree(d_ready_);
     CK(cudaMalloc(&d_ready_, cap * sizeof(int)));
+    CK(cudaMemset(d_ready_, 0, cap * sizeof(int)));
+    ticket_base_ = 0;
     if (!d_best_) CK(cudaMalloc(&d_best_, sizeof(HitPath)));
     front_cap_ = cap;
 }
@@ -516,7 +519,7 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     }
     hs->shard_level = S.k >= 2 ? 1 : 0;  // (o_0, o_1) pairs: fine enough to balance 8 ranks
     // donation policy: hand over only shallow levels, when the queue has run dry
-    hs->don_max_level = S.k >= 6 ? S.k - 1 - don_depth_ : S.k - 3;
+    hs->don_max_level = S.k >= 6 ? S.k - 1 - don_depth_ : (S.k >= 3 ? S.k - 3 : 0);
     // Deeper hand-overs in the tail (most walkers idle) measured slower on cfg5 (cursor
     // rebuild + traffic outweigh the extra parallelism): kept at the normal depth.
     hs->don_max_level_tail = hs->don_max_level;
@@ -530,8 +533,11 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     cv.d = ub;
     hc->inc = cv.u;
     hc->abort_below = abort_below;
-    hc->q_head = 0;
-    hc->q_tail = 1;
+    // tickets keep counting across searches, so slots never need clearing: a stale
+    // ready value belongs to an older (smaller) ticket and can never match
+    const unsigned long long t0 = ticket_base_;
+    hc->q_head = t0;
+    hc->q_tail = t0 + 1;
     hc->q_cap = (unsigned long long)cap;
     hc->outstanding = 1;
     std::memset(hr, 0, sizeof(Cont));
@@ -554,9 +560,10 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     }
     CK(cudaMemcpyAsync(d_spec_, hs, sizeof(Spec), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(d_ctl_, hc, sizeof(Ctl), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(Q, hr, sizeof(Cont), cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(d_ready_, 0, cap * sizeof(int), s));
-    CK(cudaMemcpyAsync(d_ready_, hone, sizeof(int), cudaMemcpyHostToDevice, s));
+    const size_t slot0 = (size_t)(t0 % (unsigned long long)cap);
+    *hone = (int)(t0 + 1);
+    CK(cudaMemcpyAsync(Q + slot0, hr, sizeof(Cont), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_ready_ + slot0, hone, sizeof(int), cudaMemcpyHostToDevice, s));
     h2d_ += sizeof(Spec) + sizeof(Ctl) + sizeof(Cont) + sizeof(int);
     const size_t smem = smem_bytes(S.G, S.k);
     if (smem != grid_smem_) {
@@ -572,11 +579,16 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
         grid_ = std::max(1, per_sm) * sms;  // all resident: spin-waiting needs it
         grid_smem_ = smem;
     }
-    hc->walkers = (unsigned)(grid_ * WPC);
+    CK(cudaEventRecord((cudaEvent_t)evk0_, s));
+    // small trees (few option tuples) do not need the whole GPU: a handful of resident
+    // CTAs finishes them without spinning up thousands of idle walkers
+    double tuples = 1.0;
+    for (int l = 0; l < S.k; ++l) tuples *= (double)(S.lvl_n[l] > 0 ? S.lvl_n[l] : 1);
+    const long long grid = (tuples * S.G <= small_tree_) ? std::min<long long>(grid_, 8) : grid_;
+    hc->walkers = (unsigned)(grid * WPC);
     CK(cudaMemcpyAsync(&((Ctl*)d_ctl_)->walkers, &hc->walkers, sizeof(unsigned),
                        cudaMemcpyHostToDevice, s));
-    CK(cudaEventRecord((cudaEvent_t)evk0_, s));
-    k_search<<<(unsigned)grid_, 32 * WPC, smem, s>>>((const Spec*)d_spec_, R, Q, d_ready_,
+    k_search<<<(unsigned)grid, 32 * WPC, smem, s>>>((const Spec*)d_spec_, R, Q, d_ready_,
                                                      (Ctl*)d_ctl_, (HitPath*)d_best_,
                                                      (Leaf*)d_leaf_);
     CK(cudaEventRecord((cudaEvent_t)evk1_, s));
@@ -587,6 +599,7 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     d2h_ += sizeof(Ctl);
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
+    ticket_base_ = hc->q_tail + 1;
     if (hc->has_hit && !hc->overflow) {
         CK(cudaMemcpyAsync(hl, d_leaf_, sizeof(Leaf), cudaMemcpyDeviceToHost, s));
         d2h_ += sizeof(Leaf);

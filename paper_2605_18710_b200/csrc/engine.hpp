@@ -104,6 +104,8 @@ class Engine {
     int don_depth_ = 3;    // donate levels <= k-1-don_depth (measured best on cfg5)
     int don_period_ = 32;  // power of two
     int backoff_cap_ = 2048;  // ns, idle walkers polling back-off cap (measured)
+    double small_tree_ = 2e5;  // option tuples x G below which 8 CTAs run the search
+    unsigned long long ticket_base_ = 0;
     long long front_cap_ = 0;
     void* h_pin_ = nullptr;
     long long launches_ = 0;
