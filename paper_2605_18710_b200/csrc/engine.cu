@@ -69,6 +69,7 @@ struct WarpHooks {
     const Walk* w;
     int cur_level;
     int don_period;
+    long long deep_after;
 
     __device__ bool hit_precedes() {  // lane 0 only
         int v0 = *(volatile int*)&ctl->ver;
@@ -83,11 +84,14 @@ struct WarpHooks {
     // 3 idle walkers are waiting: donate shallow work
     __device__ int abort() {
         ++steps;
+        // global control state is read only every don_period steps: a per-step L2 round
+        // trip (broadcast from lane 0) was the single hottest stall of the walker loop
+        if ((steps & (unsigned)(don_period - 1)) != 0) return 0;
         int code = 0;
         if (lane_id() == 0) {
             if (*(volatile int*)&ctl->abort) {
                 code = 2;
-            } else if ((steps & (unsigned)(don_period - 1)) == 0) {
+            } else {
                 if (mode == MODE_FIRST && *(volatile int*)&ctl->has_hit && hit_precedes()) {
                     code = 2;
                 } else {
@@ -96,7 +100,9 @@ struct WarpHooks {
                         unsigned long long qn = *(volatile unsigned long long*)&ctl->q_tail -
                                                 *(volatile unsigned long long*)&ctl->q_head;
                         if (qn == 0)  // queue drained and walkers waiting
-                            code = idle * 4 > ctl->walkers * 3 ? 4 : 3;
+                            // a walker that has been on its piece for long holds a big
+                            // subtree: let it split deeper levels too
+                            code = steps > deep_after ? 4 : 3;
                     }
                 }
             }
@@ -169,9 +175,11 @@ struct WarpHooks {
         double t = inc_cache >= POS_INF ? POS_INF : inc_cache * (1.0 - TIE_EPS);
         return t < S.thp ? t : S.thp;
     }
-    __device__ double incumbent() {
-        double I = bcast_inc();
-        inc_cache = I < inc_cache ? I : inc_cache;
+    __device__ double incumbent() {  // refreshed every 16 calls, like thr()
+        if ((refresh++ & 15) == 0) {
+            double I = bcast_inc();
+            inc_cache = I < inc_cache ? I : inc_cache;
+        }
         return inc_cache;
     }
     __device__ void improve(double v) {
@@ -281,7 +289,7 @@ __global__ void __launch_bounds__(32 * WPC) k_search(const Spec* Sg, Rows R, Con
         if (ticket < 0) break;
         const long long slot = (long long)((unsigned long long)ticket % ctl->q_cap);
         __threadfence();
-        load_cont_warp(Q[slot], w);
+        load_cont_warp(Q[slot], w, S.mode == MODE_FIRST);
         WarpHooks h;
         h.ctl = ctl;
         h.mode = S.mode;
@@ -296,6 +304,7 @@ __global__ void __launch_bounds__(32 * WPC) k_search(const Spec* Sg, Rows R, Con
         h.w = &w;
         h.cur_level = 0;
         h.don_period = S.don_period;
+        h.deep_after = S.deep_after;
         h.inc_cache = POS_INF;
         h.inc_cache = h.bcast_inc();
         const int d0 = Q[slot].depth;
@@ -393,6 +402,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* e = std::getenv("MOSAIC_DON_PERIOD")) don_period_ = std::atoi(e);
     if (const char* e = std::getenv("MOSAIC_BACKOFF_NS")) backoff_cap_ = std::atoi(e);
     if (const char* e = std::getenv("MOSAIC_SMALL_TREE")) small_tree_ = std::atof(e);
+    if (const char* e = std::getenv("MOSAIC_DEEP_AFTER")) deep_after_ = std::atoll(e);
     CK(cudaSetDevice(device));
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -520,9 +530,9 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     hs->shard_level = S.k >= 2 ? 1 : 0;  // (o_0, o_1) pairs: fine enough to balance 8 ranks
     // donation policy: hand over only shallow levels, when the queue has run dry
     hs->don_max_level = S.k >= 6 ? S.k - 1 - don_depth_ : (S.k >= 3 ? S.k - 3 : 0);
-    // Deeper hand-overs in the tail (most walkers idle) measured slower on cfg5 (cursor
-    // rebuild + traffic outweigh the extra parallelism): kept at the normal depth.
-    hs->don_max_level_tail = hs->don_max_level;
+    // long-running pieces may also hand over levels <= k-3 (see WarpHooks::abort)
+    hs->don_max_level_tail = S.k - 3 > hs->don_max_level ? S.k - 3 : hs->don_max_level;
+    hs->deep_after = deep_after_;
     hs->don_period = don_period_;
     hs->backoff_cap_ns = backoff_cap_;
     std::memset(hc, 0, sizeof(Ctl));

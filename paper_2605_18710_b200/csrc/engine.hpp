@@ -102,10 +102,11 @@ class Engine {
     size_t grid_smem_ = 0, smem_attr_ = 0;
     bool trace_ = false;
     int don_depth_ = 3;    // donate levels <= k-1-don_depth (measured best on cfg5)
-    int don_period_ = 32;  // power of two
+    int don_period_ = 1;   // power of two (measured: hand-over latency matters most)
     int backoff_cap_ = 2048;  // ns, idle walkers polling back-off cap (measured)
     double small_tree_ = 2e5;  // option tuples x G below which 8 CTAs run the search
     unsigned long long ticket_base_ = 0;
+    long long deep_after_ = 4096;  // steps on one piece before deeper hand-overs are allowed
     long long front_cap_ = 0;
     void* h_pin_ = nullptr;
     long long launches_ = 0;

@@ -68,7 +68,8 @@ struct Spec {
     int shard_rank, shard_world;   // multi-GPU: this rank takes the option prefixes
     int shard_level;               //   (o_0..o_L) with shard_hash % world == rank, L = shard_level
     int don_max_level;             // work donation: only levels <= this are handed over
-    int don_max_level_tail;        //   ... or <= this in the tail (most walkers idle)
+    int don_max_level_tail;        //   ... or <= this once a walker ran deep_after steps on a piece
+    long long deep_after;
     int don_period;                // check for idle walkers every don_period option steps (2^n)
     int backoff_cap_ns;            // idle walkers poll the queue with back-off up to this
     int env_n[MAXK + 1];           // product-term envelope over unplaced levels >= j

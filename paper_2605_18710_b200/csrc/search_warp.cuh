@@ -857,7 +857,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
 }
 
 // ---- cursor load / store by a whole warp ----
-__device__ __forceinline__ void load_cont_warp(const Cont& c, Walk& w) {
+__device__ __forceinline__ void load_cont_warp(const Cont& c, Walk& w, bool ancestors = true) {
     const int lane = lane_id();
     const int dep = c.depth;
     const int o = w.loff[dep];
@@ -880,7 +880,8 @@ __device__ __forceinline__ void load_cont_warp(const Cont& c, Walk& w) {
         w.oe[dep] = c.oe;
         w.vbase[dep] = -1;
         if (c.ph) w.opt[dep] = (uint16_t)c.oc;
-        for (int l = dep - 1; l >= 0; --l) {
+        // only FIRST needs them (hit paths compare every level); MIN skips the rebuild
+        for (int l = ancestors ? dep - 1 : -1; l >= 0; --l) {
             const int oc1 = w.loff[l + 1], ol = w.loff[l];
             const unsigned bit = 1u << l;
             int nbl = 0;
