@@ -141,6 +141,14 @@ int mosaic_gpu_feasible(mosaic_gpu_ctx* ctx, uint64_t mask, double tau,
 int mosaic_gpu_stage_min(mosaic_gpu_ctx* ctx, uint64_t mask, double ub, int restart,
                          double* tstar, mosaic_gpu_stage_result* stats);
 
+/* validate_plan (core.hpp:281-351) with the footprint oracle: stage s owns entries
+ * [stage_off[s], stage_off[s+1]).  Writes the ValidationCode name ("Ok", "ModuleMissing",
+ * "ModuleDuplicated", "DependencyViolated", "SmOvercommit", "MemoryOvercommit",
+ * "EmptyStage") into code_out; the message is in mosaic_gpu_last_error(). */
+int mosaic_gpu_validate_plan(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* entries,
+                             const int32_t* gpus, const int64_t* stage_off, int64_t n_stages,
+                             char* code_out, size_t code_cap);
+
 /* Plan = ordered stages (DeploymentPlan, core.hpp:100-104). */
 #define MOSAIC_GPU_MAX_STAGES 64
 typedef struct {
@@ -208,6 +216,38 @@ double mosaic_gpu_marked_ms(mosaic_gpu_ctx* ctx);
  * in C++ so the GPU box needs no reference): fills a problem for a named BASELINE
  * config "cfg1".."cfg5", "random:SEED:N:G" or "preset:NAME:COUNT:G".  The returned
  * problem owns its storage until mosaic_gpu_free_problem. */
+/* ---- N2: input generation on the device (profiler.hpp) ---- */
+/* ModuleWorkload (profiler.hpp:26-40); id is informational. */
+typedef struct {
+    const char* id;
+    double flops_per_iter, bytes_per_iter, gradient_bytes, sm_efficiency_knee,
+        memory_act_base, memory_per_quota, fixed_overhead, dp_penalty;
+} mosaic_gpu_workload;
+
+/* ClusterSpec (core.hpp:52-59). */
+typedef struct {
+    int32_t gpu_count;
+    double memory_capacity, peak_compute, peak_bandwidth, interconnect_alpha,
+        interconnect_beta;
+} mosaic_gpu_cluster;
+
+/* generate_surface (profiler.hpp:65-101) for n workloads on `device`:
+ * out[(w * nd + di) * na + ai] = evaluate_workload(w, cluster, d_set[di], a_set[ai]) with
+ * ProfilerConfig.demand_scale.  out holds n * nd * na points.  d_set = NULL uses
+ * default_dp_degrees(gpu_count), a_set = NULL default_quota_grid() (profiler.hpp:44-54);
+ * *nd_out / *na_out return the grid shape (call with out = NULL to size the buffer). */
+int mosaic_gpu_generate_surfaces(const mosaic_gpu_workload* workloads, int32_t n,
+                                 const mosaic_gpu_cluster* cluster, const int32_t* d_set,
+                                 int32_t nd, const double* a_set, int32_t na,
+                                 double demand_scale, int device, mosaic_gpu_point* out,
+                                 int32_t* nd_out, int32_t* na_out);
+
+/* The workloads and cluster a synthetic spec is generated from (make_workload /
+ * make_preset / random_instance, profiler.hpp:185-338).  Writes up to cap workloads
+ * (ids NULL) and *n = their count. */
+int mosaic_gpu_synth_workloads(const char* spec, mosaic_gpu_workload* out, int32_t cap,
+                               int32_t* n, mosaic_gpu_cluster* cluster);
+
 int mosaic_gpu_synth_problem(const char* spec, int quota_levels, mosaic_gpu_problem** out);
 void mosaic_gpu_free_problem(mosaic_gpu_problem* p);
 

@@ -399,6 +399,46 @@ int main(int argc, char** argv) {
             j["plan"] = to_json(r.plan, in.graph);
             std::printf("\"files\":%s", j.dump().c_str());
 #endif
+        } else if (op == "validate") {
+            // PLAN: stage|stage|...; stage: m:d:u:g0.g1;m:d:u:...  (validate_plan, core.hpp:281)
+            DeploymentPlan plan;
+            std::string spec = pos.at(0);
+            size_t a = 0;
+            while (a <= spec.size()) {
+                size_t b = spec.find('|', a);
+                if (b == std::string::npos) b = spec.size();
+                std::string st = spec.substr(a, b - a);
+                StageAllocation al;
+                size_t p = 0;
+                while (p < st.size()) {
+                    size_t q = st.find(';', p);
+                    if (q == std::string::npos) q = st.size();
+                    std::string ent = st.substr(p, q - p);
+                    StageAllocation::Entry e;
+                    int m, d, u;
+                    char gl[8192] = {0};
+                    std::sscanf(ent.c_str(), "%d:%d:%d:%8191s", &m, &d, &u, gl);
+                    e.module = m;
+                    e.option = {d, u, L};
+                    std::string g = gl;
+                    size_t x = 0;
+                    while (x < g.size()) {
+                        size_t y = g.find('.', x);
+                        if (y == std::string::npos) y = g.size();
+                        e.gpus.push_back(std::atoi(g.substr(x, y - x).c_str()));
+                        x = y + 1;
+                    }
+                    al.entries.push_back(e);
+                    p = q + 1;
+                }
+                plan.stages.push_back(al);
+                a = b + 1;
+            }
+            FootprintOracle fo{&in.ctx, [](const void* c, int m, const DeploymentOption& o) {
+                                   return static_cast<const PerfContext*>(c)->footprint(m, o);
+                               }};
+            auto err = validate_plan(plan, in.graph, in.cluster, fo);
+            std::printf("\"code\":\"%s\"", err ? to_string(err->code) : "Ok");
         } else if (op == "partitions") {
             auto parts = enumerate_partitions(in.graph);
             std::printf("\"count\":%zu", parts.size());

@@ -1,10 +1,12 @@
 // capi.cpp — extern "C" boundary (include/mosaic_gpu.h).  No exception crosses it.
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "../../include/mosaic_gpu.h"
+#include "pack.hpp"
 #include "planner.hpp"
 
 using namespace mosaic_b200;
@@ -242,6 +244,27 @@ int mosaic_gpu_stage_min(mosaic_gpu_ctx* ctx, uint64_t mask, double ub, int rest
     });
 }
 
+int mosaic_gpu_validate_plan(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* entries,
+                             const int32_t* gpus, const int64_t* stage_off, int64_t n_stages,
+                             char* code_out, size_t code_cap) {
+    return guard([&] {
+        std::vector<std::vector<Entry>> st(n_stages);
+        for (int64_t s = 0; s < n_stages; ++s)
+            for (int64_t e = stage_off[s]; e < stage_off[s + 1]; ++e) {
+                const auto& E = entries[e];
+                Entry x{E.module, E.dp_degree, E.quota_units, {}};
+                x.gpus.assign(gpus + E.gpu_off, gpus + E.gpu_off + E.n_gpus);
+                st[s].push_back(std::move(x));
+            }
+        std::string msg;
+        std::string code = ctx->pl->validate_plan(st, &msg);
+        if (code.empty()) code = "Ok";
+        std::snprintf(code_out, code_cap, "%s", code.c_str());
+        g_err = msg;
+        return MOSAIC_OK;
+    });
+}
+
 int mosaic_gpu_plan_stage(mosaic_gpu_ctx* ctx, int stage, mosaic_gpu_stage_result* out) {
     return guard([&] {
         if (stage < 0 || stage >= (int)ctx->plan.stages.size())
@@ -361,6 +384,61 @@ double mosaic_gpu_marked_ms(mosaic_gpu_ctx* ctx) {
     } catch (...) {
         return -1.0;
     }
+}
+
+int mosaic_gpu_generate_surfaces(const mosaic_gpu_workload* workloads, int32_t n,
+                                 const mosaic_gpu_cluster* cluster, const int32_t* d_set,
+                                 int32_t nd, const double* a_set, int32_t na,
+                                 double demand_scale, int device, mosaic_gpu_point* out,
+                                 int32_t* nd_out, int32_t* na_out) {
+    return guard([&] {
+        std::vector<int> ds;
+        std::vector<double> as;
+        if (d_set) {
+            ds.assign(d_set, d_set + nd);
+        } else {
+            for (int d = 1; d <= cluster->gpu_count; d *= 2) ds.push_back(d);  // :44-48
+        }
+        if (a_set) {
+            as.assign(a_set, a_set + na);
+        } else {
+            for (int i = 1; i <= 10; ++i) as.push_back(i / 10.0);  // :50-54
+        }
+        if (nd_out) *nd_out = (int32_t)ds.size();
+        if (na_out) *na_out = (int32_t)as.size();
+        if (!out) return MOSAIC_OK;
+        std::vector<mg::GenWorkload> ws(n);
+        for (int i = 0; i < n; ++i) {
+            const auto& w = workloads[i];
+            ws[i] = mg::GenWorkload{w.flops_per_iter,    w.bytes_per_iter,   w.gradient_bytes,
+                                    w.sm_efficiency_knee, w.memory_act_base, w.memory_per_quota,
+                                    w.fixed_overhead,     w.dp_penalty};
+        }
+        mg::GenCluster c{cluster->peak_compute, cluster->peak_bandwidth,
+                         cluster->interconnect_alpha, cluster->interconnect_beta};
+        auto pts = mg::generate_surfaces_device(ws, c, ds, as, demand_scale, device);
+        for (size_t i = 0; i < pts.size(); ++i)
+            out[i] = mosaic_gpu_point{pts[i].d, pts[i].a, pts[i].latency, pts[i].bandwidth_util,
+                                      pts[i].memory, pts[i].sm_active};
+        return MOSAIC_OK;
+    });
+}
+
+int mosaic_gpu_synth_workloads(const char* spec, mosaic_gpu_workload* out, int32_t cap,
+                               int32_t* n, mosaic_gpu_cluster* cluster) {
+    return guard([&] {
+        Cluster c;
+        auto ws = synth_workloads(spec ? spec : "", &c, nullptr);
+        *n = (int32_t)ws.size();
+        for (int i = 0; i < (int)ws.size() && i < cap; ++i)
+            out[i] = mosaic_gpu_workload{nullptr,      ws[i].flops,     ws[i].bytes,
+                                         ws[i].grad,   ws[i].knee,      ws[i].act_base,
+                                         ws[i].mem_per_quota, ws[i].fixed, ws[i].dp_penalty};
+        if (cluster)
+            *cluster = mosaic_gpu_cluster{c.gpu_count, c.memory_capacity, c.peak_compute,
+                                          c.peak_bandwidth, c.alpha, c.beta};
+        return MOSAIC_OK;
+    });
 }
 
 int mosaic_gpu_synth_problem(const char* spec, int quota_levels, mosaic_gpu_problem** out) {

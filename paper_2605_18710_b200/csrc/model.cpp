@@ -322,9 +322,9 @@ void random_instance(uint64_t seed, int n, Builder& b) {
 }
 }  // namespace
 
-Problem synth_problem(const std::string& spec, int levels_override) {
+namespace {
+Builder synth_builder(const std::string& spec, int& G, int& L) {
     Builder b;
-    int G = 1, L = 10;
     if (spec.rfind("random:", 0) == 0) {
         unsigned long long seed;
         int n, g;
@@ -342,6 +342,24 @@ Problem synth_problem(const std::string& spec, int levels_override) {
     } else {
         config(spec, b, G, L);
     }
+    return b;
+}
+}  // namespace
+
+std::vector<Workload> synth_workloads(const std::string& spec, Cluster* c, int* L) {
+    int G = 1, l = 10;
+    Builder b = synth_builder(spec, G, l);
+    if (c) {
+        *c = Cluster{};
+        c->gpu_count = G;
+    }
+    if (L) *L = l;
+    return b.ws;
+}
+
+Problem synth_problem(const std::string& spec, int levels_override) {
+    int G = 1, L = 10;
+    Builder b = synth_builder(spec, G, L);
     if (levels_override > 0) L = levels_override;
     Cluster c;
     c.gpu_count = G;

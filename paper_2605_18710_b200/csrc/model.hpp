@@ -107,5 +107,7 @@ Surface generate_surface(const Workload& w, const Cluster& c);
 // spec: cfg1..cfg5 | random:SEED:N:G | preset:NAME:COUNT:G  -> problem with the
 // default ground-truth interference (bench.hpp:31-37)
 Problem synth_problem(const std::string& spec, int quota_levels_override = 0);
+// the workloads (in module order) and cluster a spec is generated from; *L = its quota levels
+std::vector<Workload> synth_workloads(const std::string& spec, Cluster* c, int* L);
 
 }  // namespace mosaic_b200

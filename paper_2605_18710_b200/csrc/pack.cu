@@ -146,6 +146,74 @@ __global__ void __launch_bounds__(PK_THREADS)
     if (threadIdx.x == 0) counts[blockIdx.x] = n > PK_MAXROWS ? -1 : n;
 }
 
+// evaluate_workload (profiler.hpp:65-89), operation for operation (-fmad=false; fp64 div /
+// min / max are IEEE on the device).  ceil(log2(d)) is taken as the integer ceil-log2,
+// which equals the host's std::ceil(std::log2(double(d))) for every d >= 1: log2 of a
+// non-power of two is at least 1/(d ln 2) away from an integer, far above one ulp.
+__global__ void k_gen_surfaces(const GenWorkload* ws, int nw, GenCluster c, const int* dset,
+                               int nd, const double* aset, int na, double demand_scale,
+                               GenPoint* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nw * nd * na) return;
+    const int ai = i % na, di = (i / na) % nd, wi = i / (na * nd);
+    const GenWorkload w = ws[wi];
+    const int d = dset[di];
+    const double a = aset[ai];
+    const double eta0 = 0.85 + 0.15 * a / w.knee;
+    const double eta = eta0 < 1.0 ? eta0 : 1.0;  // std::min(1.0, x)
+    const double compute_time = (w.flops / d) / (a * c.peak_compute * eta);
+    const double io_time = (w.bytes / d) / c.peak_bandwidth;
+    double sync_time = 0.0;
+    if (d > 1) {
+        int e = 0;
+        while ((1LL << e) < (long long)d) ++e;
+        sync_time = c.alpha * (double)e + c.beta * w.grad;
+    }
+    GenPoint p;
+    p.d = d;
+    p.a = a;
+    const double dp_eff = 1.0 + w.dp_penalty * (d - 1);
+    const double mx = compute_time < io_time ? io_time : compute_time;  // std::max(ct, io)
+    p.latency = mx * dp_eff + sync_time + w.fixed;
+    const double sa = compute_time / p.latency;
+    p.sm_active = sa < 1.0 ? sa : 1.0;
+    const double bu = io_time / mx * demand_scale;
+    p.bandwidth_util = bu < 1.0 ? bu : 1.0;
+    p.memory = w.act_base + w.mem_per_quota * a + w.grad / d;
+    out[i] = p;
+}
+
+std::vector<GenPoint> generate_surfaces_device(const std::vector<GenWorkload>& ws,
+                                               const GenCluster& c, const std::vector<int>& d_set,
+                                               const std::vector<double>& a_set,
+                                               double demand_scale, int device) {
+    CKP(cudaSetDevice(device));
+    const size_t n = ws.size() * d_set.size() * a_set.size();
+    std::vector<GenPoint> res(n);
+    if (n == 0) return res;
+    GenWorkload* dw;
+    int* dd;
+    double* da;
+    GenPoint* dout;
+    CKP(cudaMalloc(&dw, sizeof(GenWorkload) * ws.size()));
+    CKP(cudaMalloc(&dd, sizeof(int) * d_set.size()));
+    CKP(cudaMalloc(&da, sizeof(double) * a_set.size()));
+    CKP(cudaMalloc(&dout, sizeof(GenPoint) * n));
+    CKP(cudaMemcpy(dw, ws.data(), sizeof(GenWorkload) * ws.size(), cudaMemcpyHostToDevice));
+    CKP(cudaMemcpy(dd, d_set.data(), sizeof(int) * d_set.size(), cudaMemcpyHostToDevice));
+    CKP(cudaMemcpy(da, a_set.data(), sizeof(double) * a_set.size(), cudaMemcpyHostToDevice));
+    const int T = 256;
+    k_gen_surfaces<<<(int)((n + T - 1) / T), T>>>(dw, (int)ws.size(), c, dd, (int)d_set.size(),
+                                                  da, (int)a_set.size(), demand_scale, dout);
+    CKP(cudaGetLastError());
+    CKP(cudaMemcpy(res.data(), dout, sizeof(GenPoint) * n, cudaMemcpyDeviceToHost));
+    cudaFree(dw);
+    cudaFree(dd);
+    cudaFree(da);
+    cudaFree(dout);
+    return res;
+}
+
 std::vector<std::vector<PackedRow>> pack_options_device(const std::vector<PackInput>& mods, int G,
                                                         int L, double cap, int device,
                                                         long long* h2d_bytes,

@@ -24,4 +24,22 @@ std::vector<std::vector<PackedRow>> pack_options_device(const std::vector<PackIn
                                                         long long* h2d_bytes,
                                                         std::vector<int>* range_err);
 
+struct GenWorkload {  // ModuleWorkload (profiler.hpp:26-40)
+    double flops, bytes, grad, knee, act_base, mem_per_quota, fixed, dp_penalty;
+};
+struct GenCluster {  // the ClusterSpec fields evaluate_workload reads (core.hpp:52-59)
+    double peak_compute, peak_bandwidth, alpha, beta;
+};
+struct GenPoint {
+    int d;
+    double a, latency, bandwidth_util, memory, sm_active;
+};
+
+// generate_surface (profiler.hpp:94-101) for every workload on the device: out[(w * nd + di)
+// * na + ai] = evaluate_workload(w, cluster, d_set[di], a_set[ai]) (profiler.hpp:65-89).
+std::vector<GenPoint> generate_surfaces_device(const std::vector<GenWorkload>& ws,
+                                               const GenCluster& c, const std::vector<int>& d_set,
+                                               const std::vector<double>& a_set,
+                                               double demand_scale, int device);
+
 }  // namespace mg

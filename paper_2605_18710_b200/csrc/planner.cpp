@@ -347,6 +347,67 @@ StageResult Planner::stage_eval(uint64_t mask) {
     return res;
 }
 
+// core.hpp:281-351: partition coverage, dependency order, per-GPU quota sum <= 1 + 1e-9,
+// per-GPU memory <= capacity * (1 + 1e-12) with footprint = lookup(d, a).memory + base.
+std::string Planner::validate_plan(const std::vector<std::vector<Entry>>& stages,
+                                   std::string* msg) const {
+    const int n = (int)P_.modules.size();
+    std::vector<int> stage_of(n, -1);
+    auto fail = [&](const char* code, const std::string& m) {
+        if (msg) *msg = m;
+        return std::string(code);
+    };
+    for (int si = 0; si < (int)stages.size(); ++si) {
+        if (stages[si].empty()) return fail("EmptyStage", "stage " + std::to_string(si) + " is empty");
+        for (const auto& e : stages[si]) {
+            if (e.module < 0 || e.module >= n)
+                return fail("ModuleMissing", "stage entry references unknown module index");
+            if (stage_of[e.module] != -1)
+                return fail("ModuleDuplicated", "module " + P_.modules[e.module].id +
+                                                    " appears in more than one stage");
+            stage_of[e.module] = si;
+            if ((int)e.gpus.size() != e.d)
+                return fail("SmOvercommit", "placement size does not match dp degree for " +
+                                                P_.modules[e.module].id);
+            for (int r : e.gpus)
+                if (r < 0 || r >= P_.gpu_count)
+                    return fail("SmOvercommit", "GPU index out of range for " + P_.modules[e.module].id);
+        }
+    }
+    for (int i = 0; i < n; ++i)
+        if (stage_of[i] == -1) return fail("ModuleMissing", "module " + P_.modules[i].id + " not placed");
+    for (auto [u, v] : P_.edges)
+        if (stage_of[u] >= stage_of[v])
+            return fail("DependencyViolated", "edge " + P_.modules[u].id + " -> " +
+                                                  P_.modules[v].id + " not strictly ordered");
+    for (int si = 0; si < (int)stages.size(); ++si) {
+        std::vector<double> quota(P_.gpu_count, 0.0), mem(P_.gpu_count, 0.0);
+        for (const auto& e : stages[si]) {
+            std::vector<int> g(e.gpus);
+            std::sort(g.begin(), g.end());
+            if (std::adjacent_find(g.begin(), g.end()) != g.end())
+                return fail("SmOvercommit", "replica co-location on one GPU for " + P_.modules[e.module].id);
+            const double a = (double)e.units / P_.quota_levels;
+            const double fp = P_.modules[e.module].surface.lookup(e.d, a).memory +
+                              P_.modules[e.module].memory_base;
+            for (int r : e.gpus) {
+                quota[r] += a;
+                mem[r] += fp;
+            }
+        }
+        for (int r = 0; r < P_.gpu_count; ++r) {
+            if (quota[r] > 1.0 + 1e-9)
+                return fail("SmOvercommit", "SM quota overcommit on GPU " + std::to_string(r) +
+                                                " in stage " + std::to_string(si));
+            if (mem[r] > P_.memory_capacity * (1.0 + 1e-12))
+                return fail("MemoryOvercommit", "memory overcommit on GPU " + std::to_string(r) +
+                                                    " in stage " + std::to_string(si));
+        }
+    }
+    if (msg) msg->clear();
+    return "";
+}
+
 double Planner::stage_min(uint64_t mask, double ub, bool restart, mg::SearchStats& st) {
     const auto mods = mask_modules(mask);
     if ((int)mods.size() > mg::MAXK) throw Error(TOO_LARGE, "stage larger than 12 modules");

@@ -77,6 +77,10 @@ class Planner {
     StageResult exact_stage(uint64_t mask);
     StageResult feasible(uint64_t mask, double tau);
     PlanResult solve();
+    // validate_plan (core.hpp:281-351) with the footprint oracle; "" when valid, else the
+    // ValidationCode name, message in *msg
+    std::string validate_plan(const std::vector<std::vector<Entry>>& stages,
+                              std::string* msg) const;
     // T* of a module set below `ub` (one MIN search when restart == false)
     double stage_min(uint64_t mask, double ub, bool restart, mg::SearchStats& st);
     PlanResult brute_force();

@@ -31,6 +31,7 @@ LIB_PATH = os.path.join(_HERE, "libmosaic_gpu.so")
 MAX_STAGE_MODULES = 12
 MAX_GPUS = 1024
 MAX_STAGES = 64
+MAX_MODULES = 64
 
 OK, INFEASIBLE, MODULE_NO_OPTION, RANGE, TOO_LARGE, CUDA, EMPTY = range(7)
 
@@ -65,6 +66,20 @@ class DeviceError(MosaicError):
 class Point(C.Structure):
     _fields_ = [("d", C.c_int32), ("a", C.c_double), ("latency", C.c_double),
                 ("bandwidth_util", C.c_double), ("memory", C.c_double), ("sm_active", C.c_double)]
+
+
+class WorkloadC(C.Structure):
+    _fields_ = [("id", C.c_char_p), ("flops_per_iter", C.c_double),
+                ("bytes_per_iter", C.c_double), ("gradient_bytes", C.c_double),
+                ("sm_efficiency_knee", C.c_double), ("memory_act_base", C.c_double),
+                ("memory_per_quota", C.c_double), ("fixed_overhead", C.c_double),
+                ("dp_penalty", C.c_double)]
+
+
+class ClusterC(C.Structure):
+    _fields_ = [("gpu_count", C.c_int32), ("memory_capacity", C.c_double),
+                ("peak_compute", C.c_double), ("peak_bandwidth", C.c_double),
+                ("interconnect_alpha", C.c_double), ("interconnect_beta", C.c_double)]
 
 
 class ModuleC(C.Structure):
@@ -122,6 +137,7 @@ EXPORTS = [
     "mosaic_gpu_reset_counters", "mosaic_gpu_synth_problem", "mosaic_gpu_free_problem",
     "mosaic_gpu_own_launches", "mosaic_gpu_ksearch_ms", "mosaic_gpu_ksearch_launches",
     "mosaic_gpu_h2d_bytes", "mosaic_gpu_d2h_bytes", "mosaic_gpu_mark", "mosaic_gpu_marked_ms", "mosaic_gpu_alg_bytes", "mosaic_gpu_stage_min",
+    "mosaic_gpu_validate_plan", "mosaic_gpu_generate_surfaces", "mosaic_gpu_synth_workloads",
 ]
 
 _lib = None
@@ -177,6 +193,14 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "mosaic_gpu_alg_bytes": (C.c_int64, [vp]),
         "mosaic_gpu_stage_min": (C.c_int, [vp, C.c_uint64, C.c_double, C.c_int,
                                            P(C.c_double), P(StageResultC)]),
+        "mosaic_gpu_generate_surfaces": (C.c_int, [P(WorkloadC), C.c_int32, P(ClusterC),
+                                                   P(C.c_int32), C.c_int32, P(C.c_double),
+                                                   C.c_int32, C.c_double, C.c_int, P(Point),
+                                                   P(C.c_int32), P(C.c_int32)]),
+        "mosaic_gpu_synth_workloads": (C.c_int, [C.c_char_p, P(WorkloadC), C.c_int32,
+                                                 P(C.c_int32), P(ClusterC)]),
+        "mosaic_gpu_validate_plan": (C.c_int, [vp, P(EvalEntryC), P(C.c_int32), P(C.c_int64),
+                                               C.c_int64, C.c_char_p, C.c_size_t]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -497,6 +521,23 @@ class Planner:
             return list(st[:n]), [list(rect[off[i]:off[i + 1]]) for i in range(n)]
         return list(st[:n])
 
+    def validate_plan(self, plan: "DeploymentPlan") -> tuple[str, str]:
+        """validate_plan (core.hpp:281-351) -> (ValidationCode name, message)."""
+        ents, gpus, off = [], [], [0]
+        for st in plan.stages:
+            for e in st.entries:
+                ents.append(EvalEntryC(e.module, e.option.dp_degree, e.option.quota_units,
+                                       len(e.gpus), len(gpus)))
+                gpus.extend(e.gpus)
+            off.append(len(ents))
+        E = (EvalEntryC * max(1, len(ents)))(*ents)
+        G = (C.c_int32 * max(1, len(gpus)))(*gpus)
+        O = (C.c_int64 * len(off))(*off)
+        buf = C.create_string_buffer(64)
+        L = load_library()
+        _raise(L.mosaic_gpu_validate_plan(self._ctx, E, G, O, len(plan.stages), buf, 64))
+        return buf.value.decode(), L.mosaic_gpu_last_error().decode()
+
     def launch_count(self) -> int:
         return load_library().mosaic_gpu_launch_count(self._ctx)
 
@@ -587,3 +628,75 @@ def merge_records(records: bytes, world: int, mode: int) -> int:
     buf = C.create_string_buffer(records, len(records))
     _raise(load_library().mosaic_gpu_merge_records(buf, world, mode, C.byref(w)))
     return w.value
+
+
+# ---------------------------------------------------------------------------
+# N2: input generation on the device (profiler.hpp)
+# ---------------------------------------------------------------------------
+@dataclass
+class ModuleWorkload:
+    """ModuleWorkload (profiler.hpp:26-40)."""
+    id: str
+    flops_per_iter: float
+    bytes_per_iter: float
+    gradient_bytes: float
+    sm_efficiency_knee: float
+    memory_act_base: float
+    memory_per_quota: float
+    fixed_overhead: float
+    dp_penalty: float
+
+
+@dataclass
+class ClusterSpec:
+    """ClusterSpec (core.hpp:52-59)."""
+    gpu_count: int = 1
+    memory_capacity: float = 80e9
+    peak_compute: float = 500e12
+    peak_bandwidth: float = 3.35e12
+    interconnect_alpha: float = 5e-6
+    interconnect_beta: float = 2.2e-12
+
+
+def synth_workloads(spec: str) -> tuple[list[ModuleWorkload], ClusterSpec]:
+    """Workloads (module order) and cluster behind a synthetic spec ('cfg1'..'cfg5',
+    'random:SEED:N:G', 'preset:NAME:K:G'): make_workload / make_preset / random_instance."""
+    L = load_library()
+    buf = (WorkloadC * MAX_MODULES)()
+    n = C.c_int32()
+    cl = ClusterC()
+    _raise(L.mosaic_gpu_synth_workloads(spec.encode(), buf, MAX_MODULES, C.byref(n), C.byref(cl)))
+    pp = C.POINTER(ProblemC)()
+    _raise(L.mosaic_gpu_synth_problem(spec.encode(), 0, C.byref(pp)))
+    ids = [pp.contents.modules[i].id.decode() for i in range(n.value)]
+    L.mosaic_gpu_free_problem(pp)
+    ws = [ModuleWorkload(ids[i], *[getattr(buf[i], f) for f, _ in WorkloadC._fields_[1:]])
+          for i in range(n.value)]
+    return ws, ClusterSpec(*[getattr(cl, f) for f, _ in ClusterC._fields_])
+
+
+def generate_surfaces(workloads: Sequence[ModuleWorkload], cluster: ClusterSpec,
+                      d_set: Optional[Sequence[int]] = None,
+                      a_set: Optional[Sequence[float]] = None, demand_scale: float = 1.0,
+                      device: int = 0) -> list[list[tuple]]:
+    """generate_surfaces (profiler.hpp:65-111) on the device (k_gen_surfaces): per workload,
+    the (d, a, latency, bandwidth_util, memory, sm_active) grid, d-major then a — the
+    `points` format Planner.from_surfaces takes.  d_set/a_set default to
+    default_dp_degrees(gpu_count) / default_quota_grid()."""
+    L = load_library()
+    W = (WorkloadC * max(1, len(workloads)))(*[
+        WorkloadC(None, w.flops_per_iter, w.bytes_per_iter, w.gradient_bytes,
+                  w.sm_efficiency_knee, w.memory_act_base, w.memory_per_quota,
+                  w.fixed_overhead, w.dp_penalty) for w in workloads])
+    cl = ClusterC(*[getattr(cluster, f) for f, _ in ClusterC._fields_])
+    D = (C.c_int32 * len(d_set))(*d_set) if d_set is not None else None
+    A = (C.c_double * len(a_set))(*a_set) if a_set is not None else None
+    nd, na = C.c_int32(), C.c_int32()
+    args = (W, len(workloads), C.byref(cl), D, len(d_set or []), A, len(a_set or []),
+            demand_scale, device)
+    _raise(L.mosaic_gpu_generate_surfaces(*args, None, C.byref(nd), C.byref(na)))
+    per = nd.value * na.value
+    out = (Point * max(1, per * len(workloads)))()
+    _raise(L.mosaic_gpu_generate_surfaces(*args, out, C.byref(nd), C.byref(na)))
+    return [[(p.d, p.a, p.latency, p.bandwidth_util, p.memory, p.sm_active)
+             for p in out[i * per:(i + 1) * per]] for i in range(len(workloads))]

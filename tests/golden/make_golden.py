@@ -172,8 +172,82 @@ def io_files() -> None:
     dump("io_files.json", out)
 
 
+def _plan_spec(stages) -> str:
+    return "|".join(";".join(f"{m}:{d}:{u}:{'.'.join(map(str, gp))}" for m, d, u, gp in st)
+                    for st in stages)
+
+
+def _mutate(stages, rng: random.Random, n: int, g: int, L: int):
+    st = [[list(e) for e in s] for s in stages]
+    kind = rng.choice(["none", "drop", "dup", "swap", "units", "dp", "gpu_oob", "coloc",
+                       "empty", "merge", "big", "neg_module", "memstack"])
+    flat = [(i, j) for i, s in enumerate(st) for j in range(len(s))]
+    i, j = rng.choice(flat)
+    e = st[i][j]
+    if kind == "drop":
+        del st[i][j]
+        st = [s for s in st if s] or [[]]
+    elif kind == "dup":
+        st[rng.randrange(len(st))].append(list(e))
+    elif kind == "swap" and len(st) > 1:
+        a, b = rng.sample(range(len(st)), 2)
+        st[a], st[b] = st[b], st[a]
+    elif kind == "units":
+        e[2] = min(L, e[2] + rng.randint(1, L))
+    elif kind == "dp":
+        e[1] = e[1] + 1
+    elif kind == "gpu_oob":
+        e[3] = e[3][:-1] + [g + rng.randint(0, 3)]
+    elif kind == "coloc" and e[1] >= 2:
+        e[3] = [e[3][0]] * 2 + e[3][2:]
+    elif kind == "empty":
+        st.insert(rng.randrange(len(st) + 1), [])
+    elif kind == "merge":
+        st = [[x for s in st for x in s]]
+    elif kind == "big":
+        e[2] = L
+        st[i] = [x for x in st[i]] + [[m, e[1], L, e[3]] for m in range(n)
+                                     if all(y[0] != m for s in st for y in s)]
+    elif kind == "memstack":  # every replica on GPU 0 at d=1, u=1: memory, not quota
+        st = [[[x[0], 1, 1, [0]] for x in s] for s in st]
+    elif kind == "neg_module":
+        e[0] = rng.choice([-1, n])
+    return kind, st
+
+
+def _mutate_kind(stages, kind):
+    return kind, [[[x[0], 1, 1, [0]] for x in s] for s in stages]
+
+
+def validate() -> None:
+    """H15 validate_plan verdicts of the reference on solved plans and fuzzed mutations."""
+    rng = random.Random(2605)
+    out = []
+    insts = [("cfg1", 2, 8, 10, []), ("cfg2", 4, 8, 10, []), ("cfg3", 4, 16, 10, []),
+             ("cfg4", 6, 64, 10, [])]
+    for seed in range(1, 13):
+        for extra in ([], ["mem=20e9"], ["mem=6e9"], ["mem=3e9"]):
+            insts.append((f"random:{seed}:{2 + seed % 4}:4", 2 + seed % 4, 4, 4,
+                          ["levels=4", *extra]))
+    for inst, n, g, L, extra in insts:
+        sol = ref(inst, "solve", *extra)
+        if "stages" not in sol:
+            continue
+        g, L = sol["gpus"], sol["levels"]
+        base = [[(a["m"], a["d"], a["u"], a["gpus"]) for a in s["alloc"]] for s in sol["stages"]]
+        cases = [("none", base), _mutate_kind(base, "memstack")] + [
+            _mutate(base, rng, n, g, L) for _ in range(12)]
+        for kind, st in cases:
+            spec = _plan_spec(st)
+            r = ref(inst, "validate", spec, *extra)
+            out.append({"inst": inst, "extra": extra, "kind": kind,
+                        "stages": [[list(x) for x in s] for s in st],
+                        "code": r.get("code"), "exception": r.get("exception")})
+    dump("validate.json", out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["configs", "cfg5_stages", "random_sets", "presets", "variants",
-                             "stime", "io_files"]
+                             "stime", "io_files", "validate"]
     for w in which:
         globals()[w]()

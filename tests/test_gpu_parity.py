@@ -278,3 +278,42 @@ def test_evaluator_reproduces_searched_allocations():
     pl = planner("cfg4")
     res = pl.solve()
     assert pl.stage_time(res.plan.stages) == res.plan.predicted_stage_times
+
+
+def _plan_of(stages, L):
+    return mosaic.DeploymentPlan(stages=[
+        mosaic.StageAllocation(entries=[
+            mosaic.Entry(m, mosaic.DeploymentOption(d, u, L), list(g)) for m, d, u, g in st])
+        for st in stages])
+
+
+def test_validate_plan_matches_reference_verdicts():
+    # H15 validate_plan (core.hpp:281-351) with the footprint oracle: solved plans and fuzzed
+    # mutations (drop / duplicate / reorder / overcommit / co-locate / out-of-range / empty)
+    rows = load_golden("validate.json")
+    groups = {}
+    for row in rows:
+        groups.setdefault((row["inst"], tuple(row["extra"])), []).append(row)
+    for (inst, extra), rs in groups.items():
+        lv = [int(x[7:]) for x in extra if x.startswith("levels=")]
+        rest = [x for x in extra if not x.startswith("levels=")]
+        pl = planner(inst, lv[0] if lv else 0, extra=rest)
+        L = pl.quota_levels
+        for r in rs:
+            plan = _plan_of(r["stages"], L)
+            if r["exception"]:
+                with pytest.raises(mosaic.SurfaceRangeError):
+                    pl.validate_plan(plan)
+            else:
+                code, msg = pl.validate_plan(plan)
+                assert code == r["code"], (inst, extra, r["kind"], msg)
+        pl.close()
+
+
+def test_solved_plans_validate_ok():
+    # acceptance C9: every plan solve() returns passes validate_plan with footprints
+    for spec, L in [("cfg1", 0), ("cfg3", 0), ("cfg4", 0), ("random:5:5:8", 4),
+                    ("preset:ofasys:10:8", 0)]:
+        pl = planner(spec, L)
+        assert pl.validate_plan(pl.solve().plan)[0] == "Ok"
+        pl.close()
