@@ -203,6 +203,33 @@ def reference_arm(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+TRAFFIC_CSV = "profiles/r1_dram_cfg5_solve.csv"
+
+
+def dram_traffic_per_launch():
+    """Average DRAM bytes (read + write) per k_search launch in the committed ncu list."""
+    import csv
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), TRAFFIC_CSV)
+    if not os.path.exists(path):
+        return None
+    rows = list(csv.reader(open(path)))
+    hdr = next((r for r in rows if "Kernel Name" in r), None)
+    if hdr is None:
+        return None
+    tot, ids = 0.0, set()
+    for r in rows:
+        if len(r) != len(hdr) or r is hdr:
+            continue
+        d = dict(zip(hdr, r))
+        if not d["Kernel Name"].startswith("k_search"):
+            continue
+        if d["Metric Name"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(d["Metric Unit"], 1)
+            tot += float(d["Metric Value"].replace(",", "")) * scale
+            ids.add(d["ID"])
+    return tot / len(ids) if ids else None
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -309,12 +336,15 @@ def main() -> None:
         return
 
     # ---- roofline of the dominant kernel (k_search) ----
+    # traffic: dram__bytes_read.sum + dram__bytes_write.sum per k_search launch, from the
+    # committed ncu capture of the same cfg5 solve (profiles/)
     peak, peak_kind = peaks()
     ks_ms = ctr["ksearch_ms"]
     ks_n = max(1, ctr["ksearch_launches"])
     alg_bytes = ctr.get("alg_bytes", 0)
     avg_launch_s = ks_ms / ks_n / 1000.0
     achieved = (alg_bytes / ks_n) / avg_launch_s / 1e9 if avg_launch_s > 0 else 0.0
+    traffic = dram_traffic_per_launch() if WORKLOAD == "cfg5" else None
 
     cpu = None
     if not args.no_cpu_baseline and os.path.exists(REF_DRIVER):
@@ -344,7 +374,8 @@ def main() -> None:
                 "d2h_bytes_per_step": d2h, "timing": "host wall clock, create+solve+readback"},
         "gpu_launches": ctr["own_launches"],
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "traffic_source": TRAFFIC_CSV if traffic is not None else None,
                      "kernel": "k_search", "peak_kind": peak_kind,
                      "algorithmic_bytes": "24*k B per scored leaf (k option rows x 3 fp64, "
                                           "SURVEY.md 8d)",

@@ -234,7 +234,7 @@ static size_t smem_bytes(int G, int k) { return SMEM_SPEC + WPC * walk_layout(G,
 //   MIN:   shared incumbent (atomicMin on the fp64 bits), tie band TIE_EPS.
 //   FIRST: hits are ordered by their reference-DFS path; the earliest is kept under a
 //          seqlock, and work that lies after it is abandoned.
-__global__ void __launch_bounds__(32 * WPC) k_search(const Spec* Sg, Rows R, Cont* Q, int* ready,
+__global__ void __launch_bounds__(32 * WPC, 6) k_search(const Spec* Sg, Rows R, Cont* Q, int* ready,
                                                      Ctl* ctl, HitPath* best, Leaf* leaf_out) {
     extern __shared__ __align__(16) unsigned char smem[];
     Spec& S = *reinterpret_cast<Spec*>(smem);
@@ -565,7 +565,6 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
         hc->has_hit = 1;
         CK(cudaMemcpyAsync(d_best_, seed_path, sizeof(HitPath), cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(d_leaf_, seed_leaf, sizeof(Leaf), cudaMemcpyHostToDevice, s));
-        CK(cudaStreamSynchronize(s));
         h2d_ += sizeof(HitPath) + sizeof(Leaf);
     }
     CK(cudaMemcpyAsync(d_spec_, hs, sizeof(Spec), cudaMemcpyHostToDevice, s));
@@ -605,21 +604,20 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     ++launches_;
     ++own_launches_;
     ++st.rounds;
+    // one read-back and one synchronisation per search: the control block and the leaf
+    // (1 KB, read unconditionally — cheaper than a second round trip when there is a hit)
     CK(cudaMemcpyAsync(hc, d_ctl_, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
-    d2h_ += sizeof(Ctl);
-    CK(cudaStreamSynchronize(s));
+    CK(cudaMemcpyAsync(hl, d_leaf_, sizeof(Leaf), cudaMemcpyDeviceToHost, s));
+    d2h_ += sizeof(Ctl) + sizeof(Leaf);
+    CK(cudaEventRecord((cudaEvent_t)ev1_, s));
+    CK(cudaEventSynchronize((cudaEvent_t)ev1_));
     CK(cudaGetLastError());
     ticket_base_ = hc->q_tail + 1;
     if (hc->has_hit && !hc->overflow) {
-        CK(cudaMemcpyAsync(hl, d_leaf_, sizeof(Leaf), cudaMemcpyDeviceToHost, s));
-        d2h_ += sizeof(Leaf);
-        CK(cudaStreamSynchronize(s));
         res.found = true;
         res.leaf = *hl;
     }
     if (world_ > 1) merge_ranks(S, hc, res);
-    CK(cudaEventRecord((cudaEvent_t)ev1_, s));
-    CK(cudaEventSynchronize((cudaEvent_t)ev1_));
     float kms = 0, ms = 0;
     CK(cudaEventElapsedTime(&kms, (cudaEvent_t)evk0_, (cudaEvent_t)evk1_));
     CK(cudaEventElapsedTime(&ms, (cudaEvent_t)ev0_, (cudaEvent_t)ev1_));

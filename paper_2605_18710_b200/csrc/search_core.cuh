@@ -34,6 +34,9 @@
 #ifndef MG_HD
 #define MG_HD __device__ __forceinline__
 #endif
+#ifndef MG_COLD
+#define MG_COLD __device__ __noinline__  // rare paths (hits): kept out of the hot loop
+#endif
 // Device code below is only compiled by nvcc (the host planner includes this header
 // for the Spec/Node/Leaf layouts only; there is no host search path).
 #if defined(__CUDACC__) || defined(MG_HOST_HARNESS)
@@ -219,6 +222,7 @@ MG_HX void walk_carve(Walk& w, unsigned char* base, int G, int k) {
 #ifdef MG_DEVICE_CODE
 MG_HD double envelope(const Spec& S, int j, double P) {
     double g = POS_INF;
+    #pragma unroll 1
     for (int i = 0; i < S.env_n[j]; ++i) {
         double v = S.env_a[j][i] + S.env_b[j][i] * P;
         g = v < g ? v : g;
@@ -232,6 +236,7 @@ MG_HD double contrib(const Spec& S, const Rows& R, const uint16_t* opt, unsigned
     if (!mask) return NEG_INF;
     if (S.include_self) {
         double s = 0.0, p = 1.0, mb = NEG_INF;
+        #pragma unroll 1
         for (int pos = 0; pos < S.k; ++pos) {
             int l = S.pos_lvl[pos];
             if (!(mask >> l & 1u)) continue;
@@ -247,11 +252,13 @@ MG_HD double contrib(const Spec& S, const Rows& R, const uint16_t* opt, unsigned
         return mb + dl;
     }
     double best = NEG_INF;
+    #pragma unroll 1
     for (int pos = 0; pos < S.k; ++pos) {
         int l = S.pos_lvl[pos];
         if (!(mask >> l & 1u)) continue;
         double s = 0.0, p = 1.0;
         int n = 0;
+        #pragma unroll 1
         for (int pos2 = 0; pos2 < S.k; ++pos2) {
             int l2 = S.pos_lvl[pos2];
             if (l2 == l || !(mask >> l2 & 1u)) continue;
@@ -276,6 +283,7 @@ MG_HD double contrib_o(const Spec& S, const Rows& R, const uint16_t* opt, unsign
     if (!mask) return NEG_INF;
     if (S.include_self) {
         double s = 0.0, p = 1.0, mb = NEG_INF;
+        #pragma unroll 1
         for (int pos = 0; pos < S.k; ++pos) {
             int l = S.pos_lvl[pos];
             if (!(mask >> l & 1u)) continue;
@@ -291,11 +299,13 @@ MG_HD double contrib_o(const Spec& S, const Rows& R, const uint16_t* opt, unsign
         return mb + dl;
     }
     double best = NEG_INF;
+    #pragma unroll 1
     for (int pos = 0; pos < S.k; ++pos) {
         int l = S.pos_lvl[pos];
         if (!(mask >> l & 1u)) continue;
         double s = 0.0, p = 1.0;
         int n = 0;
+        #pragma unroll 1
         for (int pos2 = 0; pos2 < S.k; ++pos2) {
             int l2 = S.pos_lvl[pos2];
             if (l2 == l || !(mask >> l2 & 1u)) continue;
@@ -316,6 +326,7 @@ MG_HD double contrib_o(const Spec& S, const Rows& R, const uint16_t* opt, unsign
 // Owner rank of an option prefix (levels 0..j with level j's option o).
 MG_HD unsigned shard_hash(const uint16_t* opt, int j, int o) {
     unsigned h = 2166136261u;
+    #pragma unroll 1
     for (int l = 0; l <= j; ++l) {
         h ^= (unsigned)(l == j ? o : opt[l]) + 0x9e37u * (unsigned)(l + 1);
         h *= 16777619u;
@@ -351,6 +362,7 @@ MG_HD void block_stats(const Spec& S, const Rows& R, const uint16_t* opt, unsign
     mb = NEG_INF;
     P = 1.0;
     mbx = NEG_INF;  // max(base - e2*B): residents' own-excluded additive bound
+    #pragma unroll 1
     for (int l = 0; l < nlev; ++l) {
         if (!(mask >> l & 1u)) continue;
         int r = S.lvl_off[l] + opt[l];
@@ -367,11 +379,13 @@ MG_HD void block_stats(const Spec& S, const Rows& R, const uint16_t* opt, unsign
 
 // -1: path H precedes the walk's leaf path (levels 0..j), +1 follows it, 0 equal.
 template <class HP>
-MG_HD int path_cmp(const HP* H, const Walk& w, int j) {
+MG_COLD int path_cmp(const HP* H, const Walk& w, int j) {
+    #pragma unroll 1
     for (int l = 0; l <= j; ++l) {
         int ho = H->opt[l];
         if (ho != w.opt[l]) return ho < w.opt[l] ? -1 : 1;
         const int o0 = w.loff[l];
+        #pragma unroll 1
         for (int b = 0; b < w.nb[l]; ++b) {
             int hx = H->x[l][b], wx = w.x[o0 + b];
             if (hx != wx) return hx > wx ? -1 : 1;  // larger count first
@@ -383,11 +397,13 @@ MG_HD int path_cmp(const HP* H, const Walk& w, int j) {
 // Does H precede every leaf the walk can still reach?  Levels < j are fixed at their
 // current (option, composition); at level j only the options after oc[j] remain.
 template <class HP>
-MG_HD bool path_precedes_rest(const HP* H, const Walk& w, int j) {
+MG_COLD bool path_precedes_rest(const HP* H, const Walk& w, int j) {
+    #pragma unroll 1
     for (int l = 0; l < j; ++l) {
         int ho = H->opt[l];
         if (ho != w.opt[l]) return ho < w.opt[l];
         const int o0 = w.loff[l];
+        #pragma unroll 1
         for (int b = 0; b < w.nb[l]; ++b) {
             int hx = H->x[l][b], wx = w.x[o0 + b];
             if (hx != wx) return hx > wx;
@@ -397,21 +413,25 @@ MG_HD bool path_precedes_rest(const HP* H, const Walk& w, int j) {
 }
 
 template <class HP>
-MG_HD void path_store(HP* H, const Walk& w, int j) {
+MG_COLD void path_store(HP* H, const Walk& w, int j) {
+    #pragma unroll 1
     for (int l = 0; l <= j; ++l) {
         H->opt[l] = w.opt[l];
         H->nb[l] = w.nb[l];
         const int o0 = w.loff[l];
+        #pragma unroll 1
         for (int b = 0; b < w.nb[l]; ++b) H->x[l][b] = w.x[o0 + b];
     }
 }
 
 // Write the FIRST leaf: options and the final block list after the last level.
-MG_HD void store_leaf(const Walk& w, int j, double v, Leaf& lf) {
+MG_COLD void store_leaf(const Walk& w, int j, double v, Leaf& lf) {
     lf.value = v;
+#pragma unroll 1
     for (int l = 0; l <= j; ++l) lf.opt[l] = w.opt[l];
     int o0 = w.loff[j];
     int m = 0;
+#pragma unroll 1
     for (int b = 0; b < w.nb[j]; ++b) {
         int xb = w.x[o0 + b], s = w.bsz[o0 + b];
         unsigned mk = w.bmk[o0 + b];

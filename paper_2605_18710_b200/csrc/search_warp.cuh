@@ -37,6 +37,7 @@ __device__ __forceinline__ int wscan_incl(int v) {
 
 __device__ __forceinline__ void parent_stats_warp(const Spec& S, const Rows& R, Walk& w, int j) {
     const int o0 = w.loff[j];
+    #pragma unroll 1
     for (int b = lane_id(); b < w.nb[j]; b += 32)
         block_stats(S, R, w.opt, w.bmk[o0 + b], j, w.pu[b], w.pm[b], w.psum[b], w.pmb[b], w.pP[b],
                     w.pmx[b]);
@@ -47,10 +48,12 @@ __device__ __forceinline__ void parent_stats_warp(const Spec& S, const Rows& R, 
 __device__ __forceinline__ bool first_comp_warp(Walk& w, int o0, int nb, int d) {
     const int lane = lane_id();
     int mylo = 0;
+    #pragma unroll 1
     for (int b = lane; b < nb; b += 32) mylo += w.lo[o0 + b];
     const int R = d - wsum(mylo);
     if (R < 0) return false;
     int carry = 0;
+    #pragma unroll 1
     for (int c = 0; c < nb; c += 32) {
         const int b = c + lane;
         const int room = b < nb ? (int)w.hi[o0 + b] - (int)w.lo[o0 + b] : 0;
@@ -73,6 +76,7 @@ __device__ __forceinline__ bool next_comp_warp(Walk& w, int o0, int nb) {
     const int lane = lane_id();
     // inclusive prefix of slack_t = hi_t - x_t and extra_t = x_t - lo_t
     int cs = 0, ce = 0;
+    #pragma unroll 1
     for (int c = 0; c < nb; c += 32) {
         const int b = c + lane;
         const int sl = b < nb ? (int)w.hi[o0 + b] - (int)w.x[o0 + b] : 0;
@@ -88,6 +92,7 @@ __device__ __forceinline__ bool next_comp_warp(Walk& w, int o0, int nb) {
     __syncwarp();
     // rightmost i <= nb-2 with x_i > lo_i and slack to its right
     int best = -1;
+    #pragma unroll 1
     for (int i = lane; i < nb - 1; i += 32)
         if (w.x[o0 + i] > w.lo[o0 + i] && cs - w.sa[i] >= 1) best = i;
     const int is = wmaxi(best);
@@ -96,6 +101,7 @@ __device__ __forceinline__ bool next_comp_warp(Walk& w, int o0, int nb) {
     __syncwarp();
     if (lane == 0) w.x[o0 + is] -= 1;
     int carry = 0;
+    #pragma unroll 1
     for (int c = 0; c < nb; c += 32) {
         const int b = c + lane;
         const bool mine = b < nb && b > is;
@@ -119,6 +125,7 @@ __device__ __forceinline__ bool last_feasible_warp(const Walk& w, int o0, int nb
                                                    const double* take) {
     int lo = 0, hi = 0;
     bool dead = false;
+    #pragma unroll 1
     for (int b = lane_id(); b < nb; b += 32) {
         const int s = w.bsz[o0 + b];
         const bool rok = le ? rest[b] <= t : rest[b] < t;
@@ -144,6 +151,7 @@ __device__ __forceinline__ bool level_has_rest_warp(const Spec& S, const Walk& w
     const int o0 = w.loff[l];
     const int nb = w.nb[l];
     int cs = 0;
+    #pragma unroll 1
     for (int c = 0; c < nb; c += 32) {
         const int b = c + lane;
         const int sl = b < nb ? (int)w.hi[o0 + b] - (int)w.x[o0 + b] : 0;
@@ -153,6 +161,7 @@ __device__ __forceinline__ bool level_has_rest_warp(const Spec& S, const Walk& w
     }
     __syncwarp();
     bool any = false;
+    #pragma unroll 1
     for (int i = lane; i < nb - 1; i += 32)
         if (w.x[o0 + i] > w.lo[o0 + i] && cs - w.sa[i] >= 1) any = true;
     const bool r = wany(any);
@@ -166,10 +175,12 @@ __device__ __forceinline__ double greedy_fill_warp(Walk& w, int o0, int nb, int 
                                                    const double* rest, const double* take) {
     const int lane = lane_id();
     int mylo = 0;
+    #pragma unroll 1
     for (int b = lane; b < nb; b += 32) mylo += (rest[b] <= t) ? 0 : w.bsz[o0 + b];
     const int rem0 = dd - wsum(mylo);
     int carry = 0;
     double v = 0.0;
+    #pragma unroll 1
     for (int c = 0; c < nb; c += 32) {
         const int b = c + lane;
         int l = 0, room = 0;
@@ -203,6 +214,7 @@ __device__ __forceinline__ bool lane_last_feasible(const Spec& S, const Rows& R,
                                                    int j, int o0, int nb, int o, int uu,
                                                    double ff, int dd, double t, bool le) {
     int lo = 0, hi = 0;
+    #pragma unroll 1
     for (int b = 0; b < nb; ++b) {
         const int s = w.bsz[o0 + b];
         const double rv = w.cs[b];
@@ -239,6 +251,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
     }
     // per block: approximate rest contribution (fast filter); the exact one is computed
     // only once some option survives the filter (proof searches rarely need it)
+    #pragma unroll 1
     for (int b = lane; b < nb; b += 32) {
         const unsigned m = w.bmk[o0 + b];
         w.cm[b] = m ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] + (S.additive ? 0.0 : S.e3 * w.pP[b])
@@ -247,6 +260,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
     __syncwarp();
     bool rest_ready = !S.include_self;
     if (rest_ready) {
+        #pragma unroll 1
         for (int b = lane; b < nb; b += 32) w.cs[b] = contrib(S, R, w.opt, w.bmk[o0 + b]);
         __syncwarp();
     }
@@ -254,6 +268,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
     const int n = S.lvl_n[j] < w.oe[j] ? S.lvl_n[j] : w.oe[j];
     const int off = S.lvl_off[j];
     const double thr = h.thr(S);
+    #pragma unroll 1
     for (int start = w.oc[j] + 1; start < n; start += 32) {
         const int o = start + lane;
         const int t = o < n ? opt_test(S, R, off + o, thr) : 2;
@@ -286,6 +301,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
             if (S.include_self) {
                 const double tx = fm ? S.theta * (1.0 + 1e-12) : Ie;
                 int lo = 0, hi = 0;
+                #pragma unroll 1
                 for (int b = 0; b < nb && pass; ++b) {
                     const int s = w.bsz[o0 + b];
                     const bool el = w.pu[b] + uu <= S.L && !(w.pm[b] + ff > S.cap_slack);
@@ -310,6 +326,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
             }
         }
         if (!rest_ready && __any_sync(FULLW, valid && pass)) {
+            #pragma unroll 1
             for (int b = lane; b < nb; b += 32) w.cs[b] = contrib(S, R, w.opt, w.bmk[o0 + b]);
             __syncwarp();
             rest_ready = true;
@@ -324,6 +341,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
                     double hiv = Ie;
                     while (true) {
                         double c = NEG_INF;
+                        #pragma unroll 1
                         for (int b = 0; b < nb; ++b) {
                             const double rv = w.cs[b];
                             if (rv < hiv && rv > c) c = rv;
@@ -352,6 +370,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
                 win = __ffs(fb) - 1;
             } else {
                 double mv = val;
+                #pragma unroll 1
                 for (int of = 16; of; of >>= 1) {
                     double x = __shfl_xor_sync(FULLW, mv, of);
                     mv = x < mv ? x : mv;
@@ -368,6 +387,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
             }
             __syncwarp();
             // block-parallel materialisation of the winner: take contributions + greedy fill
+            #pragma unroll 1
             for (int b = lane; b < nb; b += 32) {
                 const bool el = w.pu[b] + uu2 <= S.L && !(w.pm[b] + ff2 > S.cap_slack);
                 w.hi[o0 + b] = el ? w.bsz[o0 + b] : 0;
@@ -413,6 +433,7 @@ __device__ __forceinline__ void screen_options(const Spec& S, const Rows& R, Wal
             viable = false;
         } else {
             int lo = 0, hi = 0;
+            #pragma unroll 1
             for (int b = 0; b < nb && viable; ++b) {
                 const int s = w.bsz[o0 + b];
                 const bool el = w.pu[b] + uu <= S.L && !(w.pm[b] + ff > S.cap_slack);
@@ -520,6 +541,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                     o = w.vbase[j] + 32;
                 }
             } else {
+                #pragma unroll 1
                 for (; o < n; ++o) {
                     const int r = off + o;
                     const int t = opt_test(S, R, r, thr);
@@ -552,6 +574,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                 parent_stats_warp(S, R, w, j);
                 ps_lvl = j;
                 if (last) {
+                    #pragma unroll 1
                     for (int b = lane; b < nb; b += 32)
                         w.cm[b] = w.bmk[o0 + b] ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] +
                                                       (S.additive ? 0.0 : S.e3 * w.pP[b])
@@ -562,6 +585,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
             // per-block admissible take interval
             int mylo = 0, myhi = 0;
             bool mydead = false;
+            #pragma unroll 1
             for (int b = lane; b < nb; b += 32) {
                 const int s = w.bsz[o0 + b];
                 const bool el = w.pu[b] + uu <= S.L && !(w.pm[b] + ff > S.cap_slack);
@@ -617,6 +641,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                     const double tx = fm ? S.theta * (1.0 + 1e-12) : h.incumbent() * (1.0 - TIE_EPS);
                     int flo = 0, fhi = 0;
                     bool fdead = false;
+                    #pragma unroll 1
                     for (int b = lane; b < nb; b += 32) {
                         const int s = w.bsz[o0 + b];
                         const bool rok = fm ? w.cm[b] <= tx : w.cm[b] < tx;
@@ -641,6 +666,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                 }
                 double* rest = w.cs;
                 double* take = w.cb;
+                #pragma unroll 1
                 for (int b = lane; b < nb; b += 32) {
                     const unsigned m = w.bmk[o0 + b];
                     rest[b] = contrib(S, R, w.opt, m);
@@ -651,11 +677,13 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                     if (!(0.0 <= S.theta)) continue;
                     if (!last_feasible_warp(w, o0, nb, dd, S.theta, true, rest, take)) continue;
                     int mylo2 = 0;
+                    #pragma unroll 1
                     for (int b = lane; b < nb; b += 32)
                         mylo2 += (rest[b] <= S.theta) ? 0 : w.bsz[o0 + b];
                     const int rem0 = dd - wsum(mylo2);
                     int carry = 0;
                     double v = 0.0;
+                    #pragma unroll 1
                     for (int c = 0; c < nb; c += 32) {
                         const int b = c + lane;
                         int l = 0, room = 0;
@@ -690,6 +718,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                     double hiv = Ie;
                     while (true) {
                         double c = NEG_INF;
+                        #pragma unroll 1
                         for (int b = lane; b < nb; b += 32) {
                             if (rest[b] < hiv && rest[b] > c) c = rest[b];
                             if (w.hi[o0 + b] && take[b] < hiv && take[b] > c) c = take[b];
@@ -706,10 +735,12 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                         // materialise one allocation reaching v (greedy fill at hiv) so the
                         // planner can seed later FIRST probes with the argmin
                         int mylo3 = 0;
+                        #pragma unroll 1
                         for (int b = lane; b < nb; b += 32)
                             mylo3 += (rest[b] <= hiv) ? 0 : w.bsz[o0 + b];
                         const int rem0 = dd - wsum(mylo3);
                         int carry = 0;
+                        #pragma unroll 1
                         for (int c = 0; c < nb; c += 32) {
                             const int b = c + lane;
                             int l = 0, room = 0;
@@ -757,6 +788,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
         const int uu = R.u[r];
         const double ff = R.fp[r], bo = R.B[r], ba = R.base[r];
         int carry = 0;
+        #pragma unroll 1
         for (int c = 0; c < nb; c += 32) {
             const int b = c + lane;
             int xb = 0, s = 0, cnt = 0;
@@ -809,9 +841,11 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
         const double thr = h.thr(S);
         bool prune = false;
         // (when only the closed-form last level remains, its batch screen subsumes this)
+        #pragma unroll 1
         for (int l = j + 1; l < k && !prune && !(j + 1 == k - 1 && S.nonneg); ++l) {
             const int n = S.lvl_n[l], off = S.lvl_off[l];
             bool ok = false;
+            #pragma unroll 1
             for (int o = 0; o < n && !ok; ++o) {
                 const int rr = off + o;
                 const int t = opt_test(S, R, rr, thr);
@@ -820,6 +854,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                 const int d2 = R.d[rr], u2 = R.u[rr];
                 const double f2 = R.fp[rr], b2 = R.B[rr], a2 = R.base[rr];
                 int cnt = 0;
+                #pragma unroll 1
                 for (int b = lane; b < m; b += 32) {
                     if (w.cu[b] + u2 > S.L) continue;
                     if (w.cm[b] + f2 > S.cap_slack) continue;
@@ -861,6 +896,7 @@ __device__ __forceinline__ void load_cont_warp(const Cont& c, Walk& w, bool ance
     const int lane = lane_id();
     const int dep = c.depth;
     const int o = w.loff[dep];
+    #pragma unroll 1
     for (int b = lane; b < c.nb; b += 32) {
         w.bsz[o + b] = c.bsz[b];
         w.bmk[o + b] = c.bmk[b];
@@ -872,6 +908,7 @@ __device__ __forceinline__ void load_cont_warp(const Cont& c, Walk& w, bool ance
     }
     __syncwarp();
     if (lane == 0) {
+        #pragma unroll 1
         for (int l = 0; l < dep; ++l) w.opt[l] = c.opt[l];
         w.nb[dep] = c.nb;
         w.used[dep] = c.used;
@@ -881,10 +918,12 @@ __device__ __forceinline__ void load_cont_warp(const Cont& c, Walk& w, bool ance
         w.vbase[dep] = -1;
         if (c.ph) w.opt[dep] = (uint16_t)c.oc;
         // only FIRST needs them (hit paths compare every level); MIN skips the rebuild
+        #pragma unroll 1
         for (int l = ancestors ? dep - 1 : -1; l >= 0; --l) {
             const int oc1 = w.loff[l + 1], ol = w.loff[l];
             const unsigned bit = 1u << l;
             int nbl = 0;
+            #pragma unroll 1
             for (int b = 0; b < w.nb[l + 1];) {
                 const unsigned key = w.bmk[oc1 + b] & ~bit;
                 int size = 0, taken = 0;
@@ -911,6 +950,7 @@ __device__ __forceinline__ void store_cont_warp(const Walk& w, int l, int ph, Co
     const int lane = lane_id();
     const int o = w.loff[l];
     const int nb = w.nb[l];
+    #pragma unroll 1
     for (int b = lane; b < nb; b += 32) {
         c.bsz[b] = w.bsz[o + b];
         c.bmk[b] = w.bmk[o + b];
@@ -922,6 +962,7 @@ __device__ __forceinline__ void store_cont_warp(const Walk& w, int l, int ph, Co
     }
     if (lane == 0) {
         c.key = 0;
+        #pragma unroll 1
         for (int i = 0; i < MAXK; ++i) c.opt[i] = i < l ? w.opt[i] : 0;
         c.depth = (uint16_t)l;
         c.nb = (uint16_t)nb;

@@ -26,7 +26,7 @@ from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmosaic_gpu.so")
+LIB_PATH = os.environ.get("MOSAIC_LIB") or os.path.join(_HERE, "libmosaic_gpu.so")  # override: A/B runs
 
 MAX_STAGE_MODULES = 12
 MAX_GPUS = 1024
