@@ -844,27 +844,36 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
         #pragma unroll 1
         for (int l = j + 1; l < k && !prune && !(j + 1 == k - 1 && S.nonneg); ++l) {
             const int n = S.lvl_n[l], off = S.lvl_off[l];
+            // lanes over options (32 at a time), each lane scanning the m child blocks:
+            // "some option before the first stop (t == 2) passes opt_test and finds d2
+            // GPUs with room" — the same predicate as testing the options one by one
             bool ok = false;
             #pragma unroll 1
-            for (int o = 0; o < n && !ok; ++o) {
-                const int rr = off + o;
-                const int t = opt_test(S, R, rr, thr);
-                if (t == 2) break;
-                if (t == 1) continue;
-                const int d2 = R.d[rr], u2 = R.u[rr];
-                const double f2 = R.fp[rr], b2 = R.B[rr], a2 = R.base[rr];
-                int cnt = 0;
-                #pragma unroll 1
-                for (int b = lane; b < m; b += 32) {
-                    if (w.cu[b] + u2 > S.L) continue;
-                    if (w.cm[b] + f2 > S.cap_slack) continue;
-                    if (S.nonneg && S.include_self) {
-                        const double mb = w.cb[b] > a2 ? w.cb[b] : a2;
-                        if (mb + S.e1 + S.e2 * (w.cs[b] + b2) > thr) continue;
+            for (int c = 0; c < n && !ok; c += 32) {
+                const int o = c + lane;
+                const int t = o < n ? opt_test(S, R, off + o, thr) : 2;
+                const unsigned stop = __ballot_sync(FULLW, t == 2);
+                const int first_stop = stop ? __ffs(stop) - 1 : 32;
+                bool mine = false;
+                if (t == 0 && lane < first_stop) {
+                    const int rr = off + o;
+                    const int d2 = R.d[rr], u2 = R.u[rr];
+                    const double f2 = R.fp[rr], b2 = R.B[rr], a2 = R.base[rr];
+                    int cnt = 0;
+                    #pragma unroll 1
+                    for (int b = 0; b < m && cnt < d2; ++b) {
+                        if (w.cu[b] + u2 > S.L) continue;
+                        if (w.cm[b] + f2 > S.cap_slack) continue;
+                        if (S.nonneg && S.include_self) {
+                            const double mb = w.cb[b] > a2 ? w.cb[b] : a2;
+                            if (mb + S.e1 + S.e2 * (w.cs[b] + b2) > thr) continue;
+                        }
+                        cnt += w.bsz[o1 + b];
                     }
-                    cnt += w.bsz[o1 + b];
+                    mine = cnt >= d2;
                 }
-                ok = wsum(cnt) >= d2;
+                ok = wany(mine);
+                if (stop) break;
             }
             if (!ok) prune = true;
         }
