@@ -40,6 +40,8 @@ enum {
     MOSAIC_TOO_LARGE = 4,
     MOSAIC_CUDA = 5,
     MOSAIC_EMPTY = 6,
+    MOSAIC_BASELINE_INFEASIBLE = 7, /* InfeasibleBaselineError (simulator.hpp:127-129) */
+    MOSAIC_INVALID_ARGUMENT = 8,    /* std::invalid_argument (e.g. SimConfig checks) */
 };
 
 /* Kernel limits (a stage beyond them returns MOSAIC_TOO_LARGE, never a CPU path). */
@@ -149,6 +151,32 @@ int mosaic_gpu_validate_plan(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* e
                              const int32_t* gpus, const int64_t* stage_off, int64_t n_stages,
                              char* code_out, size_t code_cap);
 
+/* ---- N4: baselines and batched plan replay (simulator.hpp) ---- */
+/* SimConfig (simulator.hpp:28-35); the seed is per replay (seeds[] below). */
+typedef struct {
+    int32_t iterations;
+    int32_t stream_mode; /* 0 Pooled, 1 OnDemand */
+    double pooled_overhead, on_demand_overhead, perturbation_sigma;
+} mosaic_gpu_sim_config;
+
+/* TimelineInterval (simulator.hpp:37-43). */
+typedef struct {
+    int32_t gpu, module;
+    double start, end, quota;
+} mosaic_gpu_interval;
+
+/* simulate (simulator.hpp:68-119) of one plan (entries/gpus/stage_off as in
+ * mosaic_gpu_validate_plan) for n_seeds seeds at once, one device thread per seed.
+ * Outputs: iteration_time[n_seeds], per_stage[n_seeds * n_stages], busy[n_seeds * G],
+ * mean_busy[n_seeds] (any may be NULL); the timeline (first iteration of seeds[0]) is
+ * written to timeline[0 .. min(cap, *n_timeline)). */
+int mosaic_gpu_simulate(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* entries,
+                        const int32_t* gpus, const int64_t* stage_off, int64_t n_stages,
+                        const mosaic_gpu_sim_config* cfg, const uint64_t* seeds,
+                        int64_t n_seeds, double* iteration_time, double* per_stage,
+                        double* busy, double* mean_busy, mosaic_gpu_interval* timeline,
+                        int64_t timeline_cap, int64_t* n_timeline);
+
 /* Plan = ordered stages (DeploymentPlan, core.hpp:100-104). */
 #define MOSAIC_GPU_MAX_STAGES 64
 typedef struct {
@@ -168,6 +196,10 @@ typedef struct {
 int mosaic_gpu_plan_stage(mosaic_gpu_ctx* ctx, int stage, mosaic_gpu_stage_result* out);
 
 int mosaic_gpu_solve(mosaic_gpu_ctx* ctx, mosaic_gpu_plan_result* out);
+/* make_baseline_plan (simulator.hpp:283-313): policy 0 Megatron, 1 DistMM, full-quota
+ * options at the context's quota_levels.  Read the stages with mosaic_gpu_plan_stage.
+ * MOSAIC_BASELINE_INFEASIBLE mirrors InfeasibleBaselineError. */
+int mosaic_gpu_baseline_plan(mosaic_gpu_ctx* ctx, int policy, mosaic_gpu_plan_result* out);
 int mosaic_gpu_brute_force(mosaic_gpu_ctx* ctx, mosaic_gpu_plan_result* out);
 
 /* GAHC round trace: round r, candidate c -> (mask_x, mask_y, pruned, cache_hit, gain). */

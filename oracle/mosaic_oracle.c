@@ -79,6 +79,39 @@ static uint64_t mt_next(MT* m) {
     return y;
 }
 
+/* std::normal_distribution<double>(0,1) over mt19937_64, libstdc++ (bits/random.tcc):
+ * generate_canonical<double,53> = u / 2^64 (clamped below 1), polar method with the
+ * second variate cached; result * stddev + mean. */
+void mo_normals(uint64_t seed, int n, double* out) {
+    MT m;
+    mt_seed(&m, seed);
+    int avail = 0;
+    double saved = 0.0;
+    for (int i = 0; i < n; ++i) {
+        double ret;
+        if (avail) {
+            avail = 0;
+            ret = saved;
+        } else {
+            double x, y, r2;
+            do {
+                double c1 = (double)mt_next(&m) / 18446744073709551616.0;
+                if (c1 >= 1.0) c1 = 0x1.fffffffffffffp-1;
+                x = 2.0 * c1 - 1.0;
+                double c2 = (double)mt_next(&m) / 18446744073709551616.0;
+                if (c2 >= 1.0) c2 = 0x1.fffffffffffffp-1;
+                y = 2.0 * c2 - 1.0;
+                r2 = x * x + y * y;
+            } while (r2 > 1.0 || r2 == 0.0);
+            const double mult = sqrt(-2.0 * log(r2) / r2);
+            saved = x * mult;
+            avail = 1;
+            ret = y * mult;
+        }
+        out[i] = ret * 1.0 + 0.0;
+    }
+}
+
 /* ------------------------------------------------------------------ profiler.hpp */
 typedef struct {
     char id[32];

@@ -64,6 +64,11 @@ void mo_brute_force(mo_problem* p, mo_plan* out);  /* oracle.hpp:206-255 */
 /* allocation of stage s of the last plan */
 void mo_plan_stage(mo_problem* p, int s, mo_stage* out);
 
+/* n draws of std::normal_distribution<double>(0, 1) over std::mt19937_64(seed), libstdc++
+ * algorithm (Marsaglia polar over generate_canonical<double, 53>) as simulate() uses them
+ * (simulator.hpp:75-76, 89-91); the device replay kernel (sim.cu) restates the same. */
+void mo_normals(uint64_t seed, int n, double* out);
+
 #ifdef __cplusplus
 }
 #endif

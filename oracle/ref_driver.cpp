@@ -42,6 +42,7 @@ inline std::vector<int> probe_ok;
 #endif
 #include "mosaic/oracle.hpp"
 #include "mosaic/profiler.hpp"
+#include "mosaic/simulator.hpp"
 #include "mosaic/solver.hpp"
 #include "mosaic/stage_eval.hpp"
 
@@ -439,6 +440,59 @@ int main(int argc, char** argv) {
                                }};
             auto err = validate_plan(plan, in.graph, in.cluster, fo);
             std::printf("\"code\":\"%s\"", err ? to_string(err->code) : "Ok");
+        } else if (op == "baseline" || op == "simulate") {
+            // baseline megatron|distmm  (make_baseline_plan, simulator.hpp:283-313)
+            // simulate solve|megatron|distmm [iters=N] [sigma=S] [seed=X] [ondemand]
+            //   (simulate, simulator.hpp:68-119) on that plan
+            std::string which = pos.at(0);
+            SimConfig sc;
+            for (size_t i = 1; i < pos.size(); ++i) {
+                const std::string& a = pos[i];
+                if (a.rfind("iters=", 0) == 0) sc.iterations = std::atoi(a.c_str() + 6);
+                else if (a.rfind("sigma=", 0) == 0) sc.perturbation_sigma = std::strtod(a.c_str() + 6, nullptr);
+                else if (a.rfind("seed=", 0) == 0) sc.seed = std::strtoull(a.c_str() + 5, nullptr, 0);
+                else if (a == "ondemand") sc.stream_mode = StreamMode::OnDemand;
+            }
+            DeploymentPlan plan;
+            if (which == "solve") {
+                plan = solve(in.ctx, in.cluster, SolveConfig{L, 1e-3, prune, cache}).plan;
+            } else {
+                plan = make_baseline_plan(in.ctx, in.cluster,
+                                          which == "megatron" ? BaselinePolicy::Megatron
+                                                              : BaselinePolicy::DistMM,
+                                          L);
+            }
+            print_plan(plan);
+            std::printf("\"ok\":1");
+            if (op == "simulate") {
+                auto rep = simulate(in.ctx, in.cluster, plan, sc);
+                std::printf(",");
+                pd("sim_iteration_time", rep.iteration_time);
+                std::printf("\"per_stage\":[");
+                for (size_t i = 0; i < rep.per_stage_times.size(); ++i)
+                    std::printf("%s\"%a\"", i ? "," : "", rep.per_stage_times[i]);
+                std::printf("],\"busy\":[");
+                for (size_t i = 0; i < rep.per_gpu_busy_fraction.size(); ++i)
+                    std::printf("%s\"%a\"", i ? "," : "", rep.per_gpu_busy_fraction[i]);
+                std::printf("],");
+                pd("mean_busy", rep.mean_busy_fraction, false);
+                std::printf(",\"timeline\":[");
+                for (size_t i = 0; i < rep.timeline.size(); ++i) {
+                    const auto& t = rep.timeline[i];
+                    std::printf("%s[%d,%d,\"%a\",\"%a\",\"%a\"]", i ? "," : "", t.gpu, t.module,
+                                t.start, t.end, t.quota);
+                }
+                std::printf("]");
+            }
+        } else if (op == "normals") {
+            // normals SEED N: std::normal_distribution<double>(0,1) over std::mt19937_64(SEED)
+            // exactly as simulate() draws them (simulator.hpp:75-76, 89-91)
+            std::mt19937_64 rng(std::strtoull(pos.at(0).c_str(), nullptr, 0));
+            std::normal_distribution<double> gauss(0.0, 1.0);
+            const int n = std::atoi(pos.at(1).c_str());
+            std::printf("\"normals\":[");
+            for (int i = 0; i < n; ++i) std::printf("%s\"%a\"", i ? "," : "", gauss(rng));
+            std::printf("]");
         } else if (op == "partitions") {
             auto parts = enumerate_partitions(in.graph);
             std::printf("\"count\":%zu", parts.size());

@@ -54,6 +54,7 @@ def lib():
         for f in (L.mo_solve, L.mo_brute_force):
             f.argtypes = [C.c_void_p, C.POINTER(Plan)]
         L.mo_plan_stage.argtypes = [C.c_void_p, C.c_int, C.POINTER(Stage)]
+        L.mo_normals.argtypes = [C.c_uint64, C.c_int, C.POINTER(C.c_double)]
         _lib = L
     return _lib
 
@@ -153,3 +154,10 @@ class Problem:
 def stage_eval(spec: str, levels: int, modules) -> dict | None:
     r = Problem(spec, levels).stage_eval(sum(1 << m for m in modules))
     return r if r["status"] == 0 else None
+
+
+def normals(seed: int, n: int) -> list[float]:
+    """std::normal_distribution<double>(0,1) over std::mt19937_64(seed), restated in C."""
+    out = (C.c_double * n)()
+    lib().mo_normals(seed, n, out)
+    return list(out)

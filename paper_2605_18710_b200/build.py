@@ -20,10 +20,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX_HOST", "g++")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["engine.cu", "pack.cu"]
+CU_SOURCES = ["engine.cu", "pack.cu", "sim.cu"]
 CPP_SOURCES = ["model.cpp", "planner.cpp", "capi.cpp"]
 HEADERS = ["engine.hpp", "search_core.cuh", "search_warp.cuh", "spec_build.hpp", "model.hpp",
-           "planner.hpp", "pack.hpp"]
+           "planner.hpp", "pack.hpp", "sim.hpp"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:

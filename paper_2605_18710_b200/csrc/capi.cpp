@@ -1,4 +1,5 @@
 // capi.cpp — extern "C" boundary (include/mosaic_gpu.h).  No exception crosses it.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -28,6 +29,9 @@ int guard(F&& f) {
     } catch (const Error& e) {
         g_err = e.what();
         return e.status;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return MOSAIC_INVALID_ARGUMENT;
     } catch (const RangeError& e) {
         g_err = e.what();
         return MOSAIC_RANGE;
@@ -279,6 +283,53 @@ int mosaic_gpu_solve(mosaic_gpu_ctx* ctx, mosaic_gpu_plan_result* out) {
         ctx->plan = ctx->pl->solve();
         fill_plan(ctx->plan, out);
         return ctx->plan.status;
+    });
+}
+
+int mosaic_gpu_baseline_plan(mosaic_gpu_ctx* ctx, int policy, mosaic_gpu_plan_result* out) {
+    return guard([&] {
+        if (policy != 0 && policy != 1) throw Error(MOSAIC_INVALID_ARGUMENT, "policy");
+        ctx->plan = ctx->pl->baseline_plan(policy);
+        fill_plan(ctx->plan, out);
+        return ctx->plan.status;
+    });
+}
+
+int mosaic_gpu_simulate(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* entries,
+                        const int32_t* gpus, const int64_t* stage_off, int64_t n_stages,
+                        const mosaic_gpu_sim_config* cfg, const uint64_t* seeds,
+                        int64_t n_seeds, double* iteration_time, double* per_stage,
+                        double* busy, double* mean_busy, mosaic_gpu_interval* timeline,
+                        int64_t timeline_cap, int64_t* n_timeline) {
+    return guard([&] {
+        std::vector<std::vector<Entry>> st(n_stages);
+        for (int64_t s = 0; s < n_stages; ++s)
+            for (int64_t e = stage_off[s]; e < stage_off[s + 1]; ++e) {
+                const auto& E = entries[e];
+                Entry x{E.module, E.dp_degree, E.quota_units, {}};
+                x.gpus.assign(gpus + E.gpu_off, gpus + E.gpu_off + E.n_gpus);
+                st[s].push_back(std::move(x));
+            }
+        mg::SimCfg c;
+        c.iterations = cfg->iterations;
+        c.on_demand = cfg->stream_mode != 0;
+        c.pooled_overhead = cfg->pooled_overhead;
+        c.on_demand_overhead = cfg->on_demand_overhead;
+        c.sigma = cfg->perturbation_sigma;
+        std::vector<uint64_t> sd(seeds, seeds + n_seeds);
+        std::vector<double> it, ps, bz, mb;
+        std::vector<mg::SimInterval> tl;
+        ctx->pl->simulate(st, c, sd, it, ps, bz, mb, timeline || n_timeline ? &tl : nullptr);
+        if (iteration_time) std::copy(it.begin(), it.end(), iteration_time);
+        if (per_stage) std::copy(ps.begin(), ps.end(), per_stage);
+        if (busy) std::copy(bz.begin(), bz.end(), busy);
+        if (mean_busy) std::copy(mb.begin(), mb.end(), mean_busy);
+        if (n_timeline) *n_timeline = (int64_t)tl.size();
+        if (timeline)
+            for (int64_t i = 0; i < (int64_t)tl.size() && i < timeline_cap; ++i)
+                timeline[i] = mosaic_gpu_interval{tl[i].gpu, tl[i].module, tl[i].start,
+                                                  tl[i].end, tl[i].quota};
+        return MOSAIC_OK;
     });
 }
 

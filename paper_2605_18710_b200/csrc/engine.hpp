@@ -33,6 +33,7 @@ struct EvalEntry {  // device evaluator input (one per allocation entry)
 class Engine {
   public:
     explicit Engine(int device);
+    int device() const { return device_; }
     ~Engine();
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;

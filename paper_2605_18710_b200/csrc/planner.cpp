@@ -740,3 +740,238 @@ void Planner::stage_time(const std::vector<std::vector<Entry>>& allocs, std::vec
 }
 
 }  // namespace mosaic_b200
+
+// ---------------------------------------------------------------------------
+// N4: exclusive-allocation baselines and batched plan replay (simulator.hpp)
+// ---------------------------------------------------------------------------
+namespace mosaic_b200 {
+
+// rectified_latency of module m alone on d GPUs at full quota (perf_model.hpp:442-464 with a
+// single resident per GPU: sum = 0 + b, prod = 1 * b; no residents when include_self is off)
+double Planner::exclusive_latency(int m, int d) const {
+    const Surface& s = P_.modules[m].surface;
+    const double a = (double)P_.quota_levels / P_.quota_levels;
+    const double base = s.lookup(d, a).latency;
+    double sum = 0.0, prod = 1.0;
+    if (P_.include_self) {
+        const double b = s.lookup(1, a).bandwidth_util;
+        sum += b;
+        prod *= b;
+    } else {
+        prod = 0.0;
+    }
+    const double dl = P_.im.delta(sum, prod);
+    const double worst = std::max(-1e300, dl);
+    return base + worst;
+}
+
+// detail::dependency_waves, simulator.hpp:144-193
+std::vector<std::vector<int>> Planner::dependency_waves() const {
+    const int n = (int)P_.modules.size(), G = P_.gpu_count;
+    const std::vector<int> topo = topological_order(P_);
+    std::vector<int> depth(n, 0);
+    for (int u : topo)
+        for (auto [a, b] : P_.edges)
+            if (a == u) depth[b] = std::max(depth[b], depth[u] + 1);
+    int max_depth = 0;
+    for (int d : depth) max_depth = std::max(max_depth, d);
+    std::vector<std::vector<int>> waves;
+    for (int lvl = 0; lvl <= max_depth; ++lvl) {
+        std::vector<int> level;
+        for (int m : topo)
+            if (depth[m] == lvl) level.push_back(m);
+        if (level.empty()) continue;
+        const int wave_count = ((int)level.size() + G - 1) / G;
+        std::vector<std::pair<double, int>> load;
+        for (int m : level) {
+            const Surface& s = P_.modules[m].surface;
+            load.push_back({s.lookup(s.min_d(), s.max_a()).latency, m});
+        }
+        std::sort(load.begin(), load.end(), [](const auto& x, const auto& y) {
+            if (x.first != y.first) return x.first > y.first;
+            return x.second < y.second;
+        });
+        std::vector<std::vector<int>> split(wave_count);
+        std::vector<double> totals(wave_count, 0.0);
+        for (const auto& [lat, m] : load) {
+            int target = 0;
+            for (int w = 1; w < wave_count; ++w) {
+                if ((int)split[w].size() >= G) continue;
+                if ((int)split[target].size() >= G || totals[w] < totals[target]) target = w;
+            }
+            split[target].push_back(m);
+            totals[target] += lat;
+        }
+        for (auto& wv : split) {
+            std::sort(wv.begin(), wv.end());
+            waves.push_back(std::move(wv));
+        }
+    }
+    return waves;
+}
+
+// detail::distmm_wave, simulator.hpp:217-279.  The reference enumerates every composition
+// (d_0..d_k-1) of at most G GPUs in ascending lexicographic order and keeps the first with
+// the smallest wave time.  With every module exclusive on its own GPUs the wave time is
+// max(0, max_i f_i(d_i)), f_i = exclusive_latency, so that first minimiser is closed-form:
+// T* = the smallest threshold t for which the per-module minimal admissible degrees
+// m_i(t) = min{d : degree_ok, f_i(d) <= t} fit in G GPUs, and the lexicographically first
+// composition reaching T* is (m_0(T*), ..., m_k-1(T*)).  The k > 8 greedy is restated.
+std::vector<Entry> Planner::distmm_wave(const std::vector<int>& wave) const {
+    const int k = (int)wave.size(), G = P_.gpu_count, L = P_.quota_levels;
+    const int max_d = P_.modules[wave[0]].surface.max_d();
+    const double a = (double)L / L;
+    auto degree_ok = [&](int m, int d) {
+        const Surface& s = P_.modules[m].surface;
+        if (d > s.max_d()) return false;
+        return s.lookup(d, a).memory + P_.modules[m].memory_base <= P_.memory_capacity;
+    };
+    for (int i = 0; i < k; ++i)
+        if (!degree_ok(wave[i], 1))
+            throw Error(BASELINE_INFEASIBLE, "module " + P_.modules[wave[i]].id +
+                                                 " does not fit one GPU at full quota");
+    auto wave_time = [&](const std::vector<int>& deg) {
+        double worst = 0.0;
+        for (int i = 0; i < k; ++i) worst = std::max(worst, exclusive_latency(wave[i], deg[i]));
+        return worst;
+    };
+    std::vector<int> degrees(k, 1);
+    if (k <= 8) {
+        const int dmax = std::min(max_d, G - (k - 1));
+        std::vector<std::vector<double>> f(k, std::vector<double>(dmax + 1, 0.0));
+        std::vector<std::vector<char>> ok(k, std::vector<char>(dmax + 1, 0));
+        std::vector<double> cand{0.0};
+        for (int i = 0; i < k; ++i)
+            for (int d = 1; d <= dmax; ++d)
+                if (degree_ok(wave[i], d)) {
+                    ok[i][d] = 1;
+                    f[i][d] = exclusive_latency(wave[i], d);
+                    cand.push_back(f[i][d]);
+                }
+        auto minimal = [&](double t, std::vector<int>* out) {
+            int used = 0;
+            for (int i = 0; i < k; ++i) {
+                int m = 0;
+                for (int d = 1; d <= dmax && !m; ++d)
+                    if (ok[i][d] && !(f[i][d] > t)) m = d;
+                if (!m) return false;
+                used += m;
+                if (out) (*out)[i] = m;
+            }
+            return used <= G;
+        };
+        std::sort(cand.begin(), cand.end());
+        cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+        // feasibility is monotone in t; thresholds below 0 collapse to 0 (wave_time's clamp)
+        size_t lo = 0, hi = cand.size();
+        while (lo < hi) {
+            const size_t mid = (lo + hi) / 2;
+            if (minimal(std::max(0.0, cand[mid]), nullptr)) hi = mid; else lo = mid + 1;
+        }
+        if (lo == cand.size()) throw Error(BASELINE_INFEASIBLE, "no DistMM composition fits");
+        minimal(std::max(0.0, cand[lo]), &degrees);
+    } else {
+        int used = k;
+        while (used < G) {
+            const double cur_time = wave_time(degrees);
+            std::vector<std::pair<double, int>> lat(k);
+            for (int i = 0; i < k; ++i) lat[i] = {exclusive_latency(wave[i], degrees[i]), i};
+            std::sort(lat.rbegin(), lat.rend());
+            const int worst = lat[0].second;
+            std::vector<int> trial = degrees;
+            trial[worst]++;
+            if (trial[worst] > max_d || !degree_ok(wave[worst], trial[worst])) break;
+            if (wave_time(trial) >= cur_time) break;
+            degrees = trial;
+            ++used;
+        }
+    }
+    std::vector<Entry> out;
+    int next = 0;
+    for (int i = 0; i < k; ++i) {
+        Entry e{wave[i], degrees[i], L, {}};
+        for (int g = 0; g < degrees[i]; ++g) e.gpus.push_back(next + g);
+        next += degrees[i];
+        out.push_back(std::move(e));
+    }
+    std::sort(out.begin(), out.end(), [](const Entry& x, const Entry& y) { return x.module < y.module; });
+    return out;
+}
+
+PlanResult Planner::baseline_plan(int policy) {
+    const int G = P_.gpu_count, L = P_.quota_levels;
+    std::vector<std::vector<Entry>> stages;
+    if (policy == 0) {  // Megatron: every module alone on all GPUs, topological order
+        for (int m : topological_order(P_)) {
+            const Surface& s = P_.modules[m].surface;
+            if (G > s.max_d())
+                throw Error(BASELINE_INFEASIBLE, "gpu_count exceeds profiled DP range");
+            const double a = (double)L / L;
+            if (s.lookup(G, a).memory + P_.modules[m].memory_base > P_.memory_capacity)
+                throw Error(BASELINE_INFEASIBLE, "module " + P_.modules[m].id +
+                                                     " exceeds GPU memory at forced degree");
+            Entry e{m, G, L, {}};
+            for (int g = 0; g < G; ++g) e.gpus.push_back(g);
+            stages.push_back({e});
+        }
+    } else {
+        for (const auto& wave : dependency_waves()) stages.push_back(distmm_wave(wave));
+    }
+    std::vector<double> st;
+    std::vector<std::vector<double>> rect;
+    stage_time(stages, st, rect);
+    PlanResult pr;
+    pr.status = OK;
+    for (size_t i = 0; i < stages.size(); ++i) {
+        StageResult r;
+        r.status = OK;
+        r.stage_time = st[i];
+        r.entries = stages[i];
+        uint64_t mask = 0;
+        for (const auto& e : stages[i]) mask |= uint64_t(1) << e.module;
+        pr.masks.push_back(mask);
+        pr.stages.push_back(std::move(r));
+        pr.iteration_time += st[i];
+    }
+    return pr;
+}
+
+void Planner::simulate(const std::vector<std::vector<Entry>>& stages, const mg::SimCfg& cfg,
+                       const std::vector<uint64_t>& seeds, std::vector<double>& iter,
+                       std::vector<double>& per_stage, std::vector<double>& busy,
+                       std::vector<double>& mean_busy, std::vector<mg::SimInterval>* timeline) {
+    if (cfg.iterations < 1) throw Error(INVALID_ARGUMENT, "iterations must be >= 1");
+    if (cfg.pooled_overhead < 0 || cfg.on_demand_overhead < 0)
+        throw Error(INVALID_ARGUMENT, "overheads must be >= 0");
+    std::vector<double> st;
+    std::vector<std::vector<double>> rect;
+    stage_time(stages, st, rect);  // rectified latencies of every entry, on the device
+    std::vector<mg::SimEntry> ents;
+    std::vector<int> gpus, off{0};
+    for (size_t s = 0; s < stages.size(); ++s) {
+        for (size_t i = 0; i < stages[s].size(); ++i) {
+            const Entry& e = stages[s][i];
+            // rectified_latency(ctx, stage, e.module) looks the module up with find():
+            // its first entry in the stage
+            size_t first = i;
+            for (size_t j = 0; j < i; ++j)
+                if (stages[s][j].module == e.module) { first = j; break; }
+            const double q = (double)e.units / P_.quota_levels;
+            const Sample smp = P_.modules[e.module].surface.lookup(e.d, q);
+            mg::SimEntry se{};
+            se.dur0 = rect[s][first];
+            se.quota = q;
+            se.active_cap = smp.sm_active * smp.latency;
+            se.module = e.module;
+            se.gpu_off = (int)gpus.size();
+            se.n_gpus = (int)e.gpus.size();
+            ents.push_back(se);
+            gpus.insert(gpus.end(), e.gpus.begin(), e.gpus.end());
+        }
+        off.push_back((int)ents.size());
+    }
+    mg::simulate_device(ents, gpus, off, P_.gpu_count, cfg, seeds, eng_->device(), iter,
+                        per_stage, busy, mean_busy, timeline);
+}
+
+}  // namespace mosaic_b200

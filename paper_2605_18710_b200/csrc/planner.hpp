@@ -19,12 +19,13 @@
 #include <vector>
 
 #include "engine.hpp"
+#include "sim.hpp"
 #include "model.hpp"
 
 namespace mosaic_b200 {
 
 enum Status { OK = 0, INFEASIBLE = 1, MODULE_NO_OPTION = 2, RANGE = 3, TOO_LARGE = 4,
-              CUDA = 5, EMPTY = 6 };
+              CUDA = 5, EMPTY = 6, BASELINE_INFEASIBLE = 7, INVALID_ARGUMENT = 8 };
 
 struct Error : std::runtime_error {
     int status;
@@ -88,6 +89,15 @@ class Planner {
     void stage_time(const std::vector<std::vector<Entry>>& allocs, std::vector<double>& st,
                     std::vector<std::vector<double>>& rect);
 
+    // make_baseline_plan (simulator.hpp:283-313): policy 0 Megatron, 1 DistMM; full-quota
+    // options at this problem's quota_levels; stage times from the device evaluator
+    PlanResult baseline_plan(int policy);
+    // simulate (simulator.hpp:68-119) of a plan for many seeds on the device (sim.cu)
+    void simulate(const std::vector<std::vector<Entry>>& stages, const mg::SimCfg& cfg,
+                  const std::vector<uint64_t>& seeds, std::vector<double>& iter,
+                  std::vector<double>& per_stage, std::vector<double>& busy,
+                  std::vector<double>& mean_busy, std::vector<mg::SimInterval>* timeline);
+
     mg::Engine& engine() { return *eng_; }
     void clear_cache() { cache_.clear(); }
 
@@ -98,6 +108,9 @@ class Planner {
                     double seed_value = 0.0);
     double min_value(const std::vector<int>& mods, double ub, mg::SearchStats& st,
                      std::vector<Entry>* argmin = nullptr);
+    double exclusive_latency(int m, int d) const;
+    std::vector<Entry> distmm_wave(const std::vector<int>& wave) const;
+    std::vector<std::vector<int>> dependency_waves() const;
     bool make_seed(const std::vector<Entry>& ents, const std::vector<int>& order, bool filter,
                    double theta, double value, mg::HitPath& hp, mg::Leaf& lf) const;
     std::vector<Entry> leaf_entries(const std::vector<int>& order, const mg::Leaf& lf) const;

@@ -418,6 +418,19 @@ __device__ __forceinline__ void screen_options(const Spec& S, const Rows& R, Wal
     const int o = start + lane;
     const int o0 = w.loff[j], nb = w.nb[j];
     const int off = S.lvl_off[j];
+    // option-independent bound of the blocks the option would leave alone, once per block
+    // (-inf where no module resides yet); lives in the composition scan scratch (sa|sb),
+    // which is free between compositions
+    double* lbrv = reinterpret_cast<double*>(w.sa);
+    if (S.nonneg) {
+        #pragma unroll 1
+        for (int b = lane; b < nb; b += 32)
+            lbrv[b] = !w.bmk[o0 + b] ? NEG_INF
+                      : S.include_self
+                          ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] + envelope(S, j + 1, w.pP[b])
+                          : w.pmx[b] + S.e1 + S.e2 * w.psum[b] + envelope(S, j + 1, 0.0);
+        __syncwarp();
+    }
     const int t = o < n ? opt_test(S, R, off + o, thr) : 2;
     const unsigned brk = __ballot_sync(FULLW, t == 2);
     const int first_brk = brk ? __ffs(brk) - 1 : 32;
@@ -452,14 +465,7 @@ __device__ __forceinline__ void screen_options(const Spec& S, const Rows& R, Wal
                         }
                         tok = !(lbt > thr);
                     }
-                    if (w.bmk[o0 + b]) {
-                        const double lbr = S.include_self
-                                               ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] +
-                                                     envelope(S, j + 1, w.pP[b])
-                                               : w.pmx[b] + S.e1 + S.e2 * w.psum[b] +
-                                                     envelope(S, j + 1, 0.0);
-                        rok = !(lbr > thr);
-                    }
+                    rok = !(lbrv[b] > thr);
                 }
                 if (rok) {
                     if (tok) hi += s;

@@ -33,7 +33,8 @@ MAX_GPUS = 1024
 MAX_STAGES = 64
 MAX_MODULES = 64
 
-OK, INFEASIBLE, MODULE_NO_OPTION, RANGE, TOO_LARGE, CUDA, EMPTY = range(7)
+(OK, INFEASIBLE, MODULE_NO_OPTION, RANGE, TOO_LARGE, CUDA, EMPTY, BASELINE_INFEASIBLE,
+ INVALID_ARGUMENT) = range(9)
 
 
 class MosaicError(RuntimeError):
@@ -54,6 +55,14 @@ class OracleTooLargeError(MosaicError):
 
 class EmptyPlanError(MosaicError):
     """solver.hpp:25."""
+
+
+class InfeasibleBaselineError(MosaicError):
+    """simulator.hpp:127-129 InfeasibleBaselineError."""
+
+
+class InvalidArgumentError(MosaicError, ValueError):
+    """std::invalid_argument (e.g. SimConfig checks, simulator.hpp:70-73)."""
 
 
 class DeviceError(MosaicError):
@@ -80,6 +89,17 @@ class ClusterC(C.Structure):
     _fields_ = [("gpu_count", C.c_int32), ("memory_capacity", C.c_double),
                 ("peak_compute", C.c_double), ("peak_bandwidth", C.c_double),
                 ("interconnect_alpha", C.c_double), ("interconnect_beta", C.c_double)]
+
+
+class SimConfigC(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("stream_mode", C.c_int32),
+                ("pooled_overhead", C.c_double), ("on_demand_overhead", C.c_double),
+                ("perturbation_sigma", C.c_double)]
+
+
+class IntervalC(C.Structure):
+    _fields_ = [("gpu", C.c_int32), ("module", C.c_int32), ("start", C.c_double),
+                ("end", C.c_double), ("quota", C.c_double)]
 
 
 class ModuleC(C.Structure):
@@ -138,6 +158,7 @@ EXPORTS = [
     "mosaic_gpu_own_launches", "mosaic_gpu_ksearch_ms", "mosaic_gpu_ksearch_launches",
     "mosaic_gpu_h2d_bytes", "mosaic_gpu_d2h_bytes", "mosaic_gpu_mark", "mosaic_gpu_marked_ms", "mosaic_gpu_alg_bytes", "mosaic_gpu_stage_min",
     "mosaic_gpu_validate_plan", "mosaic_gpu_generate_surfaces", "mosaic_gpu_synth_workloads",
+    "mosaic_gpu_baseline_plan", "mosaic_gpu_simulate",
 ]
 
 _lib = None
@@ -199,6 +220,12 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                                    P(C.c_int32), P(C.c_int32)]),
         "mosaic_gpu_synth_workloads": (C.c_int, [C.c_char_p, P(WorkloadC), C.c_int32,
                                                  P(C.c_int32), P(ClusterC)]),
+        "mosaic_gpu_baseline_plan": (C.c_int, [vp, C.c_int, P(PlanResultC)]),
+        "mosaic_gpu_simulate": (C.c_int, [vp, P(EvalEntryC), P(C.c_int32), P(C.c_int64),
+                                          C.c_int64, P(SimConfigC), P(C.c_uint64), C.c_int64,
+                                          P(C.c_double), P(C.c_double), P(C.c_double),
+                                          P(C.c_double), P(IntervalC), C.c_int64,
+                                          P(C.c_int64)]),
         "mosaic_gpu_validate_plan": (C.c_int, [vp, P(EvalEntryC), P(C.c_int32), P(C.c_int64),
                                                C.c_int64, C.c_char_p, C.c_size_t]),
     }
@@ -215,7 +242,9 @@ def _raise(code: int) -> None:
         return
     msg = load_library().mosaic_gpu_last_error().decode()
     exc = {MODULE_NO_OPTION: StageInfeasibleError, RANGE: SurfaceRangeError,
-           TOO_LARGE: OracleTooLargeError, EMPTY: EmptyPlanError}.get(code, DeviceError)
+           TOO_LARGE: OracleTooLargeError, EMPTY: EmptyPlanError,
+           BASELINE_INFEASIBLE: InfeasibleBaselineError,
+           INVALID_ARGUMENT: InvalidArgumentError}.get(code, DeviceError)
     raise exc(msg or f"status {code}")
 
 
@@ -521,6 +550,52 @@ class Planner:
             return list(st[:n]), [list(rect[off[i]:off[i + 1]]) for i in range(n)]
         return list(st[:n])
 
+    def make_baseline_plan(self, policy: str) -> "DeploymentPlan":
+        """make_baseline_plan (simulator.hpp:283-313): 'megatron' or 'distmm', full-quota
+        options; raises InfeasibleBaselineError like the reference."""
+        pol = {"megatron": 0, "distmm": 1}[policy.lower()]
+        pr = PlanResultC()
+        _raise(load_library().mosaic_gpu_baseline_plan(self._ctx, pol, C.byref(pr)))
+        return self._plan(pr)
+
+    def simulate(self, plan: "DeploymentPlan", config: Optional["SimConfig"] = None,
+                 seeds: Optional[Sequence[int]] = None) -> list["SimulationReport"]:
+        """simulate (simulator.hpp:68-119) of `plan` on the device, one report per seed
+        (default: [config.seed]); the timeline is filled for the first seed only."""
+        cfg = config or SimConfig()
+        seeds = list(seeds) if seeds is not None else [cfg.seed]
+        ents, gpus, off = [], [], [0]
+        for st in plan.stages:
+            for e in st.entries:
+                ents.append(EvalEntryC(e.module, e.option.dp_degree, e.option.quota_units,
+                                       len(e.gpus), len(gpus)))
+                gpus.extend(e.gpus)
+            off.append(len(ents))
+        n, S, G = len(seeds), len(plan.stages), self.gpu_count
+        E = (EvalEntryC * max(1, len(ents)))(*ents)
+        Gp = (C.c_int32 * max(1, len(gpus)))(*gpus)
+        O = (C.c_int64 * len(off))(*off)
+        sc = SimConfigC(cfg.iterations, 1 if cfg.stream_mode == "on_demand" else 0,
+                        cfg.pooled_overhead, cfg.on_demand_overhead, cfg.perturbation_sigma)
+        sd = (C.c_uint64 * max(1, n))(*[s & (2**64 - 1) for s in seeds])
+        it = (C.c_double * max(1, n))()
+        ps = (C.c_double * max(1, n * S))()
+        bz = (C.c_double * max(1, n * G))()
+        mb = (C.c_double * max(1, n))()
+        tl = (IntervalC * max(1, len(gpus)))()
+        ntl = C.c_int64()
+        _raise(load_library().mosaic_gpu_simulate(self._ctx, E, Gp, O, S, C.byref(sc), sd, n, it,
+                                                  ps, bz, mb, tl, len(gpus), C.byref(ntl)))
+        out = []
+        for i in range(n):
+            rep = SimulationReport(it[i], list(ps[i * S:(i + 1) * S]),
+                                   list(bz[i * G:(i + 1) * G]), mb[i], [])
+            if i == 0:
+                rep.timeline = [TimelineInterval(x.gpu, x.module, x.start, x.end, x.quota)
+                                for x in tl[:ntl.value]]
+            out.append(rep)
+        return out
+
     def validate_plan(self, plan: "DeploymentPlan") -> tuple[str, str]:
         """validate_plan (core.hpp:281-351) -> (ValidationCode name, message)."""
         ents, gpus, off = [], [], [0]
@@ -633,6 +708,36 @@ def merge_records(records: bytes, world: int, mode: int) -> int:
 # ---------------------------------------------------------------------------
 # N2: input generation on the device (profiler.hpp)
 # ---------------------------------------------------------------------------
+@dataclass
+class SimConfig:
+    """SimConfig (simulator.hpp:28-35); stream_mode 'pooled' or 'on_demand'."""
+    iterations: int = 1
+    stream_mode: str = "pooled"
+    pooled_overhead: float = 0.013e-3
+    on_demand_overhead: float = 37e-3
+    perturbation_sigma: float = 0.0
+    seed: int = 0
+
+
+@dataclass
+class TimelineInterval:
+    gpu: int
+    module: int
+    start: float
+    end: float
+    quota: float
+
+
+@dataclass
+class SimulationReport:
+    """SimulationReport (simulator.hpp:45-55)."""
+    iteration_time: float
+    per_stage_times: list
+    per_gpu_busy_fraction: list
+    mean_busy_fraction: float
+    timeline: list
+
+
 @dataclass
 class ModuleWorkload:
     """ModuleWorkload (profiler.hpp:26-40)."""

@@ -246,8 +246,36 @@ def validate() -> None:
     dump("validate.json", out)
 
 
+def simulate() -> None:
+    """N4: make_baseline_plan (Megatron / DistMM) and simulate() of the reference."""
+    out = []
+    insts = [("cfg1", []), ("cfg2", []), ("cfg3", []), ("cfg4", []),
+             ("preset:imagebind:7:8", []), ("preset:ofasys:10:16", []),
+             ("random:3:4:32", ["levels=8"]), ("random:7:5:16", ["mem=6e9"])]
+    # 12 modules on 16 GPUs: dependency waves wider than 8 take the greedy branch (no solve:
+    # the reference GAHC is too slow there)
+    insts += [(f"random:{sd}:12:16", ["nosolve"]) for sd in (1, 2, 3, 4, 5, 6)]
+    for inst, extra in insts:
+        nosolve = "nosolve" in extra
+        extra = [x for x in extra if x != "nosolve"]
+        for pol in ("megatron", "distmm"):
+            out.append({"inst": inst, "extra": extra, "op": "baseline", "policy": pol,
+                        "r": ref(inst, "baseline", pol, *extra)})
+        for which, cfg in [("solve", []), ("solve", ["iters=5", "sigma=0.1", "seed=11"]),
+                           ("megatron", ["ondemand", "iters=2"]),
+                           ("distmm", ["iters=3", "sigma=0.05", "seed=9"]),
+                           ("solve", ["iters=7", "sigma=0.3", "seed=123456789", "ondemand"])]:
+            if nosolve and which == "solve":
+                continue
+            out.append({"inst": inst, "extra": extra, "op": "simulate", "policy": which,
+                        "cfg": cfg, "r": ref(inst, "simulate", which, *cfg, *extra)})
+    dump("simulate.json", out)
+    dump("normals.json", [ref("cfg1", "normals", str(sd), "400")
+                          for sd in (0, 7, 11, 123456789, 2**64 - 1)])
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["configs", "cfg5_stages", "random_sets", "presets", "variants",
-                             "stime", "io_files", "validate"]
+                             "stime", "io_files", "validate", "simulate"]
     for w in which:
         globals()[w]()
