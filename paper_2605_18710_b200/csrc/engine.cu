@@ -403,6 +403,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* e = std::getenv("MOSAIC_BACKOFF_NS")) backoff_cap_ = std::atoi(e);
     if (const char* e = std::getenv("MOSAIC_SMALL_TREE")) small_tree_ = std::atof(e);
     if (const char* e = std::getenv("MOSAIC_DEEP_AFTER")) deep_after_ = std::atoll(e);
+    if (const char* e = std::getenv("MOSAIC_LOOKAHEAD")) lookahead_ = std::atoi(e);
     CK(cudaSetDevice(device));
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -533,6 +534,7 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     // long-running pieces may also hand over levels <= k-3 (see WarpHooks::abort)
     hs->don_max_level_tail = S.k - 3 > hs->don_max_level ? S.k - 3 : hs->don_max_level;
     hs->deep_after = deep_after_;
+    hs->lookahead = lookahead_;
     hs->don_period = don_period_;
     hs->backoff_cap_ns = backoff_cap_;
     std::memset(hc, 0, sizeof(Ctl));

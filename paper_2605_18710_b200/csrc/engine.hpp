@@ -107,6 +107,9 @@ class Engine {
     int backoff_cap_ = 2048;  // ns, idle walkers polling back-off cap (measured)
     double small_tree_ = 2e5;  // option tuples x G below which 8 CTAs run the search
     unsigned long long ticket_base_ = 0;
+    // child look-ahead (can every remaining level still place an option?): off by default —
+    // the lane-parallel option screen at the next level does the same job for less
+    int lookahead_ = 0;
     long long deep_after_ = 4096;  // steps on one piece before deeper hand-overs are allowed
     long long front_cap_ = 0;
     void* h_pin_ = nullptr;

@@ -848,7 +848,9 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
         bool prune = false;
         // (when only the closed-form last level remains, its batch screen subsumes this)
         #pragma unroll 1
-        for (int l = j + 1; l < k && !prune && !(j + 1 == k - 1 && S.nonneg); ++l) {
+        for (int l = j + 1; l < k && l <= j + S.lookahead && !prune &&
+                            !(j + 1 == k - 1 && S.nonneg);
+             ++l) {
             const int n = S.lvl_n[l], off = S.lvl_off[l];
             // lanes over options (32 at a time), each lane scanning the m child blocks:
             // "some option before the first stop (t == 2) passes opt_test and finds d2
