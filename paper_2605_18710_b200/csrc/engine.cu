@@ -235,8 +235,20 @@ static size_t smem_bytes(int G, int k) { return SMEM_SPEC + WPC * walk_layout(G,
 //   FIRST: hits are ordered by their reference-DFS path; the earliest is kept under a
 //          seqlock, and work that lies after it is abandoned.
 __global__ void __launch_bounds__(32 * WPC, 6) k_search(const Spec* Sg, Rows R, Cont* Q, int* ready,
-                                                     Ctl* ctl, HitPath* best, Leaf* leaf_out) {
+                                                     Ctl* ctl, HitPath* best, Leaf* leaf_out,
+                                                     const Cont* root, long long slot0,
+                                                     int ready0) {
     extern __shared__ __align__(16) unsigned char smem[];
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        // publish the root piece (shipped with the Spec / Ctl upload): walkers that took
+        // its ticket spin on ready[slot0] until it is there
+        const int4* src = reinterpret_cast<const int4*>(root);
+        int4* dst = reinterpret_cast<int4*>(Q + slot0);
+        for (int i = threadIdx.x; i < (int)(sizeof(Cont) / 16); i += 32) dst[i] = src[i];
+        __threadfence();
+        __syncwarp();
+        if (threadIdx.x == 0) *(volatile int*)&ready[slot0] = ready0;
+    }
     Spec& S = *reinterpret_cast<Spec*>(smem);
     {
         const int n = sizeof(Spec) / 4;
@@ -422,9 +434,12 @@ Engine::Engine(int device) : device_(device) {
     evk1_ = d;
     evm0_ = e;
     evm1_ = f;
-    CK(cudaMalloc(&d_spec_, sizeof(Spec)));
-    CK(cudaMalloc(&d_ctl_, sizeof(Ctl)));
-    CK(cudaMalloc(&d_leaf_, sizeof(Leaf)));
+    // device mirror of the pinned staging layout: one upload and one read-back per search
+    CK(cudaMalloc(&d_blob_, pin_off(5)));
+    d_spec_ = static_cast<char*>(d_blob_) + pin_off(0);
+    d_ctl_ = static_cast<char*>(d_blob_) + pin_off(1);
+    d_leaf_ = static_cast<char*>(d_blob_) + pin_off(2);
+    d_root_ = static_cast<char*>(d_blob_) + pin_off(3);
     CK(cudaMallocHost(&h_pin_, pin_off(5)));
 }
 
@@ -436,9 +451,7 @@ Engine::~Engine() {
     cudaFree(d_bound_);
     cudaFree(d_d_);
     cudaFree(d_u_);
-    cudaFree(d_spec_);
-    cudaFree(d_ctl_);
-    cudaFree(d_leaf_);
+    cudaFree(d_blob_);
     cudaFree(d_front_[0]);
     cudaFree(d_ready_);
     cudaFree(d_best_);
@@ -561,21 +574,6 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     hr->bsz[0] = (uint16_t)S.G;
     *hone = 1;
     Cont* Q = reinterpret_cast<Cont*>(d_front_[0]);
-    CK(cudaEventRecord((cudaEvent_t)ev0_, s));
-    if (S.mode == MODE_FIRST && seed_path && seed_leaf) {
-        // a known leaf <= theta: the search only has to look at what precedes it
-        hc->has_hit = 1;
-        CK(cudaMemcpyAsync(d_best_, seed_path, sizeof(HitPath), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(d_leaf_, seed_leaf, sizeof(Leaf), cudaMemcpyHostToDevice, s));
-        h2d_ += sizeof(HitPath) + sizeof(Leaf);
-    }
-    CK(cudaMemcpyAsync(d_spec_, hs, sizeof(Spec), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d_ctl_, hc, sizeof(Ctl), cudaMemcpyHostToDevice, s));
-    const size_t slot0 = (size_t)(t0 % (unsigned long long)cap);
-    *hone = (int)(t0 + 1);
-    CK(cudaMemcpyAsync(Q + slot0, hr, sizeof(Cont), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d_ready_ + slot0, hone, sizeof(int), cudaMemcpyHostToDevice, s));
-    h2d_ += sizeof(Spec) + sizeof(Ctl) + sizeof(Cont) + sizeof(int);
     const size_t smem = smem_bytes(S.G, S.k);
     if (smem != grid_smem_) {
         if (smem > smem_attr_) {
@@ -590,27 +588,36 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
         grid_ = std::max(1, per_sm) * sms;  // all resident: spin-waiting needs it
         grid_smem_ = smem;
     }
-    CK(cudaEventRecord((cudaEvent_t)evk0_, s));
     // small trees (few option tuples) do not need the whole GPU: a handful of resident
     // CTAs finishes them without spinning up thousands of idle walkers
     double tuples = 1.0;
     for (int l = 0; l < S.k; ++l) tuples *= (double)(S.lvl_n[l] > 0 ? S.lvl_n[l] : 1);
     const long long grid = (tuples * S.G <= small_tree_) ? std::min<long long>(grid_, 8) : grid_;
     hc->walkers = (unsigned)(grid * WPC);
-    CK(cudaMemcpyAsync(&((Ctl*)d_ctl_)->walkers, &hc->walkers, sizeof(unsigned),
-                       cudaMemcpyHostToDevice, s));
-    k_search<<<(unsigned)grid, 32 * WPC, smem, s>>>((const Spec*)d_spec_, R, Q, d_ready_,
-                                                     (Ctl*)d_ctl_, (HitPath*)d_best_,
-                                                     (Leaf*)d_leaf_);
+    CK(cudaEventRecord((cudaEvent_t)ev0_, s));
+    if (S.mode == MODE_FIRST && seed_path && seed_leaf) {
+        // a known leaf <= theta: the search only has to look at what precedes it
+        hc->has_hit = 1;
+        *hl = *seed_leaf;
+        CK(cudaMemcpyAsync(d_best_, seed_path, sizeof(HitPath), cudaMemcpyHostToDevice, s));
+        h2d_ += sizeof(HitPath);
+    }
+    // Spec | Ctl | Leaf | root Cont in one upload (the kernel publishes the root piece)
+    CK(cudaMemcpyAsync(d_blob_, h_pin_, pin_off(4), cudaMemcpyHostToDevice, s));
+    h2d_ += (long long)pin_off(4);
+    const long long slot0 = (long long)(t0 % (unsigned long long)cap);
+    CK(cudaEventRecord((cudaEvent_t)evk0_, s));
+    k_search<<<(unsigned)grid, 32 * WPC, smem, s>>>(
+        (const Spec*)d_spec_, R, Q, d_ready_, (Ctl*)d_ctl_, (HitPath*)d_best_, (Leaf*)d_leaf_,
+        (const Cont*)d_root_, slot0, (int)(t0 + 1));
     CK(cudaEventRecord((cudaEvent_t)evk1_, s));
     ++launches_;
     ++own_launches_;
     ++st.rounds;
     // one read-back and one synchronisation per search: the control block and the leaf
     // (1 KB, read unconditionally — cheaper than a second round trip when there is a hit)
-    CK(cudaMemcpyAsync(hc, d_ctl_, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hl, d_leaf_, sizeof(Leaf), cudaMemcpyDeviceToHost, s));
-    d2h_ += sizeof(Ctl) + sizeof(Leaf);
+    CK(cudaMemcpyAsync(hc, d_ctl_, pin_off(3) - pin_off(1), cudaMemcpyDeviceToHost, s));
+    d2h_ += (long long)(pin_off(3) - pin_off(1));
     CK(cudaEventRecord((cudaEvent_t)ev1_, s));
     CK(cudaEventSynchronize((cudaEvent_t)ev1_));
     CK(cudaGetLastError());

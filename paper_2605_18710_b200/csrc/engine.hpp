@@ -93,6 +93,8 @@ class Engine {
     double *d_base_ = nullptr, *d_B_ = nullptr, *d_fp_ = nullptr, *d_bound_ = nullptr;
     int *d_d_ = nullptr, *d_u_ = nullptr;
     int n_rows_ = 0;
+    void* d_blob_ = nullptr;  // Spec | Ctl | Leaf | root Cont (pin_off layout)
+    void* d_root_ = nullptr;
     void* d_spec_ = nullptr;
     void* d_ctl_ = nullptr;
     void* d_leaf_ = nullptr;
