@@ -69,6 +69,7 @@ struct WarpHooks {
     const Walk* w;
     int cur_level;
     int don_period;
+    int may_donate;
     long long deep_after;
 
     __device__ bool hit_precedes() {  // lane 0 only
@@ -95,7 +96,7 @@ struct WarpHooks {
                 if (mode == MODE_FIRST && *(volatile int*)&ctl->has_hit && hit_precedes()) {
                     code = 2;
                 } else {
-                    unsigned int idle = *(volatile unsigned int*)&ctl->idle;
+                    unsigned int idle = may_donate ? *(volatile unsigned int*)&ctl->idle : 0u;
                     if (idle) {
                         unsigned long long qn = *(volatile unsigned long long*)&ctl->q_tail -
                                                 *(volatile unsigned long long*)&ctl->q_head;
@@ -316,6 +317,7 @@ __global__ void __launch_bounds__(32 * WPC, 6) k_search(const Spec* Sg, Rows R, 
         h.w = &w;
         h.cur_level = 0;
         h.don_period = S.don_period;
+        h.may_donate = S.donate;
         h.deep_after = S.deep_after;
         h.inc_cache = POS_INF;
         h.inc_cache = h.bcast_inc();
@@ -416,6 +418,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* e = std::getenv("MOSAIC_SMALL_TREE")) small_tree_ = std::atof(e);
     if (const char* e = std::getenv("MOSAIC_DEEP_AFTER")) deep_after_ = std::atoll(e);
     if (const char* e = std::getenv("MOSAIC_LOOKAHEAD")) lookahead_ = std::atoi(e);
+    if (const char* e = std::getenv("MOSAIC_SMALL_GRID")) small_grid_ = std::atoi(e);
     CK(cudaSetDevice(device));
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -592,8 +595,11 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     // CTAs finishes them without spinning up thousands of idle walkers
     double tuples = 1.0;
     for (int l = 0; l < S.k; ++l) tuples *= (double)(S.lvl_n[l] > 0 ? S.lvl_n[l] : 1);
-    const long long grid = (tuples * S.G <= small_tree_) ? std::min<long long>(grid_, 8) : grid_;
+    const long long grid = (tuples * S.G <= small_tree_) ? std::min<long long>(grid_, small_grid_) : grid_;
     hc->walkers = (unsigned)(grid * WPC);
+    // small trees: hand-overs cost more than they parallelise (each is a 1.3 KB piece
+    // round trip through L2); let the walker that owns the root finish it
+    hs->donate = grid < grid_ ? 0 : 1;
     CK(cudaEventRecord((cudaEvent_t)ev0_, s));
     if (S.mode == MODE_FIRST && seed_path && seed_leaf) {
         // a known leaf <= theta: the search only has to look at what precedes it

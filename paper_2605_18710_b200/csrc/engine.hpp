@@ -112,6 +112,7 @@ class Engine {
     // child look-ahead (can every remaining level still place an option?): off by default —
     // the lane-parallel option screen at the next level does the same job for less
     int lookahead_ = 0;
+    int small_grid_ = 8;  // CTAs for small trees
     long long deep_after_ = 4096;  // steps on one piece before deeper hand-overs are allowed
     long long front_cap_ = 0;
     void* h_pin_ = nullptr;
