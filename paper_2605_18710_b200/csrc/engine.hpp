@@ -105,7 +105,7 @@ class Engine {
     size_t grid_smem_ = 0, smem_attr_ = 0;
     bool trace_ = false;
     int don_depth_ = 3;    // donate levels <= k-1-don_depth (measured best on cfg5)
-    int don_period_ = 1;   // power of two (measured: hand-over latency matters most)
+    int don_period_ = 4;   // power of two; control reads every 4 steps (tools/knob_solve.sh)
     int backoff_cap_ = 2048;  // ns, idle walkers polling back-off cap (measured)
     double small_tree_ = 2e5;  // option tuples x G below which 8 CTAs run the search
     unsigned long long ticket_base_ = 0;
@@ -113,7 +113,7 @@ class Engine {
     // the lane-parallel option screen at the next level does the same job for less
     int lookahead_ = 0;
     int small_grid_ = 8;  // CTAs for small trees
-    long long deep_after_ = 4096;  // steps on one piece before deeper hand-overs are allowed
+    long long deep_after_ = 16384;  // steps on one piece before deeper hand-overs are allowed
     long long front_cap_ = 0;
     void* h_pin_ = nullptr;
     long long launches_ = 0;
