@@ -632,13 +632,6 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
         res.found = true;
         res.leaf = *hl;
     }
-    if (world_ > 1) merge_ranks(S, hc, res);
-    float kms = 0, ms = 0;
-    CK(cudaEventElapsedTime(&kms, (cudaEvent_t)evk0_, (cudaEvent_t)evk1_));
-    CK(cudaEventElapsedTime(&ms, (cudaEvent_t)ev0_, (cudaEvent_t)ev1_));
-    ksearch_ms_ += kms;
-    ++ksearch_n_;
-    search_ms_ += ms;
     if (hc->overflow) res.overflow = true;
     if (S.mode == MODE_MIN) {
         if (hc->abort && !hc->overflow) res.aborted = true;
@@ -649,6 +642,15 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
         w.u = hc->inc;
         res.value = w.d;
     }
+    // ranks must leave every search with the same answer (they replay the same control
+    // flow and all-gather once per search): merge after the local result is complete
+    if (world_ > 1) merge_ranks(S, hc, res);
+    float kms = 0, ms = 0;
+    CK(cudaEventElapsedTime(&kms, (cudaEvent_t)evk0_, (cudaEvent_t)evk1_));
+    CK(cudaEventElapsedTime(&ms, (cudaEvent_t)ev0_, (cudaEvent_t)ev1_));
+    ksearch_ms_ += kms;
+    ++ksearch_n_;
+    search_ms_ += ms;
     st.nodes += (long long)hc->nodes;
     st.leaves += (long long)hc->leaves;
     ++st.searches;
@@ -761,20 +763,27 @@ void Engine::merge_ranks(const Spec& S, const void* ctl_host, SearchResult& res)
     }
     if (ag_(ag_user_, &mine, all.data(), sizeof(RankRecord)) != 0)
         throw std::runtime_error("all-gather failed");
-    int win = -1;
+    int win = -1, minr = -1;
     double best = POS_INF;
     bool aborted = false, overflow = false;
     for (int r = 0; r < world_; ++r) {
         const RankRecord& x = all[r];
         aborted |= x.aborted != 0;
         overflow |= x.overflow != 0;
-        if (x.inc < best) best = x.inc;
+        if (minr < 0 || x.inc < best) {
+            best = x.inc;
+            minr = r;
+        }
         if (x.has_hit && (win < 0 || host_path_cmp(x.path, all[win].path, S.k) < 0)) win = r;
     }
     res.overflow = overflow;
     if (S.mode == MODE_MIN) {
+        // T* is the smallest incumbent; its leaf (the argmin the planner canonicalises)
+        // comes from the rank that holds it (lowest rank on ties)
         res.aborted = aborted;
         res.value = best;
+        res.found = all[minr].has_hit != 0;
+        if (res.found) res.leaf = all[minr].leaf;
     } else {
         res.found = win >= 0;
         if (win >= 0) res.leaf = all[win].leaf;
