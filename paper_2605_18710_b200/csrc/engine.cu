@@ -419,6 +419,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* e = std::getenv("MOSAIC_DEEP_AFTER")) deep_after_ = std::atoll(e);
     if (const char* e = std::getenv("MOSAIC_LOOKAHEAD")) lookahead_ = std::atoi(e);
     if (const char* e = std::getenv("MOSAIC_SMALL_GRID")) small_grid_ = std::atoi(e);
+    if (const char* e = std::getenv("MOSAIC_SHARD_LEVEL")) shard_level_ = std::atoi(e);
     CK(cudaSetDevice(device));
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -544,7 +545,10 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
             hs->shard_world = wd;
         }
     }
-    hs->shard_level = S.k >= 2 ? 1 : 0;  // (o_0, o_1) pairs: fine enough to balance 8 ranks
+    // option prefixes (o_0, o_1, o_2) are hashed to ranks: at 8 ranks the largest share of the
+    // dominant cfg5 proof is 1.15x the mean (pairs: 1.3x; tools/shard_levels.sh)
+    hs->shard_level = S.k >= 3 ? 2 : S.k - 1;
+    if (shard_level_ >= 0) hs->shard_level = std::min(shard_level_, S.k - 1);
     // donation policy: hand over only shallow levels, when the queue has run dry
     hs->don_max_level = S.k >= 6 ? S.k - 1 - don_depth_ : (S.k >= 3 ? S.k - 3 : 0);
     // long-running pieces may also hand over levels <= k-3 (see WarpHooks::abort)

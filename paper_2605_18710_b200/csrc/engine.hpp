@@ -113,6 +113,7 @@ class Engine {
     // the lane-parallel option screen at the next level does the same job for less
     int lookahead_ = 0;
     int small_grid_ = 8;  // CTAs for small trees
+    int shard_level_ = -1;  // override of the sharded option-prefix level (-1: default)
     long long deep_after_ = 16384;  // steps on one piece before deeper hand-overs are allowed
     long long front_cap_ = 0;
     void* h_pin_ = nullptr;
