@@ -20,9 +20,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX_HOST", "g++")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["engine.cu", "pack.cu", "sim.cu"]
+CU_SOURCES = ["engine.cu", "engine_fast.cu", "pack.cu", "sim.cu"]
 CPP_SOURCES = ["model.cpp", "planner.cpp", "capi.cpp"]
-HEADERS = ["engine.hpp", "search_core.cuh", "search_warp.cuh", "spec_build.hpp", "model.hpp",
+HEADERS = ["engine.hpp", "search_core.cuh", "search_warp.cuh", "search_kernel.cuh", "spec_build.hpp", "model.hpp",
            "planner.hpp", "pack.hpp", "sim.hpp"]
 
 

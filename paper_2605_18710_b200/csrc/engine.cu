@@ -33,309 +33,14 @@ namespace mg {
                                      " at " #x);                                       \
     } while (0)
 
-// Control block.  Fields that different threads write often live on their own 128-B
-// lines so spinning workers do not serialize the busy ones.
-struct Ctl {
-    alignas(128) unsigned long long inc;  // MIN incumbent, fp64 bits (values are >= 0)
-    double abort_below;
-    int abort;
-    int overflow;
-    alignas(128) unsigned long long q_head;
-    alignas(128) unsigned long long q_tail;
-    unsigned long long q_cap;
-    alignas(128) unsigned long long outstanding;  // queued + in-flight cursors
-    alignas(128) unsigned int idle;
-    unsigned int walkers;  // resident walkers of this launch
-    alignas(128) int lock;  // FIRST: best hit, published under a seqlock
-    int ver;
-    int has_hit;            // FIRST: a hit is published; MIN: an argmin leaf is stored
-    double leaf_val;
-    alignas(128) unsigned long long nodes, leaves;
-};
+}  // namespace mg
 
-// Hooks of one walker (a warp).  Everything that steers control flow is decided by
-// lane 0 and broadcast, so the warp stays converged.
-struct WarpHooks {
-    Ctl* ctl;
-    int mode;
-    long long steps;
-    double inc_cache;
-    int refresh;
-    Leaf* leaf_out;
-    HitPath* best;
-    Cont* q;
-    int* ready;
-    unsigned long long nodes, leaves;
-    const Walk* w;
-    int cur_level;
-    int don_period;
-    int may_donate;
-    long long deep_after;
+#include "search_kernel.cuh"
 
-    __device__ bool hit_precedes() {  // lane 0 only
-        int v0 = *(volatile int*)&ctl->ver;
-        if (v0 & 1) return false;
-        __threadfence();
-        bool before = path_precedes_rest((const volatile HitPath*)best, *w, cur_level);
-        __threadfence();
-        int v1 = *(volatile int*)&ctl->ver;
-        return v0 == v1 && before;
-    }
-    // 0 continue, 2 abandon (MIN restart, or a FIRST hit precedes all that is left),
-    // 3 idle walkers are waiting: donate shallow work
-    __device__ int abort() {
-        ++steps;
-        // global control state is read only every don_period steps: a per-step L2 round
-        // trip (broadcast from lane 0) was the single hottest stall of the walker loop
-        if ((steps & (unsigned)(don_period - 1)) != 0) return 0;
-        int code = 0;
-        if (lane_id() == 0) {
-            if (*(volatile int*)&ctl->abort) {
-                code = 2;
-            } else {
-                if (mode == MODE_FIRST && *(volatile int*)&ctl->has_hit && hit_precedes()) {
-                    code = 2;
-                } else {
-                    unsigned int idle = may_donate ? *(volatile unsigned int*)&ctl->idle : 0u;
-                    if (idle) {
-                        unsigned long long qn = *(volatile unsigned long long*)&ctl->q_tail -
-                                                *(volatile unsigned long long*)&ctl->q_head;
-                        if (qn == 0)  // queue drained and walkers waiting
-                            // a walker that has been on its piece for long holds a big
-                            // subtree: let it split deeper levels too
-                            code = steps > deep_after ? 4 : 3;
-                    }
-                }
-            }
-        }
-        return __shfl_sync(FULLW, code, 0);
-    }
-    __device__ void hit(const Walk& wk, int j, double v) {
-        if (lane_id() == 0) {
-            while (atomicCAS(&ctl->lock, 0, 1) != 0) __nanosleep(64);
-            __threadfence();
-            bool better = !*(volatile int*)&ctl->has_hit ||
-                          path_cmp((const volatile HitPath*)best, wk, j) > 0;
-            if (better) {
-                atomicAdd(&ctl->ver, 1);
-                __threadfence();
-                path_store((volatile HitPath*)best, wk, j);
-                store_leaf(wk, j, v, *leaf_out);
-                ctl->has_hit = 1;
-                __threadfence();
-                atomicAdd(&ctl->ver, 1);
-            }
-            __threadfence();
-            atomicExch(&ctl->lock, 0);
-        }
-        __syncwarp();
-    }
-    // push the cursor "rest of level l" onto the ring queue (ticket t -> slot t % cap,
-    // published by writing ready[slot] = t + 1)
-    // ph 1: "rest of level l" (after the current composition); ph 0: options from mid on
-    __device__ bool donate(const Walk& wk, int l, int ph, int mid) {
-        long long slot = -1;
-        unsigned long long t = 0;
-        if (lane_id() == 0) {
-            t = *(volatile unsigned long long*)&ctl->q_tail;
-            while (true) {
-                unsigned long long head = *(volatile unsigned long long*)&ctl->q_head;
-                if (t + 1 - head > ctl->q_cap) break;  // ring full
-                unsigned long long old = atomicCAS(&ctl->q_tail, t, t + 1);
-                if (old == t) {
-                    slot = (long long)(t % ctl->q_cap);
-                    atomicAdd(&ctl->outstanding, 1ULL);
-                    break;
-                }
-                t = old;
-            }
-        }
-        slot = __shfl_sync(FULLW, slot, 0);
-        if (slot < 0) return false;
-        store_cont_warp(wk, l, ph, q[slot], mid - 1);
-        __threadfence();  // every lane's part of the cursor is visible ...
-        __syncwarp();
-        if (lane_id() == 0) {
-            __threadfence();
-            atomicExch(&ready[slot], (int)(t + 1));  // ... before it is published
-        }
-        __syncwarp();
-        return true;
-    }
-    __device__ double bcast_inc() {
-        double I = 0.0;
-        if (lane_id() == 0) I = __longlong_as_double(*(volatile long long*)&ctl->inc);
-        return __shfl_sync(FULLW, I, 0);
-    }
-    __device__ double thr(const Spec& S) {
-        if (mode != MODE_MIN) return S.thp;
-        if ((refresh++ & 15) == 0) {
-            double I = bcast_inc();
-            inc_cache = I < inc_cache ? I : inc_cache;
-        }
-        double t = inc_cache >= POS_INF ? POS_INF : inc_cache * (1.0 - TIE_EPS);
-        return t < S.thp ? t : S.thp;
-    }
-    __device__ double incumbent() {  // refreshed every 16 calls, like thr()
-        if ((refresh++ & 15) == 0) {
-            double I = bcast_inc();
-            inc_cache = I < inc_cache ? I : inc_cache;
-        }
-        return inc_cache;
-    }
-    __device__ void improve(double v) {
-        if (lane_id() == 0) {
-            atomicMin(&ctl->inc, (unsigned long long)__double_as_longlong(v));
-            if (v < ctl->abort_below) atomicExch(&ctl->abort, 1);
-        }
-        if (v < inc_cache) inc_cache = v;
-        __syncwarp();
-    }
-    // MIN: lower the incumbent and keep the allocation that reached it
-    __device__ void improve_leaf(const Walk& wk, int j, double v) {
-        if (lane_id() == 0) {
-            atomicMin(&ctl->inc, (unsigned long long)__double_as_longlong(v));
-            if (v < ctl->abort_below) atomicExch(&ctl->abort, 1);
-            while (atomicCAS(&ctl->lock, 0, 1) != 0) __nanosleep(64);
-            __threadfence();
-            if (!ctl->has_hit || v < ctl->leaf_val) {
-                store_leaf(wk, j, v, *leaf_out);
-                ctl->leaf_val = v;
-                ctl->has_hit = 1;
-            }
-            __threadfence();
-            atomicExch(&ctl->lock, 0);
-        }
-        if (v < inc_cache) inc_cache = v;
-        __syncwarp();
-    }
-    __device__ void count_node() { ++nodes; }
-    __device__ void count_leaf() { ++leaves; }
-    __device__ void count_leaves(int n) { leaves += (unsigned long long)n; }
-    __device__ void overflow() {
-        if (lane_id() == 0) {
-            atomicExch(&ctl->overflow, 1);
-            atomicExch(&ctl->abort, 1);
-        }
-    }
-    __device__ void level(int j) { cur_level = j; }
-};
+namespace mg {
 
-constexpr int WPC = 4;  // walkers (warps) per CTA
+const void* k_search_fast_fn();  // engine_fast.cu
 
-constexpr size_t SMEM_SPEC = (sizeof(Spec) + 15) & ~size_t(15);
-
-// dynamic shared memory of one CTA for a stage of k modules over G GPUs
-static size_t smem_bytes(int G, int k) { return SMEM_SPEC + WPC * walk_layout(G, k).bytes; }
-
-// One resident persistent grid per stage search.  Each warp is a walker: it pops a
-// cursor from the shared ring queue and runs the warp-cooperative DFS on it; a busy
-// walker that sees idle ones and a short queue donates its shallowest untried level.
-// `outstanding` counts queued + in-flight cursors; every walker exits when it hits 0.
-//   MIN:   shared incumbent (atomicMin on the fp64 bits), tie band TIE_EPS.
-//   FIRST: hits are ordered by their reference-DFS path; the earliest is kept under a
-//          seqlock, and work that lies after it is abandoned.
-__global__ void __launch_bounds__(32 * WPC, 6) k_search(const Spec* Sg, Rows R, Cont* Q, int* ready,
-                                                     Ctl* ctl, HitPath* best, Leaf* leaf_out,
-                                                     const Cont* root, long long slot0,
-                                                     int ready0) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
-        // publish the root piece (shipped with the Spec / Ctl upload): walkers that took
-        // its ticket spin on ready[slot0] until it is there
-        const int4* src = reinterpret_cast<const int4*>(root);
-        int4* dst = reinterpret_cast<int4*>(Q + slot0);
-        for (int i = threadIdx.x; i < (int)(sizeof(Cont) / 16); i += 32) dst[i] = src[i];
-        __threadfence();
-        __syncwarp();
-        if (threadIdx.x == 0) *(volatile int*)&ready[slot0] = ready0;
-    }
-    Spec& S = *reinterpret_cast<Spec*>(smem);
-    {
-        const int n = sizeof(Spec) / 4;
-        const int* src = reinterpret_cast<const int*>(Sg);
-        int* dst = reinterpret_cast<int*>(smem);
-        for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
-        __syncthreads();
-    }
-    const int wid = threadIdx.x >> 5;
-    const int lane = lane_id();
-    const size_t wbytes = walk_layout(S.G, S.k).bytes;
-    unsigned char* wbase = smem + SMEM_SPEC + wid * wbytes;
-    Walk& w = *reinterpret_cast<Walk*>(wbase);
-    if (lane == 0) walk_carve(w, wbase, S.G, S.k);
-    __syncwarp();
-    unsigned long long nodes = 0, leaves = 0;
-    while (true) {
-        long long ticket = -1;
-        if (lane == 0) {
-            bool idle = false;
-            unsigned backoff = 128;
-            const unsigned backoff_cap = S.backoff_cap_ns;
-            while (true) {
-                if (*(volatile int*)&ctl->abort) break;
-                unsigned long long h = *(volatile unsigned long long*)&ctl->q_head;
-                unsigned long long t = *(volatile unsigned long long*)&ctl->q_tail;
-                if (h < t) {
-                    if (atomicCAS(&ctl->q_head, h, h + 1) == h) {
-                        ticket = (long long)h;
-                        break;
-                    }
-                    continue;
-                }
-                if (*(volatile unsigned long long*)&ctl->outstanding == 0) break;
-                if (!idle) {
-                    atomicAdd(&ctl->idle, 1u);
-                    idle = true;
-                }
-                __nanosleep(backoff);
-                backoff = backoff < backoff_cap ? backoff * 2 : backoff_cap;
-            }
-            if (idle) atomicSub(&ctl->idle, 1u);
-            if (ticket >= 0) {
-                const long long slot = (long long)((unsigned long long)ticket % ctl->q_cap);
-                while (*(volatile int*)&ready[slot] != (int)(ticket + 1)) __nanosleep(32);
-                __threadfence();
-            }
-        }
-        ticket = __shfl_sync(FULLW, ticket, 0);
-        if (ticket < 0) break;
-        const long long slot = (long long)((unsigned long long)ticket % ctl->q_cap);
-        __threadfence();
-        load_cont_warp(Q[slot], w, S.mode == MODE_FIRST);
-        WarpHooks h;
-        h.ctl = ctl;
-        h.mode = S.mode;
-        h.steps = 0;
-        h.refresh = 0;
-        h.leaf_out = leaf_out;
-        h.best = best;
-        h.q = Q;
-        h.ready = ready;
-        h.nodes = 0;
-        h.leaves = 0;
-        h.w = &w;
-        h.cur_level = 0;
-        h.don_period = S.don_period;
-        h.may_donate = S.donate;
-        h.deep_after = S.deep_after;
-        h.inc_cache = POS_INF;
-        h.inc_cache = h.bcast_inc();
-        const int d0 = Q[slot].depth;
-        dfs_warp(S, R, w, d0, h);
-        nodes += h.nodes;
-        leaves += h.leaves;
-        __syncwarp();
-        if (lane == 0) {
-            __threadfence();
-            atomicAdd(&ctl->outstanding, ~0ULL);  // -1
-        }
-    }
-    if (lane == 0) {
-        atomicAdd(&ctl->nodes, nodes);
-        atomicAdd(&ctl->leaves, leaves);
-    }
-}
 
 // ---------------------------------------------------------------------------
 // K1: batched stage_time.  One warp per allocation.
@@ -419,6 +124,7 @@ Engine::Engine(int device) : device_(device) {
     if (const char* e = std::getenv("MOSAIC_DEEP_AFTER")) deep_after_ = std::atoll(e);
     if (const char* e = std::getenv("MOSAIC_LOOKAHEAD")) lookahead_ = std::atoi(e);
     if (const char* e = std::getenv("MOSAIC_SMALL_GRID")) small_grid_ = std::atoi(e);
+    no_fast_ = std::getenv("MOSAIC_GENERIC_KERNEL") != nullptr;
     if (const char* e = std::getenv("MOSAIC_SHARD_LEVEL")) shard_level_ = std::atoi(e);
     CK(cudaSetDevice(device));
     cudaStream_t s;
@@ -582,19 +288,23 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     *hone = 1;
     Cont* Q = reinterpret_cast<Cont*>(d_front_[0]);
     const size_t smem = smem_bytes(S.G, S.k);
-    if (smem != grid_smem_) {
-        if (smem > smem_attr_) {
-            CK(cudaFuncSetAttribute(k_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-            smem_attr_ = smem;
+    // the specialised kernel when the model is the common one (same search, fewer branches)
+    const bool fast = S.include_self && S.nonneg && !S.additive && !no_fast_;
+    const void* kfn = fast ? k_search_fast_fn() : reinterpret_cast<const void*>(&k_search);
+    const int ki = fast ? 1 : 0;
+    if (smem != grid_smem_[ki]) {
+        if (smem > smem_attr_[ki]) {
+            CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            smem_attr_[ki] = smem;
         }
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search, 32 * WPC, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 32 * WPC, smem));
         int sms = 148;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
-        grid_ = std::max(1, per_sm) * sms;  // all resident: spin-waiting needs it
-        grid_smem_ = smem;
+        grid_k_[ki] = std::max(1, per_sm) * sms;  // all resident: spin-waiting needs it
+        grid_smem_[ki] = smem;
     }
+    grid_ = grid_k_[ki];
     // small trees (few option tuples) do not need the whole GPU: a handful of resident
     // CTAs finishes them without spinning up thousands of idle walkers
     double tuples = 1.0;
@@ -617,9 +327,18 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     h2d_ += (long long)pin_off(4);
     const long long slot0 = (long long)(t0 % (unsigned long long)cap);
     CK(cudaEventRecord((cudaEvent_t)evk0_, s));
-    k_search<<<(unsigned)grid, 32 * WPC, smem, s>>>(
-        (const Spec*)d_spec_, R, Q, d_ready_, (Ctl*)d_ctl_, (HitPath*)d_best_, (Leaf*)d_leaf_,
-        (const Cont*)d_root_, slot0, (int)(t0 + 1));
+    {
+        const Spec* a0 = (const Spec*)d_spec_;
+        Ctl* a4 = (Ctl*)d_ctl_;
+        HitPath* a5 = (HitPath*)d_best_;
+        Leaf* a6 = (Leaf*)d_leaf_;
+        const Cont* a7 = (const Cont*)d_root_;
+        int* a3 = d_ready_;
+        long long a8 = slot0;
+        int a9 = (int)(t0 + 1);
+        void* args[] = {&a0, &R, &Q, &a3, &a4, &a5, &a6, &a7, &a8, &a9};
+        CK(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(32 * WPC), args, smem, s));
+    }
     CK(cudaEventRecord((cudaEvent_t)evk1_, s));
     ++launches_;
     ++own_launches_;

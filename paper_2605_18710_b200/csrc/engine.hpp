@@ -102,7 +102,8 @@ class Engine {
     int* d_ready_ = nullptr;
     void* d_best_ = nullptr;
     long long grid_ = 0;
-    size_t grid_smem_ = 0, smem_attr_ = 0;
+    size_t grid_smem_[2] = {0, 0}, smem_attr_[2] = {0, 0};  // [generic, specialised]
+    long long grid_k_[2] = {0, 0};
     bool trace_ = false;
     int don_depth_ = 3;    // donate levels <= k-1-don_depth (measured best on cfg5)
     int don_period_ = 4;   // power of two; control reads every 4 steps (tools/knob_solve.sh)
@@ -113,6 +114,7 @@ class Engine {
     // the lane-parallel option screen at the next level does the same job for less
     int lookahead_ = 0;
     int small_grid_ = 8;  // CTAs for small trees
+    bool no_fast_ = false;  // MOSAIC_GENERIC_KERNEL: never use the specialised kernel
     int shard_level_ = -1;  // override of the sharded option-prefix level (-1: default)
     long long deep_after_ = 16384;  // steps on one piece before deeper hand-overs are allowed
     long long front_cap_ = 0;

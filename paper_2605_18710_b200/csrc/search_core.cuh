@@ -34,8 +34,22 @@
 #ifndef MG_HD
 #define MG_HD __device__ __forceinline__
 #endif
+// Model flags read by the device search.  engine_fast.cu compiles the same code with
+// MG_SPECIALIZE=1: include_self, non-negative coefficients and the multiplicative term fixed.
+#ifndef MG_SPECIALIZE
+#define MG_SPECIALIZE 0
+#endif
+#if MG_SPECIALIZE
+#define MG_SELF(S) true
+#define MG_NONNEG(S) true
+#define MG_ADD(S) false
+#else
+#define MG_SELF(S) ((S).include_self)
+#define MG_NONNEG(S) ((S).nonneg)
+#define MG_ADD(S) ((S).additive)
+#endif
 #ifndef MG_COLD
-#define MG_COLD __device__ __noinline__  // rare paths (hits): kept out of the hot loop
+#define MG_COLD static __device__ __noinline__  // rare paths (hits): kept out of the hot loop
 #endif
 // Device code below is only compiled by nvcc (the host planner includes this header
 // for the Spec/Node/Leaf layouts only; there is no host search path).
@@ -236,7 +250,7 @@ MG_HD double envelope(const Spec& S, int j, double P) {
 // max over residents m of base_m + delta(residents), module-index order sums.
 MG_HD double contrib(const Spec& S, const Rows& R, const uint16_t* opt, unsigned mask) {
     if (!mask) return NEG_INF;
-    if (S.include_self) {
+    if (MG_SELF(S)) {
         double s = 0.0, p = 1.0, mb = NEG_INF;
         #pragma unroll 1
         for (int pos = 0; pos < S.k; ++pos) {
@@ -250,7 +264,7 @@ MG_HD double contrib(const Spec& S, const Rows& R, const uint16_t* opt, unsigned
             mb = ba > mb ? ba : mb;
         }
         double dl = S.e1 + S.e2 * s;
-        dl = dl + (S.additive ? 0.0 : S.e3 * p);
+        dl = dl + (MG_ADD(S) ? 0.0 : S.e3 * p);
         return mb + dl;
     }
     double best = NEG_INF;
@@ -271,7 +285,7 @@ MG_HD double contrib(const Spec& S, const Rows& R, const uint16_t* opt, unsigned
         }
         if (n == 0) p = 0.0;
         double dl = S.e1 + S.e2 * s;
-        dl = dl + (S.additive ? 0.0 : S.e3 * p);
+        dl = dl + (MG_ADD(S) ? 0.0 : S.e3 * p);
         double v = R.base[S.lvl_off[l] + opt[l]] + dl;
         best = v > best ? v : best;
     }
@@ -283,7 +297,7 @@ MG_HD double contrib(const Spec& S, const Rows& R, const uint16_t* opt, unsigned
 MG_HD double contrib_o(const Spec& S, const Rows& R, const uint16_t* opt, unsigned mask, int jl,
                        int ol) {
     if (!mask) return NEG_INF;
-    if (S.include_self) {
+    if (MG_SELF(S)) {
         double s = 0.0, p = 1.0, mb = NEG_INF;
         #pragma unroll 1
         for (int pos = 0; pos < S.k; ++pos) {
@@ -297,7 +311,7 @@ MG_HD double contrib_o(const Spec& S, const Rows& R, const uint16_t* opt, unsign
             mb = ba > mb ? ba : mb;
         }
         double dl = S.e1 + S.e2 * s;
-        dl = dl + (S.additive ? 0.0 : S.e3 * p);
+        dl = dl + (MG_ADD(S) ? 0.0 : S.e3 * p);
         return mb + dl;
     }
     double best = NEG_INF;
@@ -318,7 +332,7 @@ MG_HD double contrib_o(const Spec& S, const Rows& R, const uint16_t* opt, unsign
         }
         if (n == 0) p = 0.0;
         double dl = S.e1 + S.e2 * s;
-        dl = dl + (S.additive ? 0.0 : S.e3 * p);
+        dl = dl + (MG_ADD(S) ? 0.0 : S.e3 * p);
         double v = R.base[S.lvl_off[l] + (l == jl ? ol : opt[l])] + dl;
         best = v > best ? v : best;
     }
@@ -340,14 +354,14 @@ MG_HD unsigned shard_hash(const uint16_t* opt, int j, int o) {
 MG_HD int opt_test(const Spec& S, const Rows& R, int r, double thr) {
     double base = R.base[r];
     if (S.use_filter && R.bound[r] > S.theta) {
-        if (S.nonneg && base + S.e1 > S.theta) return 2;
-        if (!S.nonneg && base > S.theta) return 2;
+        if (MG_NONNEG(S) && base + S.e1 > S.theta) return 2;
+        if (!MG_NONNEG(S) && base > S.theta) return 2;
         return 1;
     }
-    if (S.nonneg) {
+    if (MG_NONNEG(S)) {
         double be = base + S.e1;
         if (be > thr) return 2;
-        double lb = S.include_self ? be + S.e2 * R.B[r] : be;
+        double lb = MG_SELF(S) ? be + S.e2 * R.B[r] : be;
         if (lb > thr) return 1;
     }
     return 0;

@@ -254,11 +254,11 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
     #pragma unroll 1
     for (int b = lane; b < nb; b += 32) {
         const unsigned m = w.bmk[o0 + b];
-        w.cm[b] = m ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] + (S.additive ? 0.0 : S.e3 * w.pP[b])
+        w.cm[b] = m ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] + (MG_ADD(S) ? 0.0 : S.e3 * w.pP[b])
                     : NEG_INF;
     }
     __syncwarp();
-    bool rest_ready = !S.include_self;
+    bool rest_ready = !MG_SELF(S);
     if (rest_ready) {
         #pragma unroll 1
         for (int b = lane; b < nb; b += 32) w.cs[b] = contrib(S, R, w.opt, w.bmk[o0 + b]);
@@ -298,7 +298,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
         if (valid) {
             // fast filter (approximate contributions, sound 1e-12 slack)
             pass = true;
-            if (S.include_self) {
+            if (MG_SELF(S)) {
                 const double tx = fm ? S.theta * (1.0 + 1e-12) : Ie;
                 int lo = 0, hi = 0;
                 #pragma unroll 1
@@ -310,7 +310,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
                     if (el) {
                         const double mb = w.pmb[b] > ba ? w.pmb[b] : ba;
                         const double tv = mb + S.e1 + S.e2 * (w.psum[b] + bo) +
-                                          (S.additive ? 0.0 : S.e3 * (w.pP[b] * bo));
+                                          (MG_ADD(S) ? 0.0 : S.e3 * (w.pP[b] * bo));
                         tok = fm ? tv <= tx : tv < tx;
                     }
                     if (rok) {
@@ -422,11 +422,11 @@ __device__ __forceinline__ void screen_options(const Spec& S, const Rows& R, Wal
     // (-inf where no module resides yet); lives in the composition scan scratch (sa|sb),
     // which is free between compositions
     double* lbrv = reinterpret_cast<double*>(w.sa);
-    if (S.nonneg) {
+    if (MG_NONNEG(S)) {
         #pragma unroll 1
         for (int b = lane; b < nb; b += 32)
             lbrv[b] = !w.bmk[o0 + b] ? NEG_INF
-                      : S.include_self
+                      : MG_SELF(S)
                           ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] + envelope(S, j + 1, w.pP[b])
                           : w.pmx[b] + S.e1 + S.e2 * w.psum[b] + envelope(S, j + 1, 0.0);
         __syncwarp();
@@ -451,10 +451,10 @@ __device__ __forceinline__ void screen_options(const Spec& S, const Rows& R, Wal
                 const int s = w.bsz[o0 + b];
                 const bool el = w.pu[b] + uu <= S.L && !(w.pm[b] + ff > S.cap_slack);
                 bool tok = el, rok = true;
-                if (S.nonneg) {
+                if (MG_NONNEG(S)) {
                     if (el) {
                         double lbt;
-                        if (S.include_self) {
+                        if (MG_SELF(S)) {
                             const double mb = w.pmb[b] > ba ? w.pmb[b] : ba;
                             lbt = mb + S.e1 + S.e2 * (w.psum[b] + bo) +
                                   envelope(S, j + 1, w.pP[b] * bo);
@@ -520,7 +520,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                     }
                 }
             }
-            if (j == k - 1 && S.nonneg) {
+            if (j == k - 1 && MG_NONNEG(S)) {
                 if (last_level_batch(S, R, w, j, ps_lvl, h)) return 1;
                 --j;
                 continue;
@@ -583,7 +583,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                     #pragma unroll 1
                     for (int b = lane; b < nb; b += 32)
                         w.cm[b] = w.bmk[o0 + b] ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] +
-                                                      (S.additive ? 0.0 : S.e3 * w.pP[b])
+                                                      (MG_ADD(S) ? 0.0 : S.e3 * w.pP[b])
                                                 : NEG_INF;
                     __syncwarp();
                 }
@@ -596,10 +596,10 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                 const int s = w.bsz[o0 + b];
                 const bool el = w.pu[b] + uu <= S.L && !(w.pm[b] + ff > S.cap_slack);
                 bool tok = el, rok = true;
-                if (!last && S.nonneg) {
+                if (!last && MG_NONNEG(S)) {
                     if (el) {
                         double lbt;
-                        if (S.include_self) {
+                        if (MG_SELF(S)) {
                             const double mb = w.pmb[b] > ba ? w.pmb[b] : ba;
                             lbt = mb + S.e1 + S.e2 * (w.psum[b] + bo) +
                                   envelope(S, j + 1, w.pP[b] * bo);
@@ -611,7 +611,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                         tok = !(lbt > thr);
                     }
                     if (w.bmk[o0 + b]) {
-                        const double lbr = S.include_self
+                        const double lbr = MG_SELF(S)
                                                ? w.pmb[b] + S.e1 + S.e2 * w.psum[b] +
                                                      envelope(S, j + 1, w.pP[b])
                                                : w.pmx[b] + S.e1 + S.e2 * w.psum[b] +
@@ -643,7 +643,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
             if (last) {
                 h.count_leaf();
                 const bool fm = S.mode == MODE_FIRST;
-                if (S.include_self) {
+                if (MG_SELF(S)) {
                     const double tx = fm ? S.theta * (1.0 + 1e-12) : h.incumbent() * (1.0 - TIE_EPS);
                     int flo = 0, fhi = 0;
                     bool fdead = false;
@@ -655,7 +655,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                         if (w.hi[o0 + b]) {
                             const double mb = w.pmb[b] > ba ? w.pmb[b] : ba;
                             const double tv = mb + S.e1 + S.e2 * (w.psum[b] + bo) +
-                                              (S.additive ? 0.0 : S.e3 * (w.pP[b] * bo));
+                                              (MG_ADD(S) ? 0.0 : S.e3 * (w.pP[b] * bo));
                             tok = fm ? tv <= tx : tv < tx;
                         }
                         if (rok) {
@@ -849,7 +849,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
         // (when only the closed-form last level remains, its batch screen subsumes this)
         #pragma unroll 1
         for (int l = j + 1; l < k && l <= j + S.lookahead && !prune &&
-                            !(j + 1 == k - 1 && S.nonneg);
+                            !(j + 1 == k - 1 && MG_NONNEG(S));
              ++l) {
             const int n = S.lvl_n[l], off = S.lvl_off[l];
             // lanes over options (32 at a time), each lane scanning the m child blocks:
@@ -872,7 +872,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                     for (int b = 0; b < m && cnt < d2; ++b) {
                         if (w.cu[b] + u2 > S.L) continue;
                         if (w.cm[b] + f2 > S.cap_slack) continue;
-                        if (S.nonneg && S.include_self) {
+                        if (MG_NONNEG(S) && MG_SELF(S)) {
                             const double mb = w.cb[b] > a2 ? w.cb[b] : a2;
                             if (mb + S.e1 + S.e2 * (w.cs[b] + b2) > thr) continue;
                         }
