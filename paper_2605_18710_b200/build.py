@@ -20,7 +20,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX_HOST", "g++")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["engine.cu", "engine_fast.cu", "pack.cu", "sim.cu"]
+CU_SOURCES = ["engine.cu", "pack.cu", "sim.cu"]
+# engine_fast.cu is compiled once per search mode (specialised MIN / FIRST kernels)
+CU_VARIANTS = [("engine_fast.cu", "engine_fast_min", ["-DMG_FAST_MODE=0"]),
+               ("engine_fast.cu", "engine_fast_first", ["-DMG_FAST_MODE=1"])]
 CPP_SOURCES = ["model.cpp", "planner.cpp", "capi.cpp"]
 HEADERS = ["engine.hpp", "search_core.cuh", "search_warp.cuh", "search_kernel.cuh", "spec_build.hpp", "model.hpp",
            "planner.hpp", "pack.hpp", "sim.hpp"]
@@ -44,12 +47,13 @@ def build(verbose_ptxas: bool = False) -> str:
         os.path.join(HERE, "..", "include", "mosaic_gpu.h")
     ]
     objs = []
-    for src in CU_SOURCES:
+    units = [(src, src, []) for src in CU_SOURCES] + [(a, b + ".cu", c) for a, b, c in CU_VARIANTS]
+    for src, name, defs in units:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src + ".o")
+        o = os.path.join(BUILD, name + ".o")
         objs.append(o)
         if _newer(o, [s] + hdrs + [__file__]):
-            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++20",
+            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++20", *defs,
                    "-Xcompiler", "-fPIC,-ffp-contract=off", "-c", s, "-o", o]
             if verbose_ptxas:
                 cmd.insert(1, "-Xptxas=-v")

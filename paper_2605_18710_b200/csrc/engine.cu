@@ -39,7 +39,8 @@ namespace mg {
 
 namespace mg {
 
-const void* k_search_fast_fn();  // engine_fast.cu
+const void* k_search_fast_min_fn();    // engine_fast.cu, MG_FAST_MODE=0
+const void* k_search_fast_first_fn();  // engine_fast.cu, MG_FAST_MODE=1
 
 
 // ---------------------------------------------------------------------------
@@ -290,8 +291,9 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     const size_t smem = smem_bytes(S.G, S.k);
     // the specialised kernel when the model is the common one (same search, fewer branches)
     const bool fast = S.include_self && S.nonneg && !S.additive && !no_fast_;
-    const void* kfn = fast ? k_search_fast_fn() : reinterpret_cast<const void*>(&k_search);
-    const int ki = fast ? 1 : 0;
+    const void* kfn = !fast ? reinterpret_cast<const void*>(&k_search)
+                      : S.mode == MODE_MIN ? k_search_fast_min_fn() : k_search_fast_first_fn();
+    const int ki = !fast ? 0 : (S.mode == MODE_MIN ? 1 : 2);
     if (smem != grid_smem_[ki]) {
         if (smem > smem_attr_[ki]) {
             CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -102,8 +102,9 @@ class Engine {
     int* d_ready_ = nullptr;
     void* d_best_ = nullptr;
     long long grid_ = 0;
-    size_t grid_smem_[2] = {0, 0}, smem_attr_[2] = {0, 0};  // [generic, specialised]
-    long long grid_k_[2] = {0, 0};
+    // [generic, specialised MIN, specialised FIRST]
+    size_t grid_smem_[3] = {0, 0, 0}, smem_attr_[3] = {0, 0, 0};
+    long long grid_k_[3] = {0, 0, 0};
     bool trace_ = false;
     int don_depth_ = 3;    // donate levels <= k-1-don_depth (measured best on cfg5)
     int don_period_ = 4;   // power of two; control reads every 4 steps (tools/knob_solve.sh)

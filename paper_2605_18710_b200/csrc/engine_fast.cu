@@ -2,8 +2,17 @@
 // interference coefficients, multiplicative term on (every BASELINE config).  Same search
 // code as the generic kernel (search_kernel.cuh); the fixed flags drop the other branches,
 // which keeps the kernel small enough for the instruction cache.
+// Built twice by build.py: MG_FAST_MODE=0 (MIN proofs) and MG_FAST_MODE=1 (FIRST probes).
 #define MG_SPECIALIZE 1
-#define MG_KSEARCH_NAME k_search_fast
+#if MG_FAST_MODE == 0
+#define MG_KSEARCH_NAME k_search_fast_min
+#define MG_MODE_FIXED 0
+#define MG_FAST_FN k_search_fast_min_fn
+#else
+#define MG_KSEARCH_NAME k_search_fast_first
+#define MG_MODE_FIXED 1
+#define MG_FAST_FN k_search_fast_first_fn
+#endif
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -17,5 +26,5 @@
 #include "search_kernel.cuh"
 
 namespace mg {
-const void* k_search_fast_fn() { return reinterpret_cast<const void*>(&k_search_fast); }
+const void* MG_FAST_FN() { return reinterpret_cast<const void*>(&MG_KSEARCH_NAME); }
 }  // namespace mg

@@ -48,6 +48,11 @@
 #define MG_NONNEG(S) ((S).nonneg)
 #define MG_ADD(S) ((S).additive)
 #endif
+#ifdef MG_MODE_FIXED
+#define MG_MODE(S) (MG_MODE_FIXED)
+#else
+#define MG_MODE(S) ((S).mode)
+#endif
 #ifndef MG_COLD
 #define MG_COLD static __device__ __noinline__  // rare paths (hits): kept out of the hot loop
 #endif

@@ -281,10 +281,10 @@ __global__ void __launch_bounds__(32 * WPC, 6) MG_KSEARCH_NAME(const Spec* Sg, R
         if (ticket < 0) break;
         const long long slot = (long long)((unsigned long long)ticket % ctl->q_cap);
         __threadfence();
-        load_cont_warp(Q[slot], w, S.mode == MODE_FIRST);
+        load_cont_warp(Q[slot], w, MG_MODE(S) == MODE_FIRST);
         WarpHooks h;
         h.ctl = ctl;
-        h.mode = S.mode;
+        h.mode = MG_MODE(S);
         h.steps = 0;
         h.refresh = 0;
         h.leaf_out = leaf_out;

@@ -264,7 +264,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
         for (int b = lane; b < nb; b += 32) w.cs[b] = contrib(S, R, w.opt, w.bmk[o0 + b]);
         __syncwarp();
     }
-    const bool fm = S.mode == MODE_FIRST;
+    const bool fm = MG_MODE(S) == MODE_FIRST;
     const int n = S.lvl_n[j] < w.oe[j] ? S.lvl_n[j] : w.oe[j];
     const int off = S.lvl_off[j];
     const double thr = h.thr(S);
@@ -642,7 +642,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
             if (dead || sumlo > dd || sumhi < dd) continue;
             if (last) {
                 h.count_leaf();
-                const bool fm = S.mode == MODE_FIRST;
+                const bool fm = MG_MODE(S) == MODE_FIRST;
                 if (MG_SELF(S)) {
                     const double tx = fm ? S.theta * (1.0 + 1e-12) : h.incumbent() * (1.0 - TIE_EPS);
                     int flo = 0, fhi = 0;
