@@ -376,7 +376,8 @@ def main() -> None:
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
                      "traffic_source": TRAFFIC_CSV if traffic is not None else None,
-                     "kernel": "k_search", "peak_kind": peak_kind,
+                     "kernel": "k_search (k_search_fast_min / _first builds for this model)",
+                     "peak_kind": peak_kind,
                      "algorithmic_bytes": "24*k B per scored leaf (k option rows x 3 fp64, "
                                           "SURVEY.md 8d)",
                      "note": "integer/branch-bound tree search; HBM is not the binding "
