@@ -288,9 +288,9 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     hr->bsz[0] = (uint16_t)S.G;
     *hone = 1;
     Cont* Q = reinterpret_cast<Cont*>(d_front_[0]);
-    const size_t smem = smem_bytes(S.G, S.k);
     // the specialised kernel when the model is the common one (same search, fewer branches)
     const bool fast = S.include_self && S.nonneg && !S.additive && !no_fast_;
+    const size_t smem = smem_bytes(S.G, S.k, fast);
     const void* kfn = !fast ? reinterpret_cast<const void*>(&k_search)
                       : S.mode == MODE_MIN ? k_search_fast_min_fn() : k_search_fast_first_fn();
     const int ki = !fast ? 0 : (S.mode == MODE_MIN ? 1 : 2);

@@ -190,7 +190,8 @@ struct Walk {
 
 MG_HX size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-MG_HX WalkLayout walk_layout(int G, int k) {
+// lean: the specialised (include_self) kernels keep no own-excluded bound arrays (pmx, cmx)
+MG_HX WalkLayout walk_layout(int G, int k, bool lean = false) {
     WalkLayout L;
     L.slots = 0;
     L.nblk = 1;
@@ -199,27 +200,29 @@ MG_HX WalkLayout walk_layout(int G, int k) {
         L.slots += c;
         L.nblk = c > L.nblk ? c : L.nblk;
     }
-    L.bytes = align16(sizeof(Walk)) + align16(10 * 8 * (size_t)L.nblk) +
+    L.bytes = align16(sizeof(Walk)) + align16((lean ? 8 : 10) * 8 * (size_t)L.nblk) +
               align16(4 * 4 * (size_t)L.nblk) + align16(5 * 2 * (size_t)L.slots);
     return L;
 }
 
 // Point a walker's arrays into the shared-memory region right behind its header.
-MG_HX void walk_carve(Walk& w, unsigned char* base, int G, int k) {
-    const WalkLayout L = walk_layout(G, k);
+MG_HX void walk_carve(Walk& w, unsigned char* base, int G, int k, bool lean = false) {
+    const WalkLayout L = walk_layout(G, k, lean);
     unsigned char* p = base + align16(sizeof(Walk));
     double* d = reinterpret_cast<double*>(p);
+    const int n = L.nblk;
     w.pm = d;
-    w.psum = d + L.nblk;
-    w.pmb = d + 2 * L.nblk;
-    w.pP = d + 3 * L.nblk;
-    w.pmx = d + 4 * L.nblk;
-    w.cm = d + 5 * L.nblk;
-    w.cs = d + 6 * L.nblk;
-    w.cb = d + 7 * L.nblk;
-    w.cP = d + 8 * L.nblk;
-    w.cmx = d + 9 * L.nblk;
-    p += align16(10 * 8 * (size_t)L.nblk);
+    w.psum = d + n;
+    w.pmb = d + 2 * n;
+    w.pP = d + 3 * n;
+    w.pmx = lean ? nullptr : d + 4 * n;
+    const int c0 = lean ? 4 : 5;
+    w.cm = d + c0 * n;
+    w.cs = d + (c0 + 1) * n;
+    w.cb = d + (c0 + 2) * n;
+    w.cP = d + (c0 + 3) * n;
+    w.cmx = lean ? nullptr : d + 9 * n;
+    p += align16((lean ? 8 : 10) * 8 * (size_t)L.nblk);
     int* i = reinterpret_cast<int*>(p);
     w.pu = i;
     w.cu = i + L.nblk;

@@ -205,7 +205,9 @@ constexpr int WPC = 4;  // walkers (warps) per CTA
 constexpr size_t SMEM_SPEC = (sizeof(Spec) + 15) & ~size_t(15);
 
 // dynamic shared memory of one CTA for a stage of k modules over G GPUs
-static inline size_t smem_bytes(int G, int k) { return SMEM_SPEC + WPC * walk_layout(G, k).bytes; }
+static inline size_t smem_bytes(int G, int k, bool lean) {
+    return SMEM_SPEC + WPC * walk_layout(G, k, lean).bytes;
+}
 
 // One resident persistent grid per stage search.  Each warp is a walker: it pops a
 // cursor from the shared ring queue and runs the warp-cooperative DFS on it; a busy
@@ -214,7 +216,7 @@ static inline size_t smem_bytes(int G, int k) { return SMEM_SPEC + WPC * walk_la
 //   MIN:   shared incumbent (atomicMin on the fp64 bits), tie band TIE_EPS.
 //   FIRST: hits are ordered by their reference-DFS path; the earliest is kept under a
 //          seqlock, and work that lies after it is abandoned.
-__global__ void __launch_bounds__(32 * WPC, 6) MG_KSEARCH_NAME(const Spec* Sg, Rows R, Cont* Q, int* ready,
+__global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NAME(const Spec* Sg, Rows R, Cont* Q, int* ready,
                                                      Ctl* ctl, HitPath* best, Leaf* leaf_out,
                                                      const Cont* root, long long slot0,
                                                      int ready0) {
@@ -239,10 +241,10 @@ __global__ void __launch_bounds__(32 * WPC, 6) MG_KSEARCH_NAME(const Spec* Sg, R
     }
     const int wid = threadIdx.x >> 5;
     const int lane = lane_id();
-    const size_t wbytes = walk_layout(S.G, S.k).bytes;
+    const size_t wbytes = walk_layout(S.G, S.k, MG_SPECIALIZE).bytes;
     unsigned char* wbase = smem + SMEM_SPEC + wid * wbytes;
     Walk& w = *reinterpret_cast<Walk*>(wbase);
-    if (lane == 0) walk_carve(w, wbase, S.G, S.k);
+    if (lane == 0) walk_carve(w, wbase, S.G, S.k, MG_SPECIALIZE);
     __syncwarp();
     unsigned long long nodes = 0, leaves = 0;
     while (true) {

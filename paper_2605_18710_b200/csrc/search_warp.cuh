@@ -36,11 +36,12 @@ __device__ __forceinline__ int wscan_incl(int v) {
 
 
 __device__ __forceinline__ void parent_stats_warp(const Spec& S, const Rows& R, Walk& w, int j) {
+    double mbx_unused;  // the include_self kernels keep no own-excluded bound
     const int o0 = w.loff[j];
     #pragma unroll 1
     for (int b = lane_id(); b < w.nb[j]; b += 32)
         block_stats(S, R, w.opt, w.bmk[o0 + b], j, w.pu[b], w.pm[b], w.psum[b], w.pmb[b], w.pP[b],
-                    w.pmx[b]);
+                    MG_SELF(S) ? mbx_unused : w.pmx[b]);
     __syncwarp();
 }
 
@@ -816,7 +817,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                     w.cb[pos] = w.pmb[b] > ba ? w.pmb[b] : ba;
                     w.cP[pos] = w.pP[b] * bo;
                     const double bx = ba - S.e2 * bo;
-                    w.cmx[pos] = w.pmx[b] > bx ? w.pmx[b] : bx;
+                    if (!MG_SELF(S)) w.cmx[pos] = w.pmx[b] > bx ? w.pmx[b] : bx;
                     ++pos;
                 } else if (xb > 0) {
                     ++pos;
@@ -829,7 +830,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                     w.cs[pos] = w.psum[b];
                     w.cb[pos] = w.pmb[b];
                     w.cP[pos] = w.pP[b];
-                    w.cmx[pos] = w.pmx[b];
+                    if (!MG_SELF(S)) w.cmx[pos] = w.pmx[b];
                 }
             }
             carry += __shfl_sync(FULLW, inc, 31);
