@@ -116,9 +116,12 @@ int mosaic_gpu_options(mosaic_gpu_ctx* ctx, int module, int32_t* d, int32_t* uni
 /* Surface lookup (perf_model.hpp:124-147) for one module at (d, a). */
 int mosaic_gpu_lookup(mosaic_gpu_ctx* ctx, int module, int d, double a, double out4[4]);
 
-/* Compact entry for the batched evaluator: its GPU list is gpus[gpu_off .. gpu_off+n_gpus). */
+/* Compact entry (StageAllocation::Entry, core.hpp:80-84): its GPU list is
+ * gpus[gpu_off .. gpu_off+n_gpus).  quota = quota_units / quota_levels as in
+ * DeploymentOption::quota() (core.hpp:64-75); quota_levels = 0 means the context's. */
 typedef struct {
     int32_t module, dp_degree, quota_units, n_gpus;
+    int32_t quota_levels, reserved;
     int64_t gpu_off;
 } mosaic_gpu_eval_entry;
 
@@ -212,6 +215,15 @@ int mosaic_gpu_trace_cand(mosaic_gpu_ctx* ctx, int64_t r, int64_t c, uint64_t* m
 /* Drop the EvalCache (solver.hpp:39-75). */
 void mosaic_gpu_clear_cache(mosaic_gpu_ctx* ctx);
 
+/* EvalCache inspection after a solve (solver.hpp:39-75): the cached module sets in
+ * insertion order (*n = their count; masks may be NULL to size), and one entry's
+ * StageEvalResult plus the tau of every FeasibilitySearch::run it replayed, in call
+ * order, with its outcome (1 feasible).  MOSAIC_RANGE if the mask is not cached. */
+int mosaic_gpu_cache_masks(mosaic_gpu_ctx* ctx, uint64_t* masks, int64_t cap, int64_t* n);
+int mosaic_gpu_cache_entry(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_result* out,
+                           double* probe_tau, int32_t* probe_ok, int64_t cap,
+                           int64_t* n_probes);
+
 /* Multi-GPU sharding of the search frontier (one rank per GPU).  The caller
  * supplies an all-gather of `bytes` from every rank (torch.distributed over NCCL
  * in bench.py); the library calls it once per device search with a 16-byte
@@ -224,6 +236,16 @@ int mosaic_gpu_set_shard(mosaic_gpu_ctx* ctx, int rank, int world, mosaic_gpu_al
  * records are {u64 key, f64 value}; mode 0 = MIN (smallest value, then key),
  * mode 1 = FIRST (smallest key).  Writes the winning record index. */
 int mosaic_gpu_merge_records(const void* records, int world, int mode, int* winner);
+
+/* Search-engine knobs for experiments (tools/tune.py); defaults are the measured best and
+ * nothing reads the environment.  Keys: don_depth, don_period (power of two), backoff_ns,
+ * small_tree, deep_after, lookahead, small_grid, generic_kernel, shard_level,
+ * ring_per_walker, trace, and the measurement-only share_rank / share_world (search one
+ * rank's share of a sharded search on this device, unmerged: NOT the stage's answer).
+ * MOSAIC_INVALID_ARGUMENT for an unknown key. */
+int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value);
+/* Device memory held by the context's engine (option table, cursor ring, control). */
+int64_t mosaic_gpu_device_bytes(mosaic_gpu_ctx* ctx);
 
 /* Kernel launches issued by this context so far (evidence for bench.py). */
 int64_t mosaic_gpu_launch_count(mosaic_gpu_ctx* ctx);

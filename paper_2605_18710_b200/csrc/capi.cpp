@@ -193,7 +193,8 @@ int mosaic_gpu_stage_time(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* entr
         for (int64_t i = 0; i < n_allocs; ++i) {
             for (int64_t e = alloc_off[i]; e < alloc_off[i + 1]; ++e) {
                 const auto& E = entries[e];
-                Entry x{E.module, E.dp_degree, E.quota_units, {}};
+                if (E.quota_levels < 0) throw Error(MOSAIC_RANGE, "quota_levels < 0");
+                Entry x{E.module, E.dp_degree, E.quota_units, {}, E.quota_levels};
                 x.gpus.assign(gpus + E.gpu_off, gpus + E.gpu_off + E.n_gpus);
                 allocs[i].push_back(std::move(x));
             }
@@ -256,7 +257,8 @@ int mosaic_gpu_validate_plan(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* e
         for (int64_t s = 0; s < n_stages; ++s)
             for (int64_t e = stage_off[s]; e < stage_off[s + 1]; ++e) {
                 const auto& E = entries[e];
-                Entry x{E.module, E.dp_degree, E.quota_units, {}};
+                if (E.quota_levels < 0) throw Error(MOSAIC_RANGE, "quota_levels < 0");
+                Entry x{E.module, E.dp_degree, E.quota_units, {}, E.quota_levels};
                 x.gpus.assign(gpus + E.gpu_off, gpus + E.gpu_off + E.n_gpus);
                 st[s].push_back(std::move(x));
             }
@@ -265,6 +267,31 @@ int mosaic_gpu_validate_plan(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* e
         if (code.empty()) code = "Ok";
         std::snprintf(code_out, code_cap, "%s", code.c_str());
         g_err = msg;
+        return MOSAIC_OK;
+    });
+}
+
+int mosaic_gpu_cache_masks(mosaic_gpu_ctx* ctx, uint64_t* masks, int64_t cap, int64_t* n) {
+    return guard([&] {
+        const auto& o = ctx->pl->cache_order();
+        if (n) *n = (int64_t)o.size();
+        for (int64_t i = 0; masks && i < (int64_t)o.size() && i < cap; ++i) masks[i] = o[i];
+        return MOSAIC_OK;
+    });
+}
+
+int mosaic_gpu_cache_entry(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_result* out,
+                           double* probe_tau, int32_t* probe_ok, int64_t cap,
+                           int64_t* n_probes) {
+    return guard([&] {
+        const StageResult* r = ctx->pl->cache_find(mask);
+        if (!r) throw Error(MOSAIC_RANGE, "module set not in the EvalCache");
+        if (out) fill_stage(*r, out);
+        if (n_probes) *n_probes = (int64_t)r->probe_tau.size();
+        for (int64_t i = 0; i < (int64_t)r->probe_tau.size() && i < cap; ++i) {
+            if (probe_tau) probe_tau[i] = r->probe_tau[i];
+            if (probe_ok) probe_ok[i] = r->probe_ok[i];
+        }
         return MOSAIC_OK;
     });
 }
@@ -306,7 +333,8 @@ int mosaic_gpu_simulate(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* entrie
         for (int64_t s = 0; s < n_stages; ++s)
             for (int64_t e = stage_off[s]; e < stage_off[s + 1]; ++e) {
                 const auto& E = entries[e];
-                Entry x{E.module, E.dp_degree, E.quota_units, {}};
+                if (E.quota_levels < 0) throw Error(MOSAIC_RANGE, "quota_levels < 0");
+                Entry x{E.module, E.dp_degree, E.quota_units, {}, E.quota_levels};
                 x.gpus.assign(gpus + E.gpu_off, gpus + E.gpu_off + E.n_gpus);
                 st[s].push_back(std::move(x));
             }
@@ -388,6 +416,33 @@ int mosaic_gpu_set_shard(mosaic_gpu_ctx* ctx, int rank, int world, mosaic_gpu_al
         return MOSAIC_OK;
     });
 }
+
+int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value) {
+    return guard([&] {
+        mg::Tuning& t = ctx->pl->engine().tuning();
+        const std::string k = key ? key : "";
+        const long long v = (long long)value;
+        if (k == "don_depth") t.don_depth = (int)v;
+        else if (k == "don_period") {
+            if (v < 1 || (v & (v - 1))) throw Error(MOSAIC_INVALID_ARGUMENT, "don_period: power of two");
+            t.don_period = (int)v;
+        } else if (k == "backoff_ns") t.backoff_cap = (int)v;
+        else if (k == "small_tree") t.small_tree = value;
+        else if (k == "deep_after") t.deep_after = v;
+        else if (k == "lookahead") t.lookahead = (int)v;
+        else if (k == "small_grid") t.small_grid = (int)std::max(1LL, v);
+        else if (k == "generic_kernel") t.generic_kernel = v != 0;
+        else if (k == "shard_level") t.shard_level = (int)v;
+        else if (k == "ring_per_walker") t.ring_per_walker = (int)std::max(1LL, v);
+        else if (k == "trace") t.trace = v != 0;
+        else if (k == "share_rank") t.share_rank = (int)v;
+        else if (k == "share_world") t.share_world = (int)std::max(1LL, v);
+        else throw Error(MOSAIC_INVALID_ARGUMENT, "unknown tuning key " + k);
+        return MOSAIC_OK;
+    });
+}
+
+int64_t mosaic_gpu_device_bytes(mosaic_gpu_ctx* ctx) { return ctx->pl->engine().device_bytes(); }
 
 int mosaic_gpu_merge_records(const void* records, int world, int mode, int* winner) {
     struct Rec {

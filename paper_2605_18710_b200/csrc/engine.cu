@@ -117,16 +117,6 @@ static inline size_t pin_off(int i) {
 }
 
 Engine::Engine(int device) : device_(device) {
-    trace_ = std::getenv("MOSAIC_TRACE") != nullptr;
-    if (const char* e = std::getenv("MOSAIC_DON_DEPTH")) don_depth_ = std::atoi(e);
-    if (const char* e = std::getenv("MOSAIC_DON_PERIOD")) don_period_ = std::atoi(e);
-    if (const char* e = std::getenv("MOSAIC_BACKOFF_NS")) backoff_cap_ = std::atoi(e);
-    if (const char* e = std::getenv("MOSAIC_SMALL_TREE")) small_tree_ = std::atof(e);
-    if (const char* e = std::getenv("MOSAIC_DEEP_AFTER")) deep_after_ = std::atoll(e);
-    if (const char* e = std::getenv("MOSAIC_LOOKAHEAD")) lookahead_ = std::atoi(e);
-    if (const char* e = std::getenv("MOSAIC_SMALL_GRID")) small_grid_ = std::atoi(e);
-    no_fast_ = std::getenv("MOSAIC_GENERIC_KERNEL") != nullptr;
-    if (const char* e = std::getenv("MOSAIC_SHARD_LEVEL")) shard_level_ = std::atoi(e);
     CK(cudaSetDevice(device));
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -147,6 +137,7 @@ Engine::Engine(int device) : device_(device) {
     evm1_ = f;
     // device mirror of the pinned staging layout: one upload and one read-back per search
     CK(cudaMalloc(&d_blob_, pin_off(5)));
+    dev_bytes_ += (long long)pin_off(5);
     d_spec_ = static_cast<char*>(d_blob_) + pin_off(0);
     d_ctl_ = static_cast<char*>(d_blob_) + pin_off(1);
     d_leaf_ = static_cast<char*>(d_blob_) + pin_off(2);
@@ -204,6 +195,7 @@ void Engine::upload_rows(const Model& M) {
     CK(cudaMalloc(&d_bound_, n * 8));
     CK(cudaMalloc(&d_d_, n * 4));
     CK(cudaMalloc(&d_u_, n * 4));
+    dev_bytes_ += (long long)n * 40;
     if (!base.empty()) {
         CK(cudaMemcpy(d_base_, base.data(), base.size() * 8, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(d_B_, B.data(), B.size() * 8, cudaMemcpyHostToDevice));
@@ -214,16 +206,24 @@ void Engine::upload_rows(const Model& M) {
     }
 }
 
+// The cursor ring only has to hold the pieces in flight: donations happen when the queue
+// is empty and walkers are idle, and a donation into a full ring simply fails (the walker
+// keeps the work), so a ring of ring_per_walker slots per resident walker is always safe.
 void Engine::ensure_front(long long n) {
     if (n <= front_cap_) return;
     long long cap = std::max<long long>(n, 1024);
+    if (front_cap_) dev_bytes_ -= front_cap_ * (long long)(sizeof(Cont) + sizeof(int));
     cudaFree(d_front_[0]);
     CK(cudaMalloc(&d_front_[0], cap * sizeof(Cont)));
     cudaFree(d_ready_);
     CK(cudaMalloc(&d_ready_, cap * sizeof(int)));
     CK(cudaMemset(d_ready_, 0, cap * sizeof(int)));
+    dev_bytes_ += cap * (long long)(sizeof(Cont) + sizeof(int));
     ticket_base_ = 0;
-    if (!d_best_) CK(cudaMalloc(&d_best_, sizeof(HitPath)));
+    if (!d_best_) {
+        CK(cudaMalloc(&d_best_, sizeof(HitPath)));
+        dev_bytes_ += sizeof(HitPath);
+    }
     front_cap_ = cap;
 }
 
@@ -233,8 +233,6 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     cudaStream_t s = S_(stream_);
     SearchResult res;
     res.value = ub;
-    const long long cap = cap_front;
-    ensure_front(cap);
     Rows R{d_base_, d_B_, d_fp_, d_bound_, d_d_, d_u_};
     char* pin = reinterpret_cast<char*>(h_pin_);
     Spec* hs = reinterpret_cast<Spec*>(pin + pin_off(0));
@@ -245,25 +243,22 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     *hs = S;
     hs->shard_rank = rank_;
     hs->shard_world = world_;
-    if (const char* e = std::getenv("MOSAIC_SHARD_SIM")) {  // "r/w": measure one rank's share
-        int r = 0, wd = 1;
-        if (std::sscanf(e, "%d/%d", &r, &wd) == 2 && wd >= 1 && r >= 0 && r < wd) {
-            hs->shard_rank = r;
-            hs->shard_world = wd;
-        }
+    if (world_ == 1 && tune_.share_world > 1) {
+        hs->shard_rank = tune_.share_rank;
+        hs->shard_world = tune_.share_world;
     }
     // option prefixes (o_0, o_1, o_2) are hashed to ranks: at 8 ranks the largest share of the
     // dominant cfg5 proof is 1.15x the mean (pairs: 1.3x; tools/shard_levels.sh)
     hs->shard_level = S.k >= 3 ? 2 : S.k - 1;
-    if (shard_level_ >= 0) hs->shard_level = std::min(shard_level_, S.k - 1);
+    if (tune_.shard_level >= 0) hs->shard_level = std::min(tune_.shard_level, S.k - 1);
     // donation policy: hand over only shallow levels, when the queue has run dry
-    hs->don_max_level = S.k >= 6 ? S.k - 1 - don_depth_ : (S.k >= 3 ? S.k - 3 : 0);
+    hs->don_max_level = S.k >= 6 ? S.k - 1 - tune_.don_depth : (S.k >= 3 ? S.k - 3 : 0);
     // long-running pieces may also hand over levels <= k-3 (see WarpHooks::abort)
     hs->don_max_level_tail = S.k - 3 > hs->don_max_level ? S.k - 3 : hs->don_max_level;
-    hs->deep_after = deep_after_;
-    hs->lookahead = lookahead_;
-    hs->don_period = don_period_;
-    hs->backoff_cap_ns = backoff_cap_;
+    hs->deep_after = tune_.deep_after;
+    hs->lookahead = tune_.lookahead;
+    hs->don_period = tune_.don_period;
+    hs->backoff_cap_ns = tune_.backoff_cap;
     std::memset(hc, 0, sizeof(Ctl));
     union {
         double d;
@@ -273,11 +268,8 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     hc->inc = cv.u;
     hc->abort_below = abort_below;
     // tickets keep counting across searches, so slots never need clearing: a stale
-    // ready value belongs to an older (smaller) ticket and can never match
-    const unsigned long long t0 = ticket_base_;
-    hc->q_head = t0;
-    hc->q_tail = t0 + 1;
-    hc->q_cap = (unsigned long long)cap;
+    // ready value belongs to an older (smaller) ticket and can never match (q_head/q_tail
+    // are set once the ring is sized, below)
     hc->outstanding = 1;
     std::memset(hr, 0, sizeof(Cont));
     hr->depth = 0;
@@ -287,9 +279,8 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     hr->oe = (int16_t)S.lvl_n[0];
     hr->bsz[0] = (uint16_t)S.G;
     *hone = 1;
-    Cont* Q = reinterpret_cast<Cont*>(d_front_[0]);
     // the specialised kernel when the model is the common one (same search, fewer branches)
-    const bool fast = S.include_self && S.nonneg && !S.additive && !no_fast_;
+    const bool fast = S.include_self && S.nonneg && !S.additive && !tune_.generic_kernel;
     const size_t smem = smem_bytes(S.G, S.k, fast);
     const void* kfn = !fast ? reinterpret_cast<const void*>(&k_search)
                       : S.mode == MODE_MIN ? k_search_fast_min_fn() : k_search_fast_first_fn();
@@ -307,11 +298,18 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
         grid_smem_[ki] = smem;
     }
     grid_ = grid_k_[ki];
+    ensure_front(grid_ * WPC * std::max(1, tune_.ring_per_walker));
+    const long long cap = front_cap_;
+    const unsigned long long t0 = ticket_base_;
+    hc->q_head = t0;
+    hc->q_tail = t0 + 1;
+    hc->q_cap = (unsigned long long)cap;
+    Cont* Q = reinterpret_cast<Cont*>(d_front_[0]);
     // small trees (few option tuples) do not need the whole GPU: a handful of resident
     // CTAs finishes them without spinning up thousands of idle walkers
     double tuples = 1.0;
     for (int l = 0; l < S.k; ++l) tuples *= (double)(S.lvl_n[l] > 0 ? S.lvl_n[l] : 1);
-    const long long grid = (tuples * S.G <= small_tree_) ? std::min<long long>(grid_, small_grid_) : grid_;
+    const long long grid = (tuples * S.G <= tune_.small_tree) ? std::min<long long>(grid_, tune_.small_grid) : grid_;
     hc->walkers = (unsigned)(grid * WPC);
     // small trees: hand-overs cost more than they parallelise (each is a 1.3 KB piece
     // round trip through L2); let the walker that owns the root finish it
@@ -369,7 +367,7 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     }
     // ranks must leave every search with the same answer (they replay the same control
     // flow and all-gather once per search): merge after the local result is complete
-    if (world_ > 1) merge_ranks(S, hc, res);
+    if (world_ > 1 && ag_) merge_ranks(S, hc, res);
     float kms = 0, ms = 0;
     CK(cudaEventElapsedTime(&kms, (cudaEvent_t)evk0_, (cudaEvent_t)evk1_));
     CK(cudaEventElapsedTime(&ms, (cudaEvent_t)ev0_, (cudaEvent_t)ev1_));
@@ -380,7 +378,7 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     st.leaves += (long long)hc->leaves;
     ++st.searches;
     alg_bytes_ += (long long)hc->leaves * 24LL * S.k;  // k option rows x 3 fp64 per leaf
-    if (trace_)
+    if (tune_.trace)
         std::fprintf(stderr, "[mosaic] %s k=%d thr=%.17g kernel=%.3fms total=%.3fms nodes=%llu "
                              "leaves=%llu donated=%llu %s\n",
                      S.mode == MODE_MIN ? "MIN  " : "FIRST", S.k,

@@ -30,6 +30,27 @@ struct EvalEntry {  // device evaluator input (one per allocation entry)
     long long gpu_off;
 };
 
+// Search-engine knobs.  Defaults are the measured best; nothing reads the
+// environment — experiments set them through mosaic_gpu_set_tuning().
+struct Tuning {
+    int don_depth = 3;      // donate levels <= k-1-don_depth (measured best on cfg5)
+    int don_period = 4;     // power of two; control reads every 4 steps (tools/knob_solve.sh)
+    int backoff_cap = 2048; // ns, idle walkers polling back-off cap (measured)
+    double small_tree = 2e5;  // option tuples x G below which small_grid CTAs run the search
+    long long deep_after = 16384;  // steps on one piece before deeper hand-overs are allowed
+    // child look-ahead (can every remaining level still place an option?): off by default —
+    // the lane-parallel option screen at the next level does the same job for less
+    int lookahead = 0;
+    int small_grid = 8;     // CTAs for small trees
+    int generic_kernel = 0; // never use the specialised kernels
+    int shard_level = -1;   // override of the sharded option-prefix level (-1: default)
+    int ring_per_walker = 16;  // cursor-ring slots per resident walker
+    int trace = 0;          // one stderr line per device search
+    // measurement only (tools/): search rank share_rank's share of a share_world-way
+    // sharded search on this one device, without merging — NOT the stage's answer
+    int share_rank = 0, share_world = 1;
+};
+
 class Engine {
   public:
     explicit Engine(int device);
@@ -49,12 +70,17 @@ class Engine {
                   std::vector<double>& st_out, std::vector<double>& rect_out);
     double eval_ms() const { return eval_ms_; }
 
+    // fn == nullptr with world > 1: measure this rank's share only (no merge; the result
+    // is NOT the stage's answer — used to simulate shard balance on one device)
     void set_shard(int rank, int world, AllGatherFn fn, void* user) {
         rank_ = rank;
         world_ = world;
         ag_ = fn;
         ag_user_ = user;
     }
+    Tuning& tuning() { return tune_; }
+    // bytes of device memory the engine holds (option table, ring, control blocks)
+    long long device_bytes() const { return dev_bytes_; }
     long long launches() const { return launches_; }
     double search_ms() const { return search_ms_; }
     void reset_counters() {
@@ -77,7 +103,6 @@ class Engine {
     // device-side timing marks on the engine stream (bench.py)
     void mark(int which);
     double marked_ms();
-    long long cap_front = 1 << 20; // cursors in flight
 
   private:
     void ensure_front(long long n);
@@ -105,19 +130,9 @@ class Engine {
     // [generic, specialised MIN, specialised FIRST]
     size_t grid_smem_[3] = {0, 0, 0}, smem_attr_[3] = {0, 0, 0};
     long long grid_k_[3] = {0, 0, 0};
-    bool trace_ = false;
-    int don_depth_ = 3;    // donate levels <= k-1-don_depth (measured best on cfg5)
-    int don_period_ = 4;   // power of two; control reads every 4 steps (tools/knob_solve.sh)
-    int backoff_cap_ = 2048;  // ns, idle walkers polling back-off cap (measured)
-    double small_tree_ = 2e5;  // option tuples x G below which 8 CTAs run the search
+    Tuning tune_;
     unsigned long long ticket_base_ = 0;
-    // child look-ahead (can every remaining level still place an option?): off by default —
-    // the lane-parallel option screen at the next level does the same job for less
-    int lookahead_ = 0;
-    int small_grid_ = 8;  // CTAs for small trees
-    bool no_fast_ = false;  // MOSAIC_GENERIC_KERNEL: never use the specialised kernel
-    int shard_level_ = -1;  // override of the sharded option-prefix level (-1: default)
-    long long deep_after_ = 16384;  // steps on one piece before deeper hand-overs are allowed
+    long long dev_bytes_ = 0;
     long long front_cap_ = 0;
     void* h_pin_ = nullptr;
     long long launches_ = 0;

@@ -166,7 +166,7 @@ bool Planner::first_leaf(const std::vector<int>& order, bool filter, double thet
     mg::HitPath hp;
     Leaf sl;
     const bool seeded = seed && make_seed(*seed, order, filter, theta, seed_value, hp, sl);
-    if (seed && std::getenv("MOSAIC_TRACE"))
+    if (seed && eng_->tuning().trace)
         std::fprintf(stderr, "[mosaic] FIRST seed %s (theta=%.17g value=%.17g)\n",
                      seeded ? "applied" : "rejected", theta, seed_value);
     mg::SearchResult r = eng_->search(S, POS_INF, 0.0, st, seeded ? &hp : nullptr,
@@ -201,18 +201,6 @@ double Planner::min_value(const std::vector<int>& mods, double ub, mg::SearchSta
         q.mode = MODE_MIN;
         q.ub = ub;
         for (auto& [c, m] : cnt) q.level_module.push_back(m);
-        if (const char* e = std::getenv("MOSAIC_MIN_ORDER")) {  // experiments: "3,0,1,..."
-            std::vector<int> o;
-            for (const char* p = e; *p;) {
-                o.push_back(std::atoi(p));
-                while (*p && *p != ',') ++p;
-                if (*p == ',') ++p;
-            }
-            std::vector<int> a = o, b = mods;
-            std::sort(a.begin(), a.end());
-            std::sort(b.begin(), b.end());
-            if (a == b) q.level_module = o;
-        }
         mg::Spec S;
         if (!mg::build_spec(M_, q, S)) return ub;
         double ab = ub >= POS_INF ? POS_INF : ub * (1.0 - 1e-4);
@@ -281,7 +269,7 @@ StageResult Planner::stage_eval(uint64_t mask) {
     std::vector<Entry> argmin;  // an allocation reaching Tstar
     long long probes = 0;
     // FeasibilitySearch::run(tau) replayed: first leaf in fail-first DFS order.
-    auto run = [&](double tau, Leaf& leaf, std::vector<int>& order) -> bool {
+    auto run_probe = [&](double tau, Leaf& leaf, std::vector<int>& order) -> bool {
         ++probes;
         const double th = tau * (1.0 + 1e-12);
         std::vector<std::pair<int, int>> cnt;
@@ -301,6 +289,12 @@ StageResult Planner::stage_eval(uint64_t mask) {
         // seed with the argmin allocation when it is known to satisfy this probe
         const bool seed = nonneg && have_T && !argmin.empty() && Tstar <= th;
         return first_leaf(order, true, th, leaf, res.st, seed ? &argmin : nullptr, Tstar);
+    };
+    auto run = [&](double tau, Leaf& leaf, std::vector<int>& order) -> bool {
+        const bool ok = run_probe(tau, leaf, order);
+        res.probe_tau.push_back(tau);
+        res.probe_ok.push_back(ok ? 1 : 0);
+        return ok;
     };
     Leaf best, cur;
     std::vector<int> best_order, cur_order;
@@ -387,7 +381,7 @@ std::string Planner::validate_plan(const std::vector<std::vector<Entry>>& stages
             std::sort(g.begin(), g.end());
             if (std::adjacent_find(g.begin(), g.end()) != g.end())
                 return fail("SmOvercommit", "replica co-location on one GPU for " + P_.modules[e.module].id);
-            const double a = (double)e.units / P_.quota_levels;
+            const double a = (double)e.units / (e.levels ? e.levels : P_.quota_levels);
             const double fp = P_.modules[e.module].surface.lookup(e.d, a).memory +
                               P_.modules[e.module].memory_base;
             for (int r : e.gpus) {
@@ -417,15 +411,6 @@ double Planner::stage_min(uint64_t mask, double ub, bool restart, mg::SearchStat
     q.mode = MODE_MIN;
     q.ub = ub;
     q.level_module = mods;
-    if (const char* e = std::getenv("MOSAIC_MIN_ORDER")) {
-        std::vector<int> o;
-        for (const char* p = e; *p;) {
-            o.push_back(std::atoi(p));
-            while (*p && *p != ',') ++p;
-            if (*p == ',') ++p;
-        }
-        if (o.size() == mods.size()) q.level_module = o;
-    }
     mg::Spec S;
     if (!mg::build_spec(M_, q, S)) return ub;
     mg::SearchResult r = eng_->search(S, ub, 0.0, st);
@@ -481,12 +466,22 @@ StageResult Planner::exact_stage(uint64_t mask) {
         res.status = INFEASIBLE;
         return res;
     }
+    // MIN returns I* with T* in [I*(1 - TIE_EPS - rounding), I*].  Resolve the band
+    // exactly: FIRST(theta) yields a leaf of value v <= theta; keep lowering theta below v
+    // until no leaf remains — then v == T* and the last FIRST(T*) leaf is the first argmin
+    // in module-index DFS order, i.e. ExactStageSolver's strict-'<' result (oracle.hpp:120).
     double T = min_value(mods, first.value, res.st);
     Leaf lf;
     if (!first_leaf(mods, false, T, lf, res.st))
         throw Error(CUDA, "exact search lost the argmin leaf");
+    for (int guard = 0; guard < 64; ++guard) {
+        Leaf lower;
+        const double below = std::nextafter(lf.value, -POS_INF);
+        if (!first_leaf(mods, false, below, lower, res.st)) break;
+        lf = lower;
+    }
     res.status = OK;
-    res.stage_time = T;
+    res.stage_time = lf.value;
     res.entries = leaf_entries(mods, lf);
     return res;
 }
@@ -511,7 +506,7 @@ std::optional<StageResult> Planner::evaluate_cached(uint64_t mask, bool* hit, Pl
         throw Error(MODULE_NO_OPTION, "module has no feasible deployment option");
     if (r.status != OK) return std::nullopt;
     pr.feasibility_calls += r.probes;
-    if (P_.enable_cache) cache_.emplace(mask, r);
+    if (P_.enable_cache && cache_.emplace(mask, r).second) cache_order_.push_back(mask);
     return r;
 }
 
@@ -520,7 +515,7 @@ PlanResult Planner::solve() {
     PlanResult pr;
     const int n = (int)P_.modules.size();
     if (n == 0) throw Error(EMPTY, "model graph has no modules");
-    cache_.clear();
+    clear_cache();
     auto reach = reachability_masks(P_);
     std::vector<uint64_t> masks;
     std::vector<StageResult> results;
@@ -709,13 +704,14 @@ void Planner::stage_time(const std::vector<std::vector<Entry>>& allocs, std::vec
         for (const auto& e : a) {
             if (e.module < 0 || e.module >= (int)P_.modules.size())
                 throw Error(RANGE, "module not in graph");
-            uint64_t key = (uint64_t)e.module << 40 | (uint64_t)(uint32_t)e.d << 20 |
-                           (uint64_t)(uint32_t)e.units;
+            const int lv = e.levels ? e.levels : P_.quota_levels;
+            const uint64_t key = (uint64_t)e.module << 48 | (uint64_t)(uint32_t)e.d << 32 |
+                                 (uint64_t)(uint32_t)e.units << 16 | (uint64_t)(uint32_t)lv;
             auto it = row_of.find(key);
             int row;
             if (it == row_of.end()) {
                 const Surface& s = P_.modules[e.module].surface;
-                double a = (double)e.units / P_.quota_levels;
+                double a = (double)e.units / lv;
                 base.push_back(s.lookup(e.d, a).latency);      // PerfContext::base_latency
                 Bt.push_back(s.lookup(1, a).bandwidth_util);   // PerfContext::solo_bandwidth
                 row = (int)base.size() - 1;
@@ -956,7 +952,7 @@ void Planner::simulate(const std::vector<std::vector<Entry>>& stages, const mg::
             size_t first = i;
             for (size_t j = 0; j < i; ++j)
                 if (stages[s][j].module == e.module) { first = j; break; }
-            const double q = (double)e.units / P_.quota_levels;
+            const double q = (double)e.units / (e.levels ? e.levels : P_.quota_levels);
             const Sample smp = P_.modules[e.module].surface.lookup(e.d, q);
             mg::SimEntry se{};
             se.dur0 = rect[s][first];

@@ -35,6 +35,7 @@ struct Error : std::runtime_error {
 struct Entry {
     int module, d, units;
     std::vector<int> gpus;
+    int levels = 0;  // DeploymentOption::quota_levels; 0 = the problem's
 };
 
 struct StageResult {
@@ -43,6 +44,11 @@ struct StageResult {
     std::vector<Entry> entries;  // sorted by module index
     long long probes = 0;        // FeasibilitySearch::run calls replayed
     mg::SearchStats st;
+    // every replayed FeasibilitySearch::run(tau) in call order and its outcome (probes
+    // decided from T* without a device search included): the trajectory parity tests
+    // replay against the reference
+    std::vector<double> probe_tau;
+    std::vector<uint8_t> probe_ok;
 };
 
 struct TraceCand {
@@ -99,7 +105,16 @@ class Planner {
                   std::vector<double>& mean_busy, std::vector<mg::SimInterval>* timeline);
 
     mg::Engine& engine() { return *eng_; }
-    void clear_cache() { cache_.clear(); }
+    void clear_cache() {
+        cache_.clear();
+        cache_order_.clear();
+    }
+    // EvalCache contents in insertion order (solver.hpp:39-75)
+    const std::vector<uint64_t>& cache_order() const { return cache_order_; }
+    const StageResult* cache_find(uint64_t mask) const {
+        auto it = cache_.find(mask);
+        return it == cache_.end() ? nullptr : &it->second;
+    }
 
   private:
     void check_rows(int m) const;
@@ -122,6 +137,7 @@ class Planner {
     std::vector<std::string> opt_err_;
     std::unique_ptr<mg::Engine> eng_;
     std::unordered_map<uint64_t, StageResult> cache_;
+    std::vector<uint64_t> cache_order_;
 };
 
 }  // namespace mosaic_b200

@@ -220,17 +220,8 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
                                                      Ctl* ctl, HitPath* best, Leaf* leaf_out,
                                                      const Cont* root, long long slot0,
                                                      int ready0) {
+    (void)slot0;
     extern __shared__ __align__(16) unsigned char smem[];
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
-        // publish the root piece (shipped with the Spec / Ctl upload): walkers that took
-        // its ticket spin on ready[slot0] until it is there
-        const int4* src = reinterpret_cast<const int4*>(root);
-        int4* dst = reinterpret_cast<int4*>(Q + slot0);
-        for (int i = threadIdx.x; i < (int)(sizeof(Cont) / 16); i += 32) dst[i] = src[i];
-        __threadfence();
-        __syncwarp();
-        if (threadIdx.x == 0) *(volatile int*)&ready[slot0] = ready0;
-    }
     Spec& S = *reinterpret_cast<Spec*>(smem);
     {
         const int n = sizeof(Spec) / 4;
@@ -273,7 +264,9 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
                 backoff = backoff < backoff_cap ? backoff * 2 : backoff_cap;
             }
             if (idle) atomicSub(&ctl->idle, 1u);
-            if (ticket >= 0) {
+            // the root piece ships with the launch (`root`), every other piece is published
+            // in the ring by its donor
+            if (ticket >= 0 && ticket + 1 != ready0) {
                 const long long slot = (long long)((unsigned long long)ticket % ctl->q_cap);
                 while (*(volatile int*)&ready[slot] != (int)(ticket + 1)) __nanosleep(32);
                 __threadfence();
@@ -283,7 +276,8 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
         if (ticket < 0) break;
         const long long slot = (long long)((unsigned long long)ticket % ctl->q_cap);
         __threadfence();
-        load_cont_warp(Q[slot], w, MG_MODE(S) == MODE_FIRST);
+        const Cont& piece = ticket + 1 == ready0 ? *root : Q[slot];
+        load_cont_warp(piece, w, MG_MODE(S) == MODE_FIRST);
         WarpHooks h;
         h.ctl = ctl;
         h.mode = MG_MODE(S);
@@ -302,7 +296,7 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
         h.deep_after = S.deep_after;
         h.inc_cache = POS_INF;
         h.inc_cache = h.bcast_inc();
-        const int d0 = Q[slot].depth;
+        const int d0 = piece.depth;
         dfs_warp(S, R, w, d0, h);
         nodes += h.nodes;
         leaves += h.leaves;

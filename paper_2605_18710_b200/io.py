@@ -8,6 +8,7 @@ interference.json` straight to the B200 planner and get a plan JSON with the sam
 from __future__ import annotations
 
 import json
+import math
 from typing import Any, Optional
 
 from . import mosaic
@@ -128,7 +129,9 @@ def load_scenario(model, cluster, profile, interference, granularity: Optional[f
     s = surfaces_from_json(profile)
     im = interference_from_json(interference)
     if quota_levels is None:
-        quota_levels = int(round(1.0 / (granularity if granularity else 0.1)))
+        q = 1.0 / (granularity if granularity else 0.1)
+        # std::lround: halves away from zero (Python's round() is banker's rounding)
+        quota_levels = int(math.floor(q + 0.5)) if q >= 0 else -int(math.floor(-q + 0.5))
     ids = [m["id"] for m in g["modules"]]
     mods = []
     for m in g["modules"]:

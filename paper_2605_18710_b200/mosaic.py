@@ -130,7 +130,8 @@ class StageResultC(C.Structure):
 
 class EvalEntryC(C.Structure):
     _fields_ = [("module", C.c_int32), ("dp_degree", C.c_int32), ("quota_units", C.c_int32),
-                ("n_gpus", C.c_int32), ("gpu_off", C.c_int64)]
+                ("n_gpus", C.c_int32), ("quota_levels", C.c_int32), ("pad", C.c_int32),
+                ("gpu_off", C.c_int64)]
 
 
 class PlanResultC(C.Structure):
@@ -159,6 +160,8 @@ EXPORTS = [
     "mosaic_gpu_h2d_bytes", "mosaic_gpu_d2h_bytes", "mosaic_gpu_mark", "mosaic_gpu_marked_ms", "mosaic_gpu_alg_bytes", "mosaic_gpu_stage_min",
     "mosaic_gpu_validate_plan", "mosaic_gpu_generate_surfaces", "mosaic_gpu_synth_workloads",
     "mosaic_gpu_baseline_plan", "mosaic_gpu_simulate",
+    "mosaic_gpu_cache_masks", "mosaic_gpu_cache_entry", "mosaic_gpu_set_tuning",
+    "mosaic_gpu_device_bytes",
 ]
 
 _lib = None
@@ -228,6 +231,11 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                           P(C.c_int64)]),
         "mosaic_gpu_validate_plan": (C.c_int, [vp, P(EvalEntryC), P(C.c_int32), P(C.c_int64),
                                                C.c_int64, C.c_char_p, C.c_size_t]),
+        "mosaic_gpu_set_tuning": (C.c_int, [vp, C.c_char_p, C.c_double]),
+        "mosaic_gpu_device_bytes": (C.c_int64, [vp]),
+        "mosaic_gpu_cache_masks": (C.c_int, [vp, P(C.c_uint64), C.c_int64, P(C.c_int64)]),
+        "mosaic_gpu_cache_entry": (C.c_int, [vp, C.c_uint64, P(StageResultC), P(C.c_double),
+                                             P(C.c_int32), C.c_int64, P(C.c_int64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -536,7 +544,7 @@ class Planner:
         for a in allocs:
             for e in a.entries:
                 ents.append(EvalEntryC(e.module, e.option.dp_degree, e.option.quota_units,
-                                       len(e.gpus), len(gpus)))
+                                       len(e.gpus), e.option.quota_levels, 0, len(gpus)))
                 gpus.extend(e.gpus)
             off.append(len(ents))
         n = len(allocs)
@@ -568,7 +576,7 @@ class Planner:
         for st in plan.stages:
             for e in st.entries:
                 ents.append(EvalEntryC(e.module, e.option.dp_degree, e.option.quota_units,
-                                       len(e.gpus), len(gpus)))
+                                       len(e.gpus), e.option.quota_levels, 0, len(gpus)))
                 gpus.extend(e.gpus)
             off.append(len(ents))
         n, S, G = len(seeds), len(plan.stages), self.gpu_count
@@ -602,7 +610,7 @@ class Planner:
         for st in plan.stages:
             for e in st.entries:
                 ents.append(EvalEntryC(e.module, e.option.dp_degree, e.option.quota_units,
-                                       len(e.gpus), len(gpus)))
+                                       len(e.gpus), e.option.quota_levels, 0, len(gpus)))
                 gpus.extend(e.gpus)
             off.append(len(ents))
         E = (EvalEntryC * max(1, len(ents)))(*ents)
@@ -639,8 +647,38 @@ class Planner:
     def marked_ms(self) -> float:
         return load_library().mosaic_gpu_marked_ms(self._ctx)
 
+    def set_tuning(self, **knobs: float) -> None:
+        """Search-engine knobs for experiments (include/mosaic_gpu.h, mosaic_gpu_set_tuning)."""
+        for k, v in knobs.items():
+            _raise(load_library().mosaic_gpu_set_tuning(self._ctx, k.encode(), float(v)))
+
+    def device_bytes(self) -> int:
+        return load_library().mosaic_gpu_device_bytes(self._ctx)
+
     def clear_cache(self) -> None:
         load_library().mosaic_gpu_clear_cache(self._ctx)
+
+    def eval_cache(self) -> list[tuple[int, StageEvalResult, list[tuple[float, bool]]]]:
+        """EvalCache after a solve, in insertion order: (mask, result, probes), where probes
+        are the (tau, feasible) of every FeasibilitySearch::run the stage_eval replayed."""
+        L = load_library()
+        n = C.c_int64()
+        _raise(L.mosaic_gpu_cache_masks(self._ctx, None, 0, C.byref(n)))
+        masks = (C.c_uint64 * max(1, n.value))()
+        _raise(L.mosaic_gpu_cache_masks(self._ctx, masks, n.value, C.byref(n)))
+        out = []
+        for m in masks[:n.value]:
+            r = StageResultC()
+            npb = C.c_int64()
+            _raise(L.mosaic_gpu_cache_entry(self._ctx, m, C.byref(r), None, None, 0,
+                                            C.byref(npb)))
+            tau = (C.c_double * max(1, npb.value))()
+            ok = (C.c_int32 * max(1, npb.value))()
+            _raise(L.mosaic_gpu_cache_entry(self._ctx, m, C.byref(r), tau, ok, npb.value,
+                                            C.byref(npb)))
+            out.append((int(m), self._stage(r),
+                        [(tau[i], bool(ok[i])) for i in range(npb.value)]))
+        return out
 
     def set_shard(self, rank: int, world: int, allgather=None) -> None:
         """allgather(send: bytes) -> list[bytes] over ranks (torch.distributed in bench.py)."""
