@@ -138,7 +138,7 @@ def _probe_jobs(name: str, sh: dict, c: dict) -> list:
     lv = f"levels={sh['levels']}"
     mask = str(c["mask"])
     ok = [float.fromhex(t) for t, o in c["probes"] if o]
-    out = [(c["k"] - 0.5, f"{name}|feas_last_ok|{mask}",
+    out = [(c["k"] - 10.0, f"{name}|feas_last_ok|{mask}",
             [sh["spec"], "feas", mask, repr(ok[-1]), lv])]
     t_last, ok_last = c["probes"][-1]
     if not ok_last:
@@ -193,7 +193,8 @@ def status() -> None:
                                            else f"{q['wall_s']:.1f}s")
             else:
                 o = r.get("out", {})
-                same = o.get("t") == c["t"]
+                same = ("t" in o and float.fromhex(o["t"]) == float.fromhex(c["t"])
+                        and o.get("alloc") == c["alloc"])
                 st = f"{r['wall_s']:.1f}s {'MATCH' if same else 'DIFF'}"
             print(f"  k={c['k']} mask={c['mask']:#x}: {st}")
 
