@@ -203,6 +203,55 @@ def reference_arm(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+N_EVAL = 1 << 20  # allocations per evaluator step
+
+
+def evaluator_leg(pl, torch, dev, steps: int, warmup: int, peak: float, peak_kind: str) -> dict:
+    """K1 (mosaic_gpu_evaluate): stage_time of N_EVAL random cfg5 allocations per step.
+    Device leg: inputs resident in HBM (>L2, and L2 flushed between steps), kernel time by
+    CUDA events on the context stream.  e2e leg: the same call on pinned HOST arrays (H2D of
+    the inputs + D2H of the stage times inside the timed region)."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from evalgen import random_allocations
+    ent, gpus, off = random_allocations(pl, N_EVAL, seed=0)
+    n = len(off) - 1
+    tE, tG, tO = (torch.from_numpy(x).to(dev) for x in (ent, gpus, off))
+    st = torch.empty(n, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)
+    for _ in range(warmup):
+        pl.evaluate(tE, tG, tO, st, None, device=True)
+    pl.reset_counters()
+    for _ in range(steps):
+        flush_l2(torch, dev)
+        pl.evaluate(tE, tG, tO, st, None, device=True)
+    s = pl.evaluate_stats()
+    k_ms = s["kernel_ms"] / max(1, s["launches"])
+    alg = s["alg_bytes"] / max(1, s["launches"])
+    achieved = alg / (k_ms / 1e3) / 1e9 if k_ms > 0 else 0.0
+    hE, hG, hO = (torch.from_numpy(x).pin_memory() for x in (ent, gpus, off))
+    hst = torch.empty(n, dtype=torch.float64).pin_memory()
+    pl.evaluate(hE, hG, hO, hst, None)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        pl.evaluate(hE, hG, hO, hst, None)
+    e2e_s = (time.perf_counter() - t0) / max(1, steps)
+    assert torch.equal(hst.to(dev), st), "host and device evaluator legs disagree"
+    h2d = ent.nbytes + gpus.nbytes + off.nbytes
+    return {"metric": "allocations scored/sec (K1 stage_time, mosaic_gpu_evaluate)",
+            "value": n / (k_ms / 1e3) if k_ms > 0 else 0.0, "unit": "allocations/s",
+            "allocations": n, "entries": int(len(ent)), "gpu_ids": int(len(gpus)),
+            "kernel_ms": k_ms,
+            "e2e": {"value": n / e2e_s, "unit": "allocations/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": n * 8, "timing": "host wall clock, pinned host arrays"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "kernel": "k_evaluate (eval.cu)", "peak_kind": peak_kind,
+                         "algorithmic_bytes": "per allocation 16 B (offset + stage time) + "
+                                              "32 B per entry + 4 B per GPU id"},
+            "data": "synthetic: random module subsets of cfg5, candidate options, "
+                    "windows of d consecutive GPUs; inputs > L2, L2 flushed between steps"}
+
+
 TRAFFIC_CSV = "profiles/r1_dram_cfg5_solve.csv"
 
 
@@ -237,6 +286,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-evaluator", action="store_true", help="skip the K1 evaluator leg")
     ap.add_argument("--workload", default="cfg5", help="cfg1..cfg5 (default cfg5)")
     ap.add_argument("--dist-backend", default="nccl",
                     help="nccl (default); gloo lets several ranks share one GPU for testing")
@@ -346,6 +396,9 @@ def main() -> None:
     achieved = (alg_bytes / ks_n) / avg_launch_s / 1e9 if avg_launch_s > 0 else 0.0
     traffic = dram_traffic_per_launch() if WORKLOAD == "cfg5" else None
 
+    evaluator = None if args.no_evaluator else evaluator_leg(pl, torch, dev, args.steps,
+                                                              args.warmup, peak, peak_kind)
+
     cpu = None
     if not args.no_cpu_baseline and os.path.exists(REF_DRIVER):
         try:
@@ -383,6 +436,7 @@ def main() -> None:
                      "note": "integer/branch-bound tree search; HBM is not the binding "
                              "resource (see DESIGN.md)"},
         "cpu_baseline": cpu,
+        "evaluator": evaluator,
         "clocks": clk.summary(),
         "counters": ctr,
     }

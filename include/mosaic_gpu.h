@@ -4,7 +4,9 @@
  * FFI; its replaceable seams are C++ calls.  Each entry point below replaces one of
  * them and keeps its argument meaning and error behaviour:
  *
- *   mosaic_gpu_stage_time    <- stage_time / rectified_latency      perf_model.hpp:442-479
+ *   mosaic_gpu_evaluate      <- stage_time / rectified_latency over a batch of
+ *                               allocations (K1, host or device arrays)  perf_model.hpp:442-479
+ *   mosaic_gpu_stage_time    <- the same for entries at any quota granularity
  *   mosaic_gpu_options       <- candidate_options                   stage_eval.hpp:68-93
  *   mosaic_gpu_stage_eval    <- stage_eval (tau doubling, bisection,
  *                               confirmation probes; first leaf of the
@@ -133,6 +135,24 @@ typedef struct {
 int mosaic_gpu_stage_time(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* entries,
                           const int32_t* gpus, const int64_t* alloc_off, int64_t n_allocs,
                           double* stage_time_out, double* rect_out);
+
+/* Batched plan scoring (K1): stage_time of n_allocs allocations laid out exactly as for
+ * mosaic_gpu_stage_time, with the array sizes passed explicitly (entries[0..n_entries),
+ * gpus[0..n_gpu_ids)).  Entry quota_levels must be 0 or the context's.  With
+ * MOSAIC_EVAL_DEVICE all five arrays are device pointers on the context's device: nothing
+ * is copied, the caller must have finished writing them (synchronise its stream), and the
+ * call returns once the outputs are written.  Otherwise they are host memory (pinned is
+ * fastest) staged through buffers the context keeps.  Errors (MOSAIC_RANGE /
+ * MOSAIC_TOO_LARGE) are reported for the whole batch, like the reference's exceptions. */
+#define MOSAIC_EVAL_DEVICE 1u
+int mosaic_gpu_evaluate(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* entries,
+                        int64_t n_entries, const int32_t* gpus, int64_t n_gpu_ids,
+                        const int64_t* alloc_off, int64_t n_allocs, double* stage_time_out,
+                        double* rect_out, uint32_t flags);
+/* K1 counters since the last reset: kernel time (CUDA events on the context stream),
+ * launches, and algorithmic bytes (offsets + entries + GPU ids read, outputs written). */
+int mosaic_gpu_evaluate_stats(mosaic_gpu_ctx* ctx, double* kernel_ms, int64_t* launches,
+                              int64_t* alg_bytes);
 
 /* stage_eval / ExactStageSolver::solve / FeasibilitySearch::run for one module set. */
 int mosaic_gpu_stage_eval(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_result* out);

@@ -212,6 +212,34 @@ int mosaic_gpu_stage_time(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* entr
     });
 }
 
+int mosaic_gpu_evaluate(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* entries,
+                        int64_t n_entries, const int32_t* gpus, int64_t n_gpu_ids,
+                        const int64_t* alloc_off, int64_t n_allocs, double* stage_time_out,
+                        double* rect_out, uint32_t flags) {
+    static_assert(sizeof(mosaic_gpu_eval_entry) == sizeof(mg::EvalABI), "entry layout");
+    return guard([&] {
+        if (!ctx) throw Error(MOSAIC_RANGE, "null context");
+        if (n_allocs > 0 && (!entries && n_entries > 0)) throw Error(MOSAIC_RANGE, "null entries");
+        if (n_allocs > 0 && (!alloc_off || !stage_time_out)) throw Error(MOSAIC_RANGE, "null array");
+        ctx->pl->evaluate(reinterpret_cast<const mg::EvalABI*>(entries), n_entries, gpus,
+                          n_gpu_ids, reinterpret_cast<const long long*>(alloc_off), n_allocs,
+                          stage_time_out, rect_out, (flags & MOSAIC_EVAL_DEVICE) != 0);
+        return MOSAIC_OK;
+    });
+}
+
+int mosaic_gpu_evaluate_stats(mosaic_gpu_ctx* ctx, double* kernel_ms, int64_t* launches,
+                              int64_t* alg_bytes) {
+    return guard([&] {
+        if (!ctx) throw Error(MOSAIC_RANGE, "null context");
+        auto& e = ctx->pl->engine();
+        if (kernel_ms) *kernel_ms = e.evaluate_kernel_ms();
+        if (launches) *launches = e.evaluate_kernel_launches();
+        if (alg_bytes) *alg_bytes = e.evaluate_alg_bytes();
+        return MOSAIC_OK;
+    });
+}
+
 int mosaic_gpu_stage_eval(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_result* out) {
     return guard([&] {
         StageResult r = ctx->pl->stage_eval(mask);

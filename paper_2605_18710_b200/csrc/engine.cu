@@ -6,8 +6,9 @@
 //              irregular trees stay spread over all 148 SMs without host round trips.
 //              MIN: shared fp64 incumbent (atomicMin on the bits).  FIRST: the earliest
 //              hit in reference DFS order wins (path comparison under a seqlock).
-//   k_eval   : batched stage_time of explicit allocations (perf_model.hpp:442-479),
-//              one warp per allocation, resident bitmaps in shared memory.
+//   k_eval   : batched stage_time of explicit allocations (perf_model.hpp:442-479) whose
+//              entries use another quota granularity than the context (per-call rate
+//              rows); the common case runs K1 on the ABI layout (eval.cu).
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -73,7 +74,15 @@ __global__ void __launch_bounds__(32 * EVAL_WARPS)
     __syncwarp();
     double worst_stage = 0.0;
     for (int e = 0; e < ne; ++e) {
-        const EvalEntry& E = ent[e0 + e];
+        // rectified_latency uses the module's first entry (StageAllocation::find) and, without
+        // include_self, skips every resident entry of the same module
+        int self = e;
+        for (int f = 0; f < e; ++f)
+            if (ent[e0 + f].module == ent[e0 + e].module) {
+                self = f;
+                break;
+            }
+        const EvalEntry& E = ent[e0 + self];
         double worst = NEG_INF;
         for (int g = lane; g < E.n_gpus; g += 32) {
             unsigned long long m = mk[gpus[E.gpu_off + g]];
@@ -81,7 +90,7 @@ __global__ void __launch_bounds__(32 * EVAL_WARPS)
             int res = 0;
             for (int f = 0; f < ne; ++f) {
                 if (!(m >> f & 1ULL)) continue;
-                if (f == e && !P.include_self) continue;
+                if (ent[e0 + f].module == E.module && !P.include_self) continue;
                 double b = Bt[ent[e0 + f].row];
                 s = s + b;
                 p = p * b;
@@ -147,6 +156,7 @@ Engine::Engine(int device) : device_(device) {
 
 Engine::~Engine() {
     cudaSetDevice(device_);
+    free_eval();
     cudaFree(d_base_);
     cudaFree(d_B_);
     cudaFree(d_fp_);

@@ -30,6 +30,23 @@ struct EvalEntry {  // device evaluator input (one per allocation entry)
     long long gpu_off;
 };
 
+// mosaic_gpu_eval_entry (include/mosaic_gpu.h), the evaluator's input record as the caller
+// lays it out: no host-side repacking between the ABI and the kernel.
+struct EvalABI {
+    int module, d, units, n_gpus, levels, reserved;
+    long long gpu_off;
+};
+static_assert(sizeof(EvalABI) == 32, "mosaic_gpu_eval_entry layout");
+
+// Error bits of the batched evaluator (k_evaluate).
+enum {
+    EVAL_ERR_MODULE = 1,   // module index outside the graph
+    EVAL_ERR_SURFACE = 2,  // (d, units) outside the module's profiled surface
+    EVAL_ERR_GPU = 4,      // GPU id outside 0..G-1 or GPU list outside the gpus array
+    EVAL_ERR_LEVELS = 8,   // entry quota_levels differs from the context's
+    EVAL_ERR_ENTRIES = 16, // allocation with more than 64 entries or outside entries[]
+};
+
 // Search-engine knobs.  Defaults are the measured best; nothing reads the
 // environment — experiments set them through mosaic_gpu_set_tuning().
 struct Tuning {
@@ -69,6 +86,18 @@ class Engine {
                   const std::vector<double>& Bt, int G, const Model& M,
                   std::vector<double>& st_out, std::vector<double>& rect_out);
     double eval_ms() const { return eval_ms_; }
+    // K1 on the ABI layout: dense per-(module, d, units) rate tables uploaded once
+    // (base[m][d-1][u], B[m][u]; eval.cu), then any number of batched calls.  `dev` says the
+    // five arrays are device pointers on this engine's device; otherwise they are host
+    // memory and are staged through persistent device buffers.  Returns EVAL_ERR_* bits.
+    void set_rate_tables(const std::vector<double>& base, const std::vector<double>& B, int n_mod,
+                         int G, int L, const Model& M);
+    bool has_rate_tables() const { return d_tab_base_ != nullptr; }
+    int evaluate_abi(const EvalABI* ent, long long n_ent, const int* gpus, long long n_gpu_ids,
+                     const long long* off, long long n, double* st, double* rect, bool dev);
+    double evaluate_kernel_ms() const { return evk_ms_; }
+    long long evaluate_kernel_launches() const { return evk_n_; }
+    long long evaluate_alg_bytes() const { return evk_bytes_; }
 
     // fn == nullptr with world > 1: measure this rank's share only (no merge; the result
     // is NOT the stage's answer — used to simulate shard balance on one device)
@@ -93,6 +122,9 @@ class Engine {
         h2d_ = 0;
         d2h_ = 0;
         alg_bytes_ = 0;
+        evk_ms_ = 0;
+        evk_n_ = 0;
+        evk_bytes_ = 0;
     }
     long long own_launches() const { return own_launches_; }
     double ksearch_ms() const { return ksearch_ms_; }
@@ -146,6 +178,23 @@ class Engine {
     void* evk1_ = nullptr;
     void* evm0_ = nullptr;
     void* evm1_ = nullptr;
+    // K1 rate tables and staging (eval.cu)
+    double* d_tab_base_ = nullptr;
+    double* d_tab_B_ = nullptr;
+    int tab_nmod_ = 0, tab_G_ = 0, tab_L_ = 0;
+    double tab_e1_ = 0, tab_e2_ = 0, tab_e3_ = 0;
+    int tab_add_ = 0, tab_self_ = 1;
+    void* ev_buf_[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    size_t ev_cap_[5] = {0, 0, 0, 0, 0};
+    int* d_everr_ = nullptr;
+    int* h_everr_ = nullptr;
+    int ev_grid_ = 0;
+    size_t ev_smem_ = 0;
+    double evk_ms_ = 0;
+    long long evk_n_ = 0, evk_bytes_ = 0;
+    void* eva_ = nullptr;
+    void* evb_ = nullptr;
+    void free_eval();
 };
 
 }  // namespace mg

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <limits>
 #include <map>
 #include <random>
 #include <set>
@@ -81,6 +82,39 @@ Sample Surface::lookup(int d, double a) const {
     };
     return Sample{blend(&Point::latency), blend(&Point::bandwidth_util), blend(&Point::memory),
                   blend(&Point::sm_active)};
+}
+
+void Surface::rate_tables(int G, int L, double* lat, double* bw) const {
+    const double nan = std::numeric_limits<double>::quiet_NaN();
+    struct Br {
+        bool ok;
+        size_t lo, hi;
+        double w;
+    };
+    std::vector<Br> ab(L + 1);
+    for (int u = 0; u <= L; ++u) {
+        const double a = static_cast<double>(u) / L;  // DeploymentOption::quota()
+        ab[u].ok = !(a < min_a() - kTol || a > max_a() + kTol);
+        if (ab[u].ok) std::tie(ab[u].lo, ab[u].hi, ab[u].w) = bracket(av_, a, false);
+    }
+    auto blend = [&](const Br& D, const Br& A, double Point::*f) {
+        if (D.lo == D.hi && A.lo == A.hi) return at(D.lo, A.lo).*f;
+        double v00 = at(D.lo, A.lo).*f, v01 = at(D.lo, A.hi).*f;
+        double v10 = at(D.hi, A.lo).*f, v11 = at(D.hi, A.hi).*f;
+        double lo = v00 + (v01 - v00) * A.w;
+        double hi = v10 + (v11 - v10) * A.w;
+        return lo + (hi - lo) * D.w;
+    };
+    for (int d = 1; d <= G; ++d) {
+        Br D{!(d < min_d() || d > max_d()), 0, 0, 0.0};
+        if (D.ok) std::tie(D.lo, D.hi, D.w) = bracket(dv_, (double)d, true);
+        for (int u = 0; u <= L; ++u)
+            lat[(size_t)(d - 1) * (L + 1) + u] =
+                D.ok && ab[u].ok ? blend(D, ab[u], &Point::latency) : nan;
+        if (d == 1)
+            for (int u = 0; u <= L; ++u)
+                bw[u] = D.ok && ab[u].ok ? blend(D, ab[u], &Point::bandwidth_util) : nan;
+    }
 }
 
 std::string validate_graph(const Problem& P) {

@@ -37,6 +37,11 @@ class Surface {
     Surface() = default;
     Surface(std::string id, const std::vector<Point>& pts);
     Sample lookup(int d, double a) const;
+    // Dense evaluator rows: lat[(d-1)*(L+1)+u] = lookup(d, u/L).latency for d = 1..G and
+    // bw[u] = lookup(1, u/L).bandwidth_util (PerfContext::base_latency / solo_bandwidth,
+    // perf_model.hpp:417-427); NaN where lookup would raise SurfaceRangeError.  Same
+    // brackets and blend as lookup(), evaluated once per axis value.
+    void rate_tables(int G, int L, double* lat, double* bw) const;
     const std::vector<double>& d_values() const { return dv_; }
     const std::vector<double>& a_values() const { return av_; }
     const std::vector<Point>& grid() const { return grid_; }  // [di * |a| + ai]

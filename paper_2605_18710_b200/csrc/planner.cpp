@@ -693,13 +693,82 @@ PlanResult Planner::brute_force() {
     return pr;
 }
 
+bool Planner::ensure_rate_tables() {
+    if (rate_tables_) return rate_tables_ > 0;
+    const int n = (int)P_.modules.size(), G = P_.gpu_count, L = P_.quota_levels;
+    const double bytes = 8.0 * n * ((double)G + 1.0) * (L + 1.0);
+    if (bytes > 512.0 * 1024 * 1024) {
+        rate_tables_ = -1;
+        return false;
+    }
+    std::vector<double> base((size_t)n * G * (L + 1)), B((size_t)n * (L + 1));
+    for (int m = 0; m < n; ++m)
+        P_.modules[m].surface.rate_tables(G, L, base.data() + (size_t)m * G * (L + 1),
+                                          B.data() + (size_t)m * (L + 1));
+    eng_->set_rate_tables(base, B, n, G, L, M_);
+    rate_tables_ = 1;
+    return true;
+}
+
+static void raise_eval_errors(int err) {
+    if (err & mg::EVAL_ERR_ENTRIES)
+        throw Error(TOO_LARGE, "evaluator supports 64 entries per stage (or bad alloc_off)");
+    if (err & mg::EVAL_ERR_MODULE) throw Error(RANGE, "module not in graph");
+    if (err & mg::EVAL_ERR_GPU) throw Error(RANGE, "GPU index out of range");
+    if (err & mg::EVAL_ERR_SURFACE) throw Error(RANGE, "(d, quota) outside the profiled surface");
+    if (err & mg::EVAL_ERR_LEVELS)
+        throw Error(RANGE, "entry quota_levels differs from the context's");
+}
+
+void Planner::evaluate(const mg::EvalABI* ent, long long n_ent, const int* gpus,
+                       long long n_gpu_ids, const long long* off, long long n, double* st,
+                       double* rect, bool device_ptrs) {
+    if (n < 0 || n_ent < 0 || n_gpu_ids < 0) throw Error(RANGE, "negative size");
+    if (n == 0) return;
+    if (!ensure_rate_tables())
+        throw Error(TOO_LARGE, "rate tables too large for this problem; use stage_time");
+    raise_eval_errors(eng_->evaluate_abi(ent, n_ent, gpus, n_gpu_ids, off, n, st, rect,
+                                         device_ptrs));
+}
+
 void Planner::stage_time(const std::vector<std::vector<Entry>>& allocs, std::vector<double>& st,
                          std::vector<std::vector<double>>& rect) {
+    for (const auto& a : allocs)
+        if (a.size() > 64) throw Error(TOO_LARGE, "evaluator supports 64 entries per stage");
+    bool table_ok = true;
+    for (const auto& a : allocs)
+        for (const auto& e : a)
+            if (e.levels != 0 && e.levels != P_.quota_levels) table_ok = false;
+    if (table_ok && ensure_rate_tables()) {
+        // K1 on the ABI layout
+        std::vector<mg::EvalABI> ent;
+        std::vector<int> gpus;
+        std::vector<long long> off{0};
+        for (const auto& a : allocs) {
+            for (const auto& e : a) {
+                ent.push_back(mg::EvalABI{e.module, e.d, e.units, (int)e.gpus.size(), e.levels, 0,
+                                          (long long)gpus.size()});
+                gpus.insert(gpus.end(), e.gpus.begin(), e.gpus.end());
+            }
+            off.push_back((long long)ent.size());
+        }
+        st.assign(allocs.size(), 0.0);
+        std::vector<double> rflat(ent.size(), 0.0);
+        raise_eval_errors(eng_->evaluate_abi(ent.data(), (long long)ent.size(), gpus.data(),
+                                             (long long)gpus.size(), off.data(),
+                                             (long long)allocs.size(), st.data(), rflat.data(),
+                                             false));
+        rect.assign(allocs.size(), {});
+        for (size_t i = 0; i < allocs.size(); ++i)
+            rect[i].assign(rflat.begin() + off[i], rflat.begin() + off[i + 1]);
+        return;
+    }
+    // entries at another quota granularity: per-call rate rows (k_eval)
     std::vector<mg::EvalEntry> ent;
     std::vector<int> gpus;
     std::vector<long long> off{0};
     std::vector<double> base, Bt;
-    std::unordered_map<uint64_t, int> row_of;  // (module, d, units) -> table row
+    std::unordered_map<uint64_t, int> row_of;  // (module, d, units, levels) -> table row
     for (const auto& a : allocs) {
         for (const auto& e : a) {
             if (e.module < 0 || e.module >= (int)P_.modules.size())
@@ -713,7 +782,7 @@ void Planner::stage_time(const std::vector<std::vector<Entry>>& allocs, std::vec
                 const Surface& s = P_.modules[e.module].surface;
                 double a = (double)e.units / lv;
                 base.push_back(s.lookup(e.d, a).latency);      // PerfContext::base_latency
-                Bt.push_back(s.lookup(1, a).bandwidth_util);   // PerfContext::solo_bandwidth
+                Bt.push_back(s.lookup(1, a).bandwidth_util);   // PerfContext::solo_bandwidth (eager)
                 row = (int)base.size() - 1;
                 row_of.emplace(key, row);
             } else {
@@ -725,7 +794,6 @@ void Planner::stage_time(const std::vector<std::vector<Entry>>& allocs, std::vec
                                         (long long)gpus.size()});
             gpus.insert(gpus.end(), e.gpus.begin(), e.gpus.end());
         }
-        if (a.size() > 64) throw Error(TOO_LARGE, "evaluator supports 64 entries per stage");
         off.push_back((long long)ent.size());
     }
     std::vector<double> rflat;

@@ -94,6 +94,10 @@ class Planner {
     // stage_time of explicit allocations (entries per allocation sorted by module)
     void stage_time(const std::vector<std::vector<Entry>>& allocs, std::vector<double>& st,
                     std::vector<std::vector<double>>& rect);
+    // K1 on the ABI layout (mosaic_gpu_evaluate): host or device arrays, no repacking.
+    // Throws Error(RANGE / TOO_LARGE) for the reference's exceptions.
+    void evaluate(const mg::EvalABI* ent, long long n_ent, const int* gpus, long long n_gpu_ids,
+                  const long long* off, long long n, double* st, double* rect, bool device_ptrs);
 
     // make_baseline_plan (simulator.hpp:283-313): policy 0 Megatron, 1 DistMM; full-quota
     // options at this problem's quota_levels; stage times from the device evaluator
@@ -118,6 +122,7 @@ class Planner {
 
   private:
     void check_rows(int m) const;
+    bool ensure_rate_tables();  // false when they would not fit (then the row path is used)
     bool first_leaf(const std::vector<int>& order, bool filter, double theta, mg::Leaf& leaf,
                     mg::SearchStats& st, const std::vector<Entry>* seed = nullptr,
                     double seed_value = 0.0);
@@ -138,6 +143,7 @@ class Planner {
     std::unique_ptr<mg::Engine> eng_;
     std::unordered_map<uint64_t, StageResult> cache_;
     std::vector<uint64_t> cache_order_;
+    int rate_tables_ = 0;  // 0 not built yet, 1 built, -1 too large for this problem
 };
 
 }  // namespace mosaic_b200

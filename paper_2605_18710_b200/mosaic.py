@@ -161,7 +161,7 @@ EXPORTS = [
     "mosaic_gpu_validate_plan", "mosaic_gpu_generate_surfaces", "mosaic_gpu_synth_workloads",
     "mosaic_gpu_baseline_plan", "mosaic_gpu_simulate",
     "mosaic_gpu_cache_masks", "mosaic_gpu_cache_entry", "mosaic_gpu_set_tuning",
-    "mosaic_gpu_device_bytes",
+    "mosaic_gpu_device_bytes", "mosaic_gpu_evaluate", "mosaic_gpu_evaluate_stats",
 ]
 
 _lib = None
@@ -233,6 +233,10 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                                C.c_int64, C.c_char_p, C.c_size_t]),
         "mosaic_gpu_set_tuning": (C.c_int, [vp, C.c_char_p, C.c_double]),
         "mosaic_gpu_device_bytes": (C.c_int64, [vp]),
+        "mosaic_gpu_evaluate": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int64, vp, C.c_int64,
+                                          vp, vp, C.c_uint32]),
+        "mosaic_gpu_evaluate_stats": (C.c_int, [vp, P(C.c_double), P(C.c_int64),
+                                                P(C.c_int64)]),
         "mosaic_gpu_cache_masks": (C.c_int, [vp, P(C.c_uint64), C.c_int64, P(C.c_int64)]),
         "mosaic_gpu_cache_entry": (C.c_int, [vp, C.c_uint64, P(StageResultC), P(C.c_double),
                                              P(C.c_int32), C.c_int64, P(C.c_int64)]),
@@ -558,6 +562,30 @@ class Planner:
             return list(st[:n]), [list(rect[off[i]:off[i + 1]]) for i in range(n)]
         return list(st[:n])
 
+    def evaluate(self, entries, gpus, alloc_off, stage_time_out, rect_out=None,
+                 device: bool = False) -> None:
+        """K1 on flat arrays (mosaic_gpu_evaluate): `entries` holds mosaic_gpu_eval_entry
+        records as an (n_entries, 8) int32 array (see pack_eval_entries), `gpus` int32,
+        `alloc_off` int64 (n_allocs + 1), outputs float64.  numpy arrays (host) or, with
+        device=True, CUDA tensors on this planner's device (the caller synchronises the
+        stream that wrote them)."""
+        def ptr(x):
+            if x is None:
+                return None
+            if hasattr(x, "data_ptr"):
+                return x.data_ptr()
+            return x.ctypes.data
+        n = len(alloc_off) - 1
+        _raise(load_library().mosaic_gpu_evaluate(
+            self._ctx, ptr(entries), len(entries), ptr(gpus), len(gpus), ptr(alloc_off), n,
+            ptr(stage_time_out), ptr(rect_out), 1 if device else 0))
+
+    def evaluate_stats(self) -> dict:
+        ms, n, b = C.c_double(), C.c_int64(), C.c_int64()
+        _raise(load_library().mosaic_gpu_evaluate_stats(self._ctx, C.byref(ms), C.byref(n),
+                                                        C.byref(b)))
+        return {"kernel_ms": ms.value, "launches": n.value, "alg_bytes": b.value}
+
     def make_baseline_plan(self, policy: str) -> "DeploymentPlan":
         """make_baseline_plan (simulator.hpp:283-313): 'megatron' or 'distmm', full-quota
         options; raises InfeasibleBaselineError like the reference."""
@@ -717,6 +745,23 @@ def solve(planner: Planner) -> SolveResult:
 
 def brute_force_optimum(planner: Planner) -> Optional[OracleResult]:
     return planner.brute_force_optimum()
+
+
+def pack_eval_entries(module, dp_degree, quota_units, n_gpus, gpu_off, quota_levels=None):
+    """(n, 8) int32 view of mosaic_gpu_eval_entry records from per-entry columns (numpy):
+    module, dp_degree, quota_units, n_gpus, quota_levels (0 = the context's), reserved,
+    gpu_off (int64, little-endian low/high words)."""
+    import numpy as np
+    n = len(module)
+    out = np.zeros((n, 8), dtype=np.int32)
+    out[:, 0] = module
+    out[:, 1] = dp_degree
+    out[:, 2] = quota_units
+    out[:, 3] = n_gpus
+    if quota_levels is not None:
+        out[:, 4] = quota_levels
+    out[:, 6:8] = np.asarray(gpu_off, dtype=np.int64).reshape(n, 1).view(np.int32)
+    return out
 
 
 def stage_time(planner: Planner, allocation: StageAllocation) -> float:

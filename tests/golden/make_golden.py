@@ -108,6 +108,47 @@ def random_sets() -> None:
                               "big": big})
 
 
+def stime_edge() -> None:
+    """K1 edge cases against the reference's stage_time: dp degrees off the profiled d grid
+    (log2 interpolation), any quota unit, duplicate modules (StageAllocation::find takes the
+    first entry), repeated and unsorted GPU ids, negative coefficients."""
+    rng = random.Random(777)
+    out, all_cases = [], []
+    for inst, n, g, L in [("cfg5", 8, 128, 32), ("cfg3", 4, 32, 10), ("random:3:6:24", 6, 24, 10)]:
+        cases = []
+        for t in range(40):
+            k = rng.randint(1, min(n + 2, 10))
+            mods = [rng.randrange(n) for _ in range(k)]
+            if t % 2 == 0:
+                mods = sorted(set(mods))
+            ents = []
+            for m in mods:
+                d = rng.randint(1, g)
+                u = rng.randint(1, L)
+                gp = rng.sample(range(g), d)
+                if t % 3 == 0:
+                    gp = sorted(gp)
+                if t % 5 == 0 and gp:
+                    gp.append(gp[0])  # a repeated GPU id
+                ents.append((m, d, u, gp))
+            cases.append(ents)
+        all_cases += [(inst, c) for c in cases]
+    # lazy range errors: an out-of-hull option (a = 1/32 < 0.1) on a duplicate entry is
+    # never looked up unless that entry is counted as a resident on a self entry's GPU
+    lo = list(range(8))
+    cases_cfg5 = [[(0, 8, 16, lo), (0, 4, 1, [100, 101, 102, 103])],
+                  [(0, 8, 16, lo), (0, 4, 1, [4, 5, 6, 7])],
+                  [(0, 8, 16, lo), (1, 4, 1, [4, 5, 6, 7])],
+                  [(0, 8, 16, lo), (1, 4, 8, [4, 5, 6, 7]), (0, 2, 1, [120, 7])]]
+    for inst, ents in [("cfg5", c) for c in cases_cfg5] + all_cases:
+        spec = ";".join(f"{m}:{d}:{u}:{'.'.join(map(str, gp))}" for m, d, u, gp in ents)
+        for extra in ([], ["noself"], ["additive"], ["e=1e-3,-2e-4,5e-4"],
+                      ["noself", "e=1e-3,-2e-4,5e-4"]):
+            r = ref(inst, "stime", spec, *extra)
+            out.append({"inst": inst, "extra": extra, "entries": ents, "t": r.get("t")})
+    dump("stime_edge.json", out)
+
+
 def presets() -> None:
     # acceptance.cpp:171-198 (C5): all presets at 8 GPUs, with and without prune+cache
     out = []

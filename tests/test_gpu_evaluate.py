@@ -1,0 +1,136 @@
+"""K1 evaluator (mosaic_gpu_evaluate, eval.cu) parity with the reference's stage_time
+(perf_model.hpp:442-479): fp64 bit patterns, host and device arrays, edge cases and errors."""
+import math
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, hexf, load_golden
+
+pytestmark = pytest.mark.gpu
+
+mosaic = pytest.importorskip("paper_2605_18710_b200.mosaic")
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+from evalgen import random_allocations, to_allocations  # noqa: E402
+from test_gpu_parity import planner  # noqa: E402
+
+EDGE = load_golden("stime_edge.json")
+
+
+def test_edge_cases_match_reference_bits():
+    # off-grid dp degrees (log2 interpolation in the rate tables), any quota unit,
+    # duplicate modules, repeated / unsorted GPU ids, negative coefficients
+    groups = {}
+    for row in EDGE:
+        groups.setdefault((row["inst"], tuple(row["extra"])), []).append(row)
+    for (inst, extra), rows in groups.items():
+        pl = planner(inst, extra=list(extra))
+
+        def alloc(row):
+            return mosaic.StageAllocation(
+                [mosaic.Entry(m, mosaic.DeploymentOption(d, u, pl.quota_levels), gp)
+                 for m, d, u, gp in row["entries"]])
+        ok = [r for r in rows if r["t"] is not None]
+        got = pl.stage_time([alloc(r) for r in ok])
+        want = [hexf(r["t"]) for r in ok]
+        bad = [(i, g, w) for i, (g, w) in enumerate(zip(got, want)) if g != w]
+        assert not bad, (inst, extra, bad[:5])
+        # the reference throws SurfaceRangeError exactly when a lookup it makes (a self
+        # entry's base latency, a counted resident's solo bandwidth) leaves the hull
+        for r in rows:
+            if r["t"] is None:
+                with pytest.raises(mosaic.SurfaceRangeError):
+                    pl.stage_time([alloc(r)])
+        pl.close()
+
+
+def _torch():
+    return pytest.importorskip("torch")
+
+
+@pytest.mark.parametrize("spec,extra", [("cfg5", ()), ("cfg5", ("noself",)),
+                                        ("cfg4", ("additive",)),
+                                        ("cfg3", ("e=1e-3,-2e-4,5e-4",))])
+def test_evaluate_host_device_and_reference_api_agree(spec, extra):
+    torch = _torch()
+    pl = planner(spec, extra=list(extra))
+    ent, gpus, off = random_allocations(pl, 20000, seed=3)
+    n = len(off) - 1
+    st_h = np.zeros(n)
+    rect_h = np.zeros(len(ent))
+    pl.evaluate(ent, gpus, off, st_h, rect_h)
+    dev = torch.device("cuda", 0)
+    tE, tG, tO = (torch.from_numpy(x).to(dev) for x in (ent, gpus, off))
+    st_d = torch.zeros(n, dtype=torch.float64, device=dev)
+    rect_d = torch.zeros(len(ent), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    pl.evaluate(tE, tG, tO, st_d, rect_d, device=True)
+    assert np.array_equal(st_d.cpu().numpy(), st_h)
+    assert np.array_equal(rect_d.cpu().numpy(), rect_h)
+    # the reference-API path (one StageAllocation per allocation) on a slice
+    allocs = to_allocations(ent, gpus, off, pl.quota_levels, 0, 300)
+    st_r, rect_r = pl.stage_time(allocs, with_rectified=True)
+    assert st_r == list(st_h[:300])
+    assert [x for r in rect_r for x in r] == list(rect_h[:off[300]])
+    s = pl.evaluate_stats()
+    assert s["launches"] >= 2 and s["kernel_ms"] > 0 and s["alg_bytes"] > 0
+    pl.close()
+
+
+def test_evaluate_matches_restatement_oracle():
+    from oracle import restatement
+    if not restatement.available():
+        pytest.skip("oracle restatement not built")
+    pl = planner("cfg5")
+    ent, gpus, off = random_allocations(pl, 400, seed=11)
+    st = np.zeros(len(off) - 1)
+    pl.evaluate(ent, gpus, off, st)
+    prob = restatement.Problem("cfg5")
+    for a in range(len(off) - 1):
+        ents = []
+        for e in range(off[a], off[a + 1]):
+            m, d, u, ng = (int(x) for x in ent[e, :4])
+            go = int(ent[e, 6:8].copy().view(np.int64)[0])
+            ents.append((m, d, u, [int(x) for x in gpus[go:go + ng]]))
+        assert st[a] == prob.stage_time(ents), a
+    pl.close()
+
+
+def test_evaluate_edge_shapes_and_errors():
+    pl = planner("cfg5")
+    L = pl.quota_levels
+    # empty allocation -> 0.0 (stage_time's seed); entry without GPUs -> base - 1e300
+    ent = mosaic.pack_eval_entries([0, 1], [4, 4], [8, 8], [0, 4], [0, 0])
+    gpus = np.arange(4, dtype=np.int32)
+    off = np.array([0, 0, 1, 2], dtype=np.int64)
+    st = np.zeros(3)
+    rect = np.zeros(2)
+    pl.evaluate(ent, gpus, off, st, rect)
+    assert st[0] == 0.0 and st[1] == 0.0
+    assert rect[0] < -1e299
+    ref = pl.stage_time([mosaic.StageAllocation(
+        [mosaic.Entry(1, mosaic.DeploymentOption(4, 8, L), [0, 1, 2, 3])])])
+    assert st[2] == ref[0]
+    # the same quota at another granularity goes through the per-call row path
+    twice = pl.stage_time([mosaic.StageAllocation(
+        [mosaic.Entry(1, mosaic.DeploymentOption(4, 16, 2 * L), [0, 1, 2, 3])])])
+    assert twice == ref
+    cases = [
+        (mosaic.pack_eval_entries([9], [4], [8], [4], [0]), mosaic.SurfaceRangeError),  # module
+        (mosaic.pack_eval_entries([1], [4], [8], [4], [0], [2 * L]), mosaic.SurfaceRangeError),
+        (mosaic.pack_eval_entries([1], [4], [L + 1], [4], [0]), mosaic.SurfaceRangeError),
+        (mosaic.pack_eval_entries([1], [4], [8], [5], [0]), mosaic.SurfaceRangeError),  # ids
+    ]
+    for e, exc in cases:
+        with pytest.raises(exc):
+            pl.evaluate(e, gpus, np.array([0, 1], dtype=np.int64), np.zeros(1))
+    g2 = np.array([0, 1, 2, 999], dtype=np.int32)
+    with pytest.raises(mosaic.SurfaceRangeError):
+        pl.evaluate(mosaic.pack_eval_entries([1], [4], [8], [4], [0]), g2,
+                    np.array([0, 1], dtype=np.int64), np.zeros(1))
+    big = mosaic.pack_eval_entries([0] * 65, [1] * 65, [1] * 65, [1] * 65, [0] * 65)
+    with pytest.raises(mosaic.OracleTooLargeError):
+        pl.evaluate(big, gpus, np.array([0, 65], dtype=np.int64), np.zeros(1))
+    pl.close()
