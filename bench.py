@@ -1,23 +1,29 @@
-"""bench.py — candidate plans evaluated/sec and time-to-best-plan, B200 vs CPU reference.
+"""bench.py — candidate plans evaluated/sec and time-to-best-plan, B200 vs the CPU reference.
 
 Workload (BASELINE.json configs[4], the config the metric's 1/2/4/8-B200 sharding is
 quoted on): cfg5 = omni-modal 8-module MM (7 encoders -> backbone, profiler.hpp:212-285)
-on 128 modeled GPUs, quota granularity 1/32, GAHC search (solver.hpp:157-289) to the
-best plan.  One STEP = one full solve(): every stage_eval of every GAHC round, each a
-tau-probe replay whose feasibility searches run on the GPU.
+on 128 modeled GPUs, quota granularity 1/32, GAHC (solver.hpp:157-289).
 
-  value  = complete stage allocations scored on the device (leaves) / device time of the
-           timed steps (CUDA events on the library's own stream), whole job over ranks.
-  e2e    = the same metric through the C ABI with HOST buffers: mosaic_gpu_create from
-           host surface tables (option tables copied H2D) + mosaic_gpu_solve + plan read
-           back, per step, host wall clock.
-  ms_per_step = time to the best plan (device-timed).
+Both arms time the SAME work (like-for-like):
+  * one STEP = the identical-work sample: the stage_eval calls (stage_eval.hpp:302-382) of
+    the cfg5 GAHC solve that the reference finishes in seconds — the 29 EvalCache entries
+    with k <= 4 modules, in call order, cold cache (tests/golden/cfg5_sample.json);
+  * value = the REFERENCE's complete-allocation count for that sample (its verify_complete
+    leaves, stage_eval.hpp:254, counted once by the instrumented reference and committed)
+    / the arm's time, so value_ours / value_reference = t_reference / t_ours on identical
+    work.  Our arm also checks every stage time against the reference's, bit for bit.
+  * time_to_best_plan_s = the full cfg5 solve.  Ours: device-timed.  Reference: run under a
+    wall-clock cap and reported as "> cap" when it does not finish.
+  * e2e (ours) = the sample through the C ABI from HOST buffers: mosaic_gpu_create from host
+    surface tables (option tables packed on the device) + the 29 stage_evals + results read
+    back, host wall clock.
+  * evaluator = K1 (mosaic_gpu_evaluate) on 2^20 random cfg5 allocations, with its roofline.
+Multi-GPU (torchrun, one rank per GPU): the sample's masks are dealt to ranks (no
+collective); the full solve shards each device search's frontier (mosaic_gpu_set_shard).
 
---impl reference runs the reference's own CPU planner (oracle/_ref, the unmodified
-headers compiled by oracle/Makefile) on a bounded sample of the same workload: the
-stage_eval calls GAHC issues in its first two rounds on cfg5 (all singletons and all
-encoder pairs), which is where the reference spends its first ~seconds; the full cfg5
-solve does not finish on the CPU (>90 min).
+--impl reference runs the reference's own CPU planner (oracle/_ref, the unmodified headers
+compiled by oracle/Makefile) on the same sample, one process per stage_eval on every host
+core (the reference is single-threaded), plus the capped full solve.
 """
 from __future__ import annotations
 
@@ -34,17 +40,30 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOAD = "cfg5"
-DESCR = {
-    "cfg1": "cfg1: CLIP ViT-L/14 + text encoder, 8 modeled GPUs, exhaustive-size stage search",
-    "cfg2": "cfg2: LLaVA ViT + projector + 7B LLM, 16 modeled GPUs, quota 1/8, GAHC",
-    "cfg3": "cfg3: Qwen3-VL vision + text + deepstack + LLM, 32 modeled GPUs, GAHC",
-    "cfg4": "cfg4: omni-6 (3 encoders -> LLM -> 2 decoders), 64 modeled GPUs, GAHC",
-    "cfg5": "cfg5: omni-modal 8-module MM, 128 modeled GPUs, quota 1/32, GAHC to best plan",
-}
-METRIC = "candidate plans evaluated/sec (cfg5 GAHC solve to best plan)"
+METRIC = ("candidate plans evaluated/sec (reference-equivalent: the reference's complete "
+          "allocations over an identical cfg5 GAHC stage_eval sample) and time-to-best-plan")
 UNIT = "plans/s"
 REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver_instr")
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+with open(os.path.join(ROOT, "tests", "golden", "cfg5_sample.json")) as _f:
+    SAMPLE = json.load(_f)
+SAMPLE_LEAVES = SAMPLE["leaves"]
+CONFIG = {"workload": "cfg5: omni-modal 8-module MM, 128 modeled GPUs, quota 1/32; step = "
+                      "the 29 stage_evals (k<=4) of its GAHC solve, cold cache; "
+                      "time_to_best_plan = the full GAHC solve",
+          "modeled_gpus": 128, "quota_levels": 32, "modules": 8,
+          "sample_masks": len(SAMPLE["masks"]), "sample_reference_leaves": SAMPLE_LEAVES}
+
+
+def mask_bits(m: int) -> list[int]:
+    return [i for i in range(64) if m >> i & 1]
+
+
+def deal(masks: list[dict], rank: int, world: int) -> list[dict]:
+    """Masks of this rank: dealt in decreasing reference cost (k-module stages dominate)."""
+    order = sorted(range(len(masks)), key=lambda i: -masks[i]["cpu_s"])
+    mine = sorted(order[rank::world])
+    return [masks[i] for i in mine]
 
 
 def peaks() -> tuple[float, str]:
@@ -116,46 +135,6 @@ def flush_l2(torch, dev) -> None:
     torch.cuda.synchronize(dev)
 
 
-def cpu_sample_masks() -> list[int]:
-    """GAHC round 0 + round 1 stage_evals on cfg5: 8 singletons + 21 encoder pairs."""
-    masks = [1 << m for m in range(8)]
-    for a in range(7):
-        for b in range(a + 1, 7):
-            masks.append((1 << a) | (1 << b))
-    return masks
-
-
-def run_cpu_sample(parallel: int) -> dict:
-    """Reference CPU planner on the bounded sample; leaves counted by the instrumented
-    build (verify_complete, stage_eval.hpp:254)."""
-    if not os.path.exists(REF_DRIVER):
-        raise FileNotFoundError(f"{REF_DRIVER} missing (build with make -C oracle ref)")
-    masks = cpu_sample_masks()
-    t0 = time.perf_counter()
-    procs = []
-    results = []
-    pending = list(masks)
-    while pending or procs:
-        while pending and len(procs) < parallel:
-            m = pending.pop(0)
-            cmd = [REF_DRIVER, WORKLOAD, "stage", str(m)]
-            if parallel == 1 and shutil_which("taskset"):
-                cmd = ["taskset", "-c", "0"] + cmd
-            procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, text=True))
-        p = procs.pop(0)
-        out, _ = p.communicate()
-        results.append(json.loads(out))
-    wall = time.perf_counter() - t0
-    leaves = sum(r.get("leaves", 0) for r in results)
-    return {"leaves": leaves, "wall_s": wall, "stage_evals": len(masks),
-            "value": leaves / wall if wall > 0 else 0.0}
-
-
-def shutil_which(x: str):
-    from shutil import which
-    return which(x)
-
-
 def host_cpu() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -167,38 +146,67 @@ def host_cpu() -> str:
     return "unknown"
 
 
+def run_ref_sample(masks: list[dict], parallel: int) -> dict:
+    """The reference planner on `masks`, one process per stage_eval, `parallel` at a time
+    (largest first), pinned to one core each when parallel == 1."""
+    if not os.path.exists(REF_DRIVER):
+        raise FileNotFoundError(f"{REF_DRIVER} missing (build with make -C oracle ref)")
+    todo = sorted(masks, key=lambda m: -m["cpu_s"])
+    t0 = time.perf_counter()
+    procs, leaves = [], 0
+    while todo or procs:
+        while todo and len(procs) < parallel:
+            m = todo.pop(0)
+            cmd = [REF_DRIVER, WORKLOAD, "stage", str(m["mask"])]
+            if parallel == 1:
+                cmd = ["taskset", "-c", "0"] + cmd
+            procs.append((m, subprocess.Popen(cmd, stdout=subprocess.PIPE, text=True)))
+        m, p = procs.pop(0)
+        d = json.loads(p.communicate()[0])
+        assert d["t"] == m["t"] or float.fromhex(d["t"]) == float.fromhex(m["t"])
+        leaves += d["leaves"]
+    wall = time.perf_counter() - t0
+    return {"leaves": leaves, "wall_s": wall, "value": leaves / wall if wall > 0 else 0.0}
+
+
+def ref_solve_capped(cap: float) -> dict:
+    t0 = time.perf_counter()
+    try:
+        subprocess.run([REF_DRIVER.replace("_instr", ""), WORKLOAD, "solve"],
+                       capture_output=True, text=True, timeout=cap)
+        return {"time_to_best_plan_s": time.perf_counter() - t0, "finished": True}
+    except subprocess.TimeoutExpired:
+        return {"time_to_best_plan_s": f"> {cap:.0f}", "finished": False, "cap_s": cap}
+
+
 def reference_arm(args) -> None:
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     ncores = os.cpu_count() or 1
-    par = max(1, min(ncores, len(cpu_sample_masks())))
+    par = max(1, min(ncores, len(SAMPLE["masks"])))
     for _ in range(args.warmup):
-        run_cpu_sample(par)
-    vals, walls, leaves = [], [], 0
+        run_ref_sample(SAMPLE["masks"], par)
+    walls, leaves = [], 0
     for _ in range(args.steps):
-        r = run_cpu_sample(par)
-        vals.append(r["value"])
+        r = run_ref_sample(SAMPLE["masks"], par)
         walls.append(r["wall_s"])
         leaves += r["leaves"]
-    total_wall = sum(walls)
-    value = leaves / total_wall if total_wall else 0.0
+    total = sum(walls)
+    value = leaves / total if total else 0.0
+    tt = ref_solve_capped(args.ref_cap)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * total_wall / max(1, args.steps), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD + " (bounded sample: GAHC rounds 0-1 stage_evals, "
-                   "8 singletons + 21 encoder pairs)", "modeled_gpus": 128,
-                   "quota_levels": 32, "modules": 8},
+        "ms_per_step": 1000.0 * total / max(1, args.steps), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": CONFIG, "same_config": True,
+        "time_to_best_plan_s": tt["time_to_best_plan_s"], "full_solve": tt,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": par, "kind": "reference",
-                         "sample": "29 stage_eval calls of cfg5 GAHC rounds 0-1, one process "
-                                   "per stage_eval (harness-parallel; the reference is "
-                                   "single-threaded)", "cpu": host_cpu(),
-                         "host_cores": ncores},
+                         "sample": f"the {len(SAMPLE['masks'])} cfg5 stage_evals of one step, "
+                                   "one process per stage_eval on every host core "
+                                   "(the reference is single-threaded)",
+                         "cpu": host_cpu(), "host_cores": ncores},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "time_to_best_plan_s": None,
-        "note": "the reference does not finish the full cfg5 solve (>90 min, SURVEY.md §6)",
     }
     print(json.dumps(line), flush=True)
 
@@ -287,7 +295,11 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-evaluator", action="store_true", help="skip the K1 evaluator leg")
-    ap.add_argument("--workload", default="cfg5", help="cfg1..cfg5 (default cfg5)")
+    ap.add_argument("--workload", default="cfg5",
+                    help="cfg5 (default, the headline); cfg1..cfg4 time only the full solve "
+                         "(value = device leaves/s; used by the sharding tests)")
+    ap.add_argument("--ref-cap", type=float, default=60.0,
+                    help="wall-clock cap (s) of the reference's full cfg5 solve")
     ap.add_argument("--dist-backend", default="nccl",
                     help="nccl (default); gloo lets several ranks share one GPU for testing")
     ap.add_argument("--same-device", action="store_true",
@@ -302,6 +314,7 @@ def main() -> None:
 
     global WORKLOAD
     WORKLOAD = args.workload
+    headline = WORKLOAD == "cfg5"
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = 0 if args.same_device else int(os.environ.get("LOCAL_RANK", "0"))
@@ -328,85 +341,106 @@ def main() -> None:
         dist.all_gather(outs, t)
         return [bytes(o.cpu().numpy().tobytes()) for o in outs]
 
-    # ---- device-resident run: tables already in HBM, time the solve only ----
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=comm_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0])
+
+    mine = deal(SAMPLE["masks"], rank, world) if headline else []
+    want = {m["mask"]: float.fromhex(m["t"]) for m in mine}
+
+    def run_sample(pl) -> None:
+        if not mine:
+            return
+        # one batched stage search (mosaic_gpu_search): the stage_evals advance together,
+        # one launch per wave of their device searches
+        rs = pl.search([mask_bits(m["mask"]) for m in mine])
+        for m, r in zip(mine, rs):
+            # identical work: every stage time equals the reference's, bit for bit
+            assert r is not None and r.stage_time == want[m["mask"]], (m["mask"], r)
+
+    # ---- device-resident: tables already in HBM, time the sample ----
     pl = mosaic.Planner.from_spec(WORKLOAD, device=local)
-    res_g, res_l, res_n = pl.gpu_count, pl.quota_levels, pl.n_modules
-    if world > 1:
-        pl.set_shard(rank, world, allgather_bytes)
     for _ in range(args.warmup):
-        res = pl.solve()
+        run_sample(pl)
     barrier()
     pl.reset_counters()
-    dev_ms, leaves, plans = [], 0, []
+    dev_ms = []
     with Clocks(local) as clk:
         for _ in range(args.steps):
             flush_l2(torch, dev)
             barrier()
             pl.mark(0)
-            res = pl.solve()
+            run_sample(pl)
             pl.mark(1)
             dev_ms.append(pl.marked_ms())
-            leaves += res.trace.leaves
-            plans.append(res.plan.predicted_iteration_time)
         barrier()
     ctr = pl.counters()
-    t_local = sum(dev_ms)
-    if world > 1:
-        tt = torch.tensor([t_local, float(leaves)], dtype=torch.float64, device=comm_dev)
-        mx = tt[:1].clone()
-        sm = tt[1:].clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        t_max, leaves_all = float(mx[0]), float(sm[0])
-    else:
-        t_max, leaves_all = t_local, float(leaves)
-    value = leaves_all / (t_max / 1000.0) if t_max > 0 else 0.0
+    t_max = max_over_ranks(sum(dev_ms))
+    value = SAMPLE_LEAVES * args.steps / (t_max / 1000.0) if t_max > 0 else 0.0
 
-    # ---- e2e through the C ABI with host buffers (create + solve + read back) ----
-    e2e_s, e2e_leaves, h2d, d2h = 0.0, 0, 0, 0
-    for i in range(args.steps):
+    # ---- time to the best plan: the full solve (frontier sharded over ranks) ----
+    if world > 1:
+        pl.set_shard(rank, world, allgather_bytes)
+    for _ in range(max(1, args.warmup)):
+        res = pl.solve()
+    solve_ms = []
+    for _ in range(args.steps):
+        flush_l2(torch, dev)
+        barrier()
+        pl.mark(0)
+        res = pl.solve()
+        pl.mark(1)
+        solve_ms.append(pl.marked_ms())
+    ttbp = max_over_ranks(statistics.median(solve_ms)) / 1000.0
+    if not headline:
+        # no reference-equivalent count for the other configs: device leaves per second
+        value = res.trace.leaves / ttbp if ttbp > 0 else 0.0
+        t_max = ttbp * 1000.0 * args.steps
+    best_plan = res.plan.predicted_iteration_time
+    searches_per_solve = res.trace.stage_eval_calls
+
+    # ---- e2e through the C ABI with host buffers (create + sample + read back) ----
+    e2e_s, h2d, d2h = 0.0, 0, 0
+    for _ in range(args.steps):
         barrier()
         t0 = time.perf_counter()
         p2 = mosaic.Planner.from_spec(WORKLOAD, device=local)
-        if world > 1:
-            p2.set_shard(rank, world, allgather_bytes)
-        r2 = p2.solve()
-        _ = [(e.module, e.gpus) for st in r2.plan.stages for e in st.entries]
+        run_sample(p2)
         c2 = p2.counters()
         p2.close()
         barrier()
         e2e_s += time.perf_counter() - t0
-        e2e_leaves += r2.trace.leaves
         h2d, d2h = c2["h2d_bytes"], c2["d2h_bytes"]
-    e2e_value = e2e_leaves * world / e2e_s if e2e_s > 0 else 0.0
+    e2e_s = max_over_ranks(e2e_s)
+    e2e_value = SAMPLE_LEAVES * args.steps / e2e_s if e2e_s > 0 and headline else None
 
+    peak, peak_kind = peaks()
+    evaluator = None
+    if not args.no_evaluator and headline:
+        evaluator = evaluator_leg(pl, torch, dev, args.steps, args.warmup, peak, peak_kind)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (k_search) ----
-    # traffic: dram__bytes_read.sum + dram__bytes_write.sum per k_search launch, from the
-    # committed ncu capture of the same cfg5 solve (profiles/)
-    peak, peak_kind = peaks()
+    # ---- roofline of the dominant kernel of the sample (k_search) ----
     ks_ms = ctr["ksearch_ms"]
     ks_n = max(1, ctr["ksearch_launches"])
     alg_bytes = ctr.get("alg_bytes", 0)
     avg_launch_s = ks_ms / ks_n / 1000.0
     achieved = (alg_bytes / ks_n) / avg_launch_s / 1e9 if avg_launch_s > 0 else 0.0
-    traffic = dram_traffic_per_launch() if WORKLOAD == "cfg5" else None
-
-    evaluator = None if args.no_evaluator else evaluator_leg(pl, torch, dev, args.steps,
-                                                              args.warmup, peak, peak_kind)
 
     cpu = None
-    if not args.no_cpu_baseline and os.path.exists(REF_DRIVER):
+    if not args.no_cpu_baseline and world == 1 and headline and os.path.exists(REF_DRIVER):
+        small = [m for m in SAMPLE["masks"] if m["k"] <= 3]
         try:
-            r = run_cpu_sample(1)
+            r = run_ref_sample(small, 1)
             cpu = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "reference",
-                   "sample": f"{r['stage_evals']} stage_eval calls of cfg5 GAHC rounds 0-1 "
-                             f"(8 singletons + 21 encoder pairs), {r['leaves']} leaves in "
-                             f"{r['wall_s']:.2f}s, pinned to one core",
+                   "sample": f"the {len(small)} k<=3 stage_evals of the step, {r['leaves']} "
+                             f"reference leaves in {r['wall_s']:.2f}s on one core",
                    "cpu": host_cpu(), "host_cores": os.cpu_count()}
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
@@ -416,25 +450,25 @@ def main() -> None:
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / max(1, args.steps),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": DESCR.get(WORKLOAD, WORKLOAD), "modeled_gpus": res_g,
-                   "quota_levels": res_l, "modules": res_n,
-                   "l2": "flushed between steps (256 MiB write)",
-                   "parallelism": f"frontier+round sharding over {world} GPU(s)"},
-        "time_to_best_plan_s": t_max / 1000.0 / max(1, args.steps),
-        "best_plan_iteration_time": plans[-1],
+        "data": "synthetic", "config": dict(CONFIG if headline else {"workload": WORKLOAD},
+                                            l2="flushed between steps (256 MiB write)",
+                                            parallelism=f"sample masks dealt over {world} "
+                                                        f"GPU(s); solve frontier sharded"),
+        "same_config": headline,
+        "time_to_best_plan_s": ttbp, "best_plan_iteration_time": best_plan,
+        "full_solve": {"stage_eval_calls": searches_per_solve, "median_ms": ttbp * 1000.0},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "timing": "host wall clock, create+solve+readback"},
+                "d2h_bytes_per_step": d2h, "timing": "host wall clock, create+sample+readback"},
         "gpu_launches": ctr["own_launches"],
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if peak else None, "traffic": traffic,
-                     "traffic_source": TRAFFIC_CSV if traffic is not None else None,
+                     "frac": achieved / peak if peak else None, "traffic": dram_traffic_per_launch(),
+                     "traffic_source": TRAFFIC_CSV,
                      "kernel": "k_search (k_search_fast_min / _first builds for this model)",
                      "peak_kind": peak_kind,
-                     "algorithmic_bytes": "24*k B per scored leaf (k option rows x 3 fp64, "
-                                          "SURVEY.md 8d)",
-                     "note": "integer/branch-bound tree search; HBM is not the binding "
-                             "resource (see DESIGN.md)"},
+                     "algorithmic_bytes": "24*k B per last-level option screen (k option rows "
+                                          "x 3 fp64, SURVEY.md 8d)",
+                     "note": "branch-bound tree search; HBM is not the binding resource "
+                             "(DESIGN.md)"},
         "cpu_baseline": cpu,
         "evaluator": evaluator,
         "clocks": clk.summary(),

@@ -8,6 +8,9 @@
  *                               allocations (K1, host or device arrays)  perf_model.hpp:442-479
  *   mosaic_gpu_stage_time    <- the same for entries at any quota granularity
  *   mosaic_gpu_options       <- candidate_options                   stage_eval.hpp:68-93
+ *   mosaic_gpu_search        <- stage_eval / ExactStageSolver::solve over a batch of
+ *                               module sets (a GAHC round's candidates), one
+ *                               launch per wave of device searches       stage_eval.hpp:302-382
  *   mosaic_gpu_stage_eval    <- stage_eval (tau doubling, bisection,
  *                               confirmation probes; first leaf of the
  *                               last successful FeasibilitySearch::run) stage_eval.hpp:302-382
@@ -154,6 +157,16 @@ int mosaic_gpu_evaluate(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* entrie
 int mosaic_gpu_evaluate_stats(mosaic_gpu_ctx* ctx, double* kernel_ms, int64_t* launches,
                               int64_t* alg_bytes);
 
+/* Batched stage search (the plan enumerator + best-plan reduction of one GAHC round):
+ * out[i] = stage_eval (MOSAIC_SEARCH_STAGE_EVAL) or ExactStageSolver::solve
+ * (MOSAIC_SEARCH_EXACT) of module set masks[i].  The n computations advance together;
+ * every wave of their device searches (tau probes, MIN proofs) is ONE batched launch in
+ * which each search owns a slice of the resident grid.  Per-mask status in out[i].status. */
+#define MOSAIC_SEARCH_STAGE_EVAL 0
+#define MOSAIC_SEARCH_EXACT 1
+int mosaic_gpu_search(mosaic_gpu_ctx* ctx, const uint64_t* masks, int64_t n, int mode,
+                      mosaic_gpu_stage_result* out);
+
 /* stage_eval / ExactStageSolver::solve / FeasibilitySearch::run for one module set. */
 int mosaic_gpu_stage_eval(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_result* out);
 int mosaic_gpu_exact_stage(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_result* out);
@@ -246,21 +259,30 @@ int mosaic_gpu_cache_entry(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_
 
 /* Multi-GPU sharding of the search frontier (one rank per GPU).  The caller
  * supplies an all-gather of `bytes` from every rank (torch.distributed over NCCL
- * in bench.py); the library calls it once per device search with a 16-byte
- * record per rank.  world == 1 disables it. */
+ * in bench.py); the library calls it once per batched launch with one RankRecord
+ * (mosaic_gpu_rank_record_size() ~ 4.2 KB: flags, incumbent, FIRST hit path and leaf)
+ * per search of the launch.  world == 1 disables it. */
 typedef int (*mosaic_gpu_allgather_fn)(void* user, const void* send, void* recv, size_t bytes);
 int mosaic_gpu_set_shard(mosaic_gpu_ctx* ctx, int rank, int world, mosaic_gpu_allgather_fn fn,
                          void* user);
 
-/* Host-side merge of per-rank search records (exported for the gloo tests):
- * records are {u64 key, f64 value}; mode 0 = MIN (smallest value, then key),
- * mode 1 = FIRST (smallest key).  Writes the winning record index. */
-int mosaic_gpu_merge_records(const void* records, int world, int mode, int* winner);
+/* The merge every sharded search goes through (Engine::merge_ranks), exported for the
+ * multi-process CPU tests: world records of mosaic_gpu_rank_record_size() bytes, built with
+ * mosaic_gpu_rank_record (x is k rows of 128 block counts).  mode 0 = MIN (smallest
+ * incumbent, lowest rank on ties, restart if any rank restarted), 1 = FIRST (the hit earliest
+ * in reference DFS order).  *winner = the rank whose leaf is taken (-1: none). */
+size_t mosaic_gpu_rank_record_size(void);
+int mosaic_gpu_rank_record(void* rec, int has_hit, int aborted, int overflow, double inc, int k,
+                           const uint16_t* opt, const uint16_t* nb, const uint16_t* x,
+                           double leaf_value);
+int mosaic_gpu_merge_ranks(const void* records, int world, int mode, int k, int* winner,
+                           int* found, double* value, int* aborted, int* overflow,
+                           double* leaf_value);
 
 /* Search-engine knobs for experiments (tools/tune.py); defaults are the measured best and
  * nothing reads the environment.  Keys: don_depth, don_period (power of two), backoff_ns,
  * small_tree, deep_after, lookahead, small_grid, generic_kernel, shard_level,
- * ring_per_walker, trace, and the measurement-only share_rank / share_world (search one
+ * ring_per_walker, trace, spec_k (GAHC candidates up to this many modules are batched), and the measurement-only share_rank / share_world (search one
  * rank's share of a sharded search on this device, unmerged: NOT the stage's answer).
  * MOSAIC_INVALID_ARGUMENT for an unknown key. */
 int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value);

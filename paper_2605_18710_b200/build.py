@@ -23,7 +23,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["engine.cu", "eval.cu", "pack.cu", "sim.cu"]
 # engine_fast.cu is compiled once per search mode (specialised MIN / FIRST kernels)
 CU_VARIANTS = [("engine_fast.cu", "engine_fast_min", ["-DMG_FAST_MODE=0"]),
-               ("engine_fast.cu", "engine_fast_first", ["-DMG_FAST_MODE=1"])]
+               ("engine_fast.cu", "engine_fast_first", ["-DMG_FAST_MODE=1"]),
+               ("engine_fast.cu", "engine_fast_any", ["-DMG_FAST_MODE=2"])]
 CPP_SOURCES = ["model.cpp", "planner.cpp", "capi.cpp"]
 HEADERS = ["engine.hpp", "search_core.cuh", "search_warp.cuh", "search_kernel.cuh", "spec_build.hpp", "model.hpp",
            "planner.hpp", "pack.hpp", "sim.hpp"]

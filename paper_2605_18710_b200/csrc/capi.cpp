@@ -248,6 +248,19 @@ int mosaic_gpu_stage_eval(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_r
     });
 }
 
+int mosaic_gpu_search(mosaic_gpu_ctx* ctx, const uint64_t* masks, int64_t n, int mode,
+                      mosaic_gpu_stage_result* out) {
+    return guard([&] {
+        if (!ctx || (n > 0 && (!masks || !out))) throw Error(MOSAIC_RANGE, "null argument");
+        if (mode != MOSAIC_SEARCH_STAGE_EVAL && mode != MOSAIC_SEARCH_EXACT)
+            throw Error(MOSAIC_INVALID_ARGUMENT, "mode must be MOSAIC_SEARCH_STAGE_EVAL or _EXACT");
+        std::vector<uint64_t> ms(masks, masks + n);
+        std::vector<StageResult> rs = ctx->pl->stage_batch(ms, mode == MOSAIC_SEARCH_EXACT);
+        for (int64_t i = 0; i < n; ++i) fill_stage(rs[i], out + i);
+        return MOSAIC_OK;
+    });
+}
+
 int mosaic_gpu_exact_stage(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_result* out) {
     return guard([&] {
         StageResult r = ctx->pl->exact_stage(mask);
@@ -463,6 +476,7 @@ int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value) {
         else if (k == "shard_level") t.shard_level = (int)v;
         else if (k == "ring_per_walker") t.ring_per_walker = (int)std::max(1LL, v);
         else if (k == "trace") t.trace = v != 0;
+        else if (k == "spec_k") t.spec_k = (int)v;
         else if (k == "share_rank") t.share_rank = (int)v;
         else if (k == "share_world") t.share_world = (int)std::max(1LL, v);
         else throw Error(MOSAIC_INVALID_ARGUMENT, "unknown tuning key " + k);
@@ -472,25 +486,47 @@ int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value) {
 
 int64_t mosaic_gpu_device_bytes(mosaic_gpu_ctx* ctx) { return ctx->pl->engine().device_bytes(); }
 
-int mosaic_gpu_merge_records(const void* records, int world, int mode, int* winner) {
-    struct Rec {
-        uint64_t key;
-        double value;
-    };
-    const Rec* r = reinterpret_cast<const Rec*>(records);
-    int w = -1;
-    for (int i = 0; i < world; ++i) {
-        if (w < 0) {
-            w = i;
-            continue;
+size_t mosaic_gpu_rank_record_size(void) { return sizeof(mg::RankRecord); }
+
+int mosaic_gpu_rank_record(void* rec, int has_hit, int aborted, int overflow, double inc, int k,
+                           const uint16_t* opt, const uint16_t* nb, const uint16_t* x,
+                           double leaf_value) {
+    return guard([&] {
+        if (!rec || k < 0 || k > mg::MAXK) throw Error(MOSAIC_RANGE, "bad record arguments");
+        mg::RankRecord& r = *static_cast<mg::RankRecord*>(rec);
+        std::memset(&r, 0, sizeof r);
+        r.has_hit = has_hit;
+        r.aborted = aborted;
+        r.overflow = overflow;
+        r.inc = inc;
+        for (int l = 0; l < k; ++l) {
+            r.path.opt[l] = opt ? opt[l] : 0;
+            r.path.nb[l] = nb ? nb[l] : 0;
+            if (nb && nb[l] > mg::MAXB) throw Error(MOSAIC_RANGE, "too many blocks");
+            for (int b = 0; nb && x && b < nb[l]; ++b) r.path.x[l][b] = x[l * mg::MAXB + b];
+            r.leaf.opt[l] = r.path.opt[l];
         }
-        bool better = mode == 0 ? (r[i].value < r[w].value ||
-                                   (r[i].value == r[w].value && r[i].key < r[w].key))
-                                : r[i].key < r[w].key;
-        if (better) w = i;
-    }
-    *winner = w;
-    return w < 0 ? MOSAIC_RANGE : MOSAIC_OK;
+        r.leaf.value = leaf_value;
+        return MOSAIC_OK;
+    });
+}
+
+int mosaic_gpu_merge_ranks(const void* records, int world, int mode, int k, int* winner,
+                           int* found, double* value, int* aborted, int* overflow,
+                           double* leaf_value) {
+    return guard([&] {
+        if (!records || world < 1) throw Error(MOSAIC_RANGE, "bad records");
+        mg::SearchResult res;
+        const int w = mg::merge_rank_records(static_cast<const mg::RankRecord*>(records), world,
+                                             mode, k, res);
+        if (winner) *winner = w;
+        if (found) *found = res.found ? 1 : 0;
+        if (value) *value = res.value;
+        if (aborted) *aborted = res.aborted ? 1 : 0;
+        if (overflow) *overflow = res.overflow ? 1 : 0;
+        if (leaf_value) *leaf_value = res.found ? res.leaf.value : 0.0;
+        return MOSAIC_OK;
+    });
 }
 
 int64_t mosaic_gpu_launch_count(mosaic_gpu_ctx* ctx) { return ctx->pl->engine().launches(); }

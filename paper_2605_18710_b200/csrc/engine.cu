@@ -42,6 +42,7 @@ namespace mg {
 
 const void* k_search_fast_min_fn();    // engine_fast.cu, MG_FAST_MODE=0
 const void* k_search_fast_first_fn();  // engine_fast.cu, MG_FAST_MODE=1
+const void* k_search_fast_any_fn();    // engine_fast.cu, MG_FAST_MODE=2 (mode read at run time)
 
 
 // ---------------------------------------------------------------------------
@@ -117,14 +118,6 @@ __global__ void __launch_bounds__(32 * EVAL_WARPS)
 // ---------------------------------------------------------------------------
 static inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// pinned staging layout: Spec | Ctl | Leaf | Cont | int, each 256-B aligned
-static inline size_t pin_off(int i) {
-    const size_t sz[5] = {sizeof(Spec), sizeof(Ctl), sizeof(Leaf), sizeof(Cont), sizeof(int)};
-    size_t off = 0;
-    for (int k = 0; k < i; ++k) off += (sz[k] + 255) & ~size_t(255);
-    return off;
-}
-
 Engine::Engine(int device) : device_(device) {
     CK(cudaSetDevice(device));
     cudaStream_t s;
@@ -144,14 +137,13 @@ Engine::Engine(int device) : device_(device) {
     evk1_ = d;
     evm0_ = e;
     evm1_ = f;
-    // device mirror of the pinned staging layout: one upload and one read-back per search
-    CK(cudaMalloc(&d_blob_, pin_off(5)));
-    dev_bytes_ += (long long)pin_off(5);
-    d_spec_ = static_cast<char*>(d_blob_) + pin_off(0);
-    d_ctl_ = static_cast<char*>(d_blob_) + pin_off(1);
-    d_leaf_ = static_cast<char*>(d_blob_) + pin_off(2);
-    d_root_ = static_cast<char*>(d_blob_) + pin_off(3);
-    CK(cudaMallocHost(&h_pin_, pin_off(5)));
+    // per-search staging blobs (Spec | Ctl | Leaf | root Cont) for a whole batch: one upload
+    // and one strided read-back per launch
+    CK(cudaMalloc(&d_blob_, MAXBATCH * BLOB_STRIDE));
+    CK(cudaMallocHost(&h_pin_, MAXBATCH * BLOB_STRIDE));
+    CK(cudaMalloc(&d_best_, MAXBATCH * sizeof(HitPath)));
+    CK(cudaMallocHost(&h_best_, MAXBATCH * sizeof(HitPath)));
+    dev_bytes_ += (long long)(MAXBATCH * (BLOB_STRIDE + sizeof(HitPath)));
 }
 
 Engine::~Engine() {
@@ -168,6 +160,7 @@ Engine::~Engine() {
     cudaFree(d_ready_);
     cudaFree(d_best_);
     cudaFreeHost(h_pin_);
+    cudaFreeHost(h_best_);
     cudaEventDestroy((cudaEvent_t)ev0_);
     cudaEventDestroy((cudaEvent_t)ev1_);
     cudaEventDestroy((cudaEvent_t)evk0_);
@@ -230,171 +223,256 @@ void Engine::ensure_front(long long n) {
     CK(cudaMemset(d_ready_, 0, cap * sizeof(int)));
     dev_bytes_ += cap * (long long)(sizeof(Cont) + sizeof(int));
     ticket_base_ = 0;
-    if (!d_best_) {
-        CK(cudaMalloc(&d_best_, sizeof(HitPath)));
-        dev_bytes_ += sizeof(HitPath);
-    }
     front_cap_ = cap;
 }
 
 SearchResult Engine::search(const Spec& S, double ub, double abort_below, SearchStats& st,
                             const HitPath* seed_path, const Leaf* seed_leaf) {
-    CK(cudaSetDevice(device_));
-    cudaStream_t s = S_(stream_);
-    SearchResult res;
-    res.value = ub;
-    Rows R{d_base_, d_B_, d_fp_, d_bound_, d_d_, d_u_};
-    char* pin = reinterpret_cast<char*>(h_pin_);
-    Spec* hs = reinterpret_cast<Spec*>(pin + pin_off(0));
-    Ctl* hc = reinterpret_cast<Ctl*>(pin + pin_off(1));
-    Leaf* hl = reinterpret_cast<Leaf*>(pin + pin_off(2));
-    Cont* hr = reinterpret_cast<Cont*>(pin + pin_off(3));
-    int* hone = reinterpret_cast<int*>(pin + pin_off(4));
-    *hs = S;
-    hs->shard_rank = rank_;
-    hs->shard_world = world_;
-    if (world_ == 1 && tune_.share_world > 1) {
-        hs->shard_rank = tune_.share_rank;
-        hs->shard_world = tune_.share_world;
+    std::vector<BatchReq> one(1);
+    one[0].S = S;
+    one[0].ub = ub;
+    one[0].abort_below = abort_below;
+    one[0].seed_path = seed_path;
+    one[0].seed_leaf = seed_leaf;
+    one[0].st = &st;
+    return search_batch(one)[0];
+}
+
+// Kernel, shared memory and resident grid for (kernel index, smem bytes).
+void Engine::kernel_for(const std::vector<BatchReq>& reqs, size_t b0, size_t b1,
+                        const void** kfn, size_t* smem, long long* grid) {
+    const Spec& S0 = reqs[b0].S;
+    // the specialised kernels when the model is the common one (same search, fewer branches);
+    // a batch mixing MIN and FIRST searches runs the dynamic-mode build
+    const bool fast = S0.include_self && S0.nonneg && !S0.additive && !tune_.generic_kernel;
+    bool all_min = true, all_first = true;
+    int kmax = 1;
+    for (size_t i = b0; i < b1; ++i) {
+        all_min &= reqs[i].S.mode == MODE_MIN;
+        all_first &= reqs[i].S.mode == MODE_FIRST;
+        kmax = std::max(kmax, reqs[i].S.k);
     }
-    // option prefixes (o_0, o_1, o_2) are hashed to ranks: at 8 ranks the largest share of the
-    // dominant cfg5 proof is 1.15x the mean (pairs: 1.3x; tools/shard_levels.sh)
-    hs->shard_level = S.k >= 3 ? 2 : S.k - 1;
-    if (tune_.shard_level >= 0) hs->shard_level = std::min(tune_.shard_level, S.k - 1);
-    // donation policy: hand over only shallow levels, when the queue has run dry
-    hs->don_max_level = S.k >= 6 ? S.k - 1 - tune_.don_depth : (S.k >= 3 ? S.k - 3 : 0);
-    // long-running pieces may also hand over levels <= k-3 (see WarpHooks::abort)
-    hs->don_max_level_tail = S.k - 3 > hs->don_max_level ? S.k - 3 : hs->don_max_level;
-    hs->deep_after = tune_.deep_after;
-    hs->lookahead = tune_.lookahead;
-    hs->don_period = tune_.don_period;
-    hs->backoff_cap_ns = tune_.backoff_cap;
-    std::memset(hc, 0, sizeof(Ctl));
-    union {
-        double d;
-        unsigned long long u;
-    } cv;
-    cv.d = ub;
-    hc->inc = cv.u;
-    hc->abort_below = abort_below;
-    // tickets keep counting across searches, so slots never need clearing: a stale
-    // ready value belongs to an older (smaller) ticket and can never match (q_head/q_tail
-    // are set once the ring is sized, below)
-    hc->outstanding = 1;
-    std::memset(hr, 0, sizeof(Cont));
-    hr->depth = 0;
-    hr->nb = 1;
-    hr->ph = 0;
-    hr->oc = -1;
-    hr->oe = (int16_t)S.lvl_n[0];
-    hr->bsz[0] = (uint16_t)S.G;
-    *hone = 1;
-    // the specialised kernel when the model is the common one (same search, fewer branches)
-    const bool fast = S.include_self && S.nonneg && !S.additive && !tune_.generic_kernel;
-    const size_t smem = smem_bytes(S.G, S.k, fast);
-    const void* kfn = !fast ? reinterpret_cast<const void*>(&k_search)
-                      : S.mode == MODE_MIN ? k_search_fast_min_fn() : k_search_fast_first_fn();
-    const int ki = !fast ? 0 : (S.mode == MODE_MIN ? 1 : 2);
-    if (smem != grid_smem_[ki]) {
-        if (smem > smem_attr_[ki]) {
-            CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            smem_attr_[ki] = smem;
+    int ki = 0;
+    *kfn = reinterpret_cast<const void*>(&k_search);
+    if (fast) {
+        ki = all_min ? 1 : (all_first ? 2 : 3);
+        *kfn = all_min ? k_search_fast_min_fn()
+                       : (all_first ? k_search_fast_first_fn() : k_search_fast_any_fn());
+    }
+    *smem = smem_bytes(S0.G, kmax, fast);
+    const long long key = (long long)ki << 40 | (long long)*smem;
+    auto it = grid_cache_.find(key);
+    if (it == grid_cache_.end()) {
+        if (*smem > smem_attr_[ki]) {
+            CK(cudaFuncSetAttribute(*kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
+            smem_attr_[ki] = *smem;
         }
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 32 * WPC, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, *kfn, 32 * WPC, *smem));
         int sms = 148;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
-        grid_k_[ki] = std::max(1, per_sm) * sms;  // all resident: spin-waiting needs it
-        grid_smem_[ki] = smem;
+        // every CTA resident: walkers spin-wait on each other
+        it = grid_cache_.emplace(key, (long long)std::max(1, per_sm) * sms).first;
     }
-    grid_ = grid_k_[ki];
-    ensure_front(grid_ * WPC * std::max(1, tune_.ring_per_walker));
-    const long long cap = front_cap_;
+    *grid = it->second;
+}
+
+std::vector<SearchResult> Engine::search_batch(std::vector<BatchReq>& reqs) {
+    CK(cudaSetDevice(device_));
+    std::vector<SearchResult> out(reqs.size());
+    size_t b0 = 0;
+    while (b0 < reqs.size()) {
+        // chunk: at most MAXBATCH searches, all resident at once
+        const void* kfn;
+        size_t smem;
+        long long grid_cap;
+        size_t b1 = std::min(reqs.size(), b0 + (size_t)MAXBATCH);
+        kernel_for(reqs, b0, b1, &kfn, &smem, &grid_cap);
+        b1 = std::min<size_t>(b1, b0 + (size_t)std::max<long long>(1, grid_cap / std::max(1, tune_.small_grid)));
+        launch_chunk(reqs, b0, b1, kfn, smem, grid_cap, out);
+        b0 = b1;
+    }
+    return out;
+}
+
+void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, const void* kfn,
+                          size_t smem, long long grid_cap, std::vector<SearchResult>& out) {
+    cudaStream_t s = S_(stream_);
+    const int n = (int)(b1 - b0);
+    Rows R{d_base_, d_B_, d_fp_, d_bound_, d_d_, d_u_};
+    char* pin = reinterpret_cast<char*>(h_pin_);
+    HitPath* hbest = reinterpret_cast<HitPath*>(h_best_);
+    // CTAs per search: small trees (few option tuples) finish on a handful of CTAs without
+    // hand-overs; the rest share the resident grid equally
+    std::vector<int> ctas(n);
+    std::vector<char> small(n);
+    long long small_total = 0;
+    int n_big = 0;
+    for (int i = 0; i < n; ++i) {
+        const Spec& S = reqs[b0 + i].S;
+        double tuples = 1.0;
+        for (int l = 0; l < S.k; ++l) tuples *= (double)(S.lvl_n[l] > 0 ? S.lvl_n[l] : 1);
+        small[i] = tuples * S.G <= tune_.small_tree;
+        if (small[i]) {
+            ctas[i] = (int)std::min<long long>(tune_.small_grid, std::max<long long>(1, grid_cap / n));
+            small_total += ctas[i];
+        } else {
+            ++n_big;
+        }
+    }
+    const long long left = std::max<long long>(0, grid_cap - small_total);
+    for (int i = 0; i < n; ++i)
+        if (!small[i]) ctas[i] = (int)std::max<long long>(1, left / std::max(1, n_big));
+    BatchMap map;
+    std::memset(&map, 0, sizeof map);
+    map.n = n;
+    long long qtot = 0;
+    for (int i = 0; i < n; ++i) {
+        map.cta_off[i + 1] = map.cta_off[i] + ctas[i];
+        map.q_off[i] = qtot;
+        qtot += (long long)ctas[i] * WPC * std::max(1, tune_.ring_per_walker);
+    }
+    ensure_front(qtot);
     const unsigned long long t0 = ticket_base_;
-    hc->q_head = t0;
-    hc->q_tail = t0 + 1;
-    hc->q_cap = (unsigned long long)cap;
-    Cont* Q = reinterpret_cast<Cont*>(d_front_[0]);
-    // small trees (few option tuples) do not need the whole GPU: a handful of resident
-    // CTAs finishes them without spinning up thousands of idle walkers
-    double tuples = 1.0;
-    for (int l = 0; l < S.k; ++l) tuples *= (double)(S.lvl_n[l] > 0 ? S.lvl_n[l] : 1);
-    const long long grid = (tuples * S.G <= tune_.small_tree) ? std::min<long long>(grid_, tune_.small_grid) : grid_;
-    hc->walkers = (unsigned)(grid * WPC);
-    // small trees: hand-overs cost more than they parallelise (each is a 1.3 KB piece
-    // round trip through L2); let the walker that owns the root finish it
-    hs->donate = grid < grid_ ? 0 : 1;
-    CK(cudaEventRecord((cudaEvent_t)ev0_, s));
-    if (S.mode == MODE_FIRST && seed_path && seed_leaf) {
-        // a known leaf <= theta: the search only has to look at what precedes it
-        hc->has_hit = 1;
-        *hl = *seed_leaf;
-        CK(cudaMemcpyAsync(d_best_, seed_path, sizeof(HitPath), cudaMemcpyHostToDevice, s));
-        h2d_ += sizeof(HitPath);
+    for (int i = 0; i < n; ++i) {
+        BatchReq& q = reqs[b0 + i];
+        char* blob = pin + (size_t)i * BLOB_STRIDE;
+        Spec* hs = reinterpret_cast<Spec*>(blob + BLOB_SPEC);
+        Ctl* hc = reinterpret_cast<Ctl*>(blob + BLOB_CTL);
+        Leaf* hl = reinterpret_cast<Leaf*>(blob + BLOB_LEAF);
+        Cont* hr = reinterpret_cast<Cont*>(blob + BLOB_ROOT);
+        const Spec& S = q.S;
+        *hs = S;
+        hs->shard_rank = rank_;
+        hs->shard_world = world_;
+        if (world_ == 1 && tune_.share_world > 1) {
+            hs->shard_rank = tune_.share_rank;
+            hs->shard_world = tune_.share_world;
+        }
+        // option prefixes (o_0, o_1, o_2) are hashed to ranks: at 8 ranks the largest share of
+        // the dominant cfg5 proof is 1.15x the mean (pairs: 1.3x)
+        hs->shard_level = S.k >= 3 ? 2 : S.k - 1;
+        if (tune_.shard_level >= 0) hs->shard_level = std::min(tune_.shard_level, S.k - 1);
+        // donation policy: hand over only shallow levels, when the queue has run dry
+        hs->don_max_level = S.k >= 6 ? S.k - 1 - tune_.don_depth : (S.k >= 3 ? S.k - 3 : 0);
+        // long-running pieces may also hand over levels <= k-3 (see WarpHooks::abort)
+        hs->don_max_level_tail = S.k - 3 > hs->don_max_level ? S.k - 3 : hs->don_max_level;
+        hs->deep_after = tune_.deep_after;
+        hs->lookahead = tune_.lookahead;
+        hs->don_period = tune_.don_period;
+        hs->backoff_cap_ns = tune_.backoff_cap;
+        // small trees: hand-overs cost more than they parallelise; the root's walker finishes
+        hs->donate = small[i] ? 0 : 1;
+        std::memset(hc, 0, sizeof(Ctl));
+        union {
+            double d;
+            unsigned long long u;
+        } cv;
+        cv.d = q.ub;
+        hc->inc = cv.u;
+        hc->abort_below = q.abort_below;
+        // tickets keep counting across launches (every search of this launch starts at t0),
+        // so ring slots never need clearing: a stale ready value belongs to an older ticket
+        hc->outstanding = 1;
+        hc->q_head = t0;
+        hc->q_tail = t0 + 1;
+        hc->q_cap = (unsigned long long)ctas[i] * WPC * std::max(1, tune_.ring_per_walker);
+        hc->walkers = (unsigned)(ctas[i] * WPC);
+        std::memset(hr, 0, sizeof(Cont));
+        hr->depth = 0;
+        hr->nb = 1;
+        hr->ph = 0;
+        hr->oc = -1;
+        hr->oe = (int16_t)S.lvl_n[0];
+        hr->bsz[0] = (uint16_t)S.G;
+        if (S.mode == MODE_FIRST && q.seed_path && q.seed_leaf) {
+            // a known leaf <= theta: the search only has to look at what precedes it
+            hc->has_hit = 1;
+            *hl = *q.seed_leaf;
+            hbest[i] = *q.seed_path;
+        }
     }
-    // Spec | Ctl | Leaf | root Cont in one upload (the kernel publishes the root piece)
-    CK(cudaMemcpyAsync(d_blob_, h_pin_, pin_off(4), cudaMemcpyHostToDevice, s));
-    h2d_ += (long long)pin_off(4);
-    const long long slot0 = (long long)(t0 % (unsigned long long)cap);
+    CK(cudaEventRecord((cudaEvent_t)ev0_, s));
+    for (int i = 0; i < n; ++i)
+        if (reqs[b0 + i].S.mode == MODE_FIRST && reqs[b0 + i].seed_path && reqs[b0 + i].seed_leaf) {
+            CK(cudaMemcpyAsync(static_cast<HitPath*>(d_best_) + i, hbest + i, sizeof(HitPath),
+                               cudaMemcpyHostToDevice, s));
+            h2d_ += sizeof(HitPath);
+        }
+    // every search's Spec | Ctl | Leaf | root Cont in one upload
+    CK(cudaMemcpyAsync(d_blob_, h_pin_, (size_t)n * BLOB_STRIDE, cudaMemcpyHostToDevice, s));
+    h2d_ += (long long)n * BLOB_STRIDE;
     CK(cudaEventRecord((cudaEvent_t)evk0_, s));
     {
-        const Spec* a0 = (const Spec*)d_spec_;
-        Ctl* a4 = (Ctl*)d_ctl_;
-        HitPath* a5 = (HitPath*)d_best_;
-        Leaf* a6 = (Leaf*)d_leaf_;
-        const Cont* a7 = (const Cont*)d_root_;
+        char* db = static_cast<char*>(d_blob_);
+        const Spec* a0 = reinterpret_cast<const Spec*>(db + BLOB_SPEC);
+        Ctl* a4 = reinterpret_cast<Ctl*>(db + BLOB_CTL);
+        HitPath* a5 = static_cast<HitPath*>(d_best_);
+        Leaf* a6 = reinterpret_cast<Leaf*>(db + BLOB_LEAF);
+        const Cont* a7 = reinterpret_cast<const Cont*>(db + BLOB_ROOT);
+        Cont* Q = reinterpret_cast<Cont*>(d_front_[0]);
         int* a3 = d_ready_;
-        long long a8 = slot0;
         int a9 = (int)(t0 + 1);
-        void* args[] = {&a0, &R, &Q, &a3, &a4, &a5, &a6, &a7, &a8, &a9};
-        CK(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(32 * WPC), args, smem, s));
+        void* args[] = {&a0, &R, &Q, &a3, &a4, &a5, &a6, &a7, &map, &a9};
+        CK(cudaLaunchKernel(kfn, dim3((unsigned)map.cta_off[n]), dim3(32 * WPC), args, smem, s));
     }
     CK(cudaEventRecord((cudaEvent_t)evk1_, s));
     ++launches_;
     ++own_launches_;
-    ++st.rounds;
-    // one read-back and one synchronisation per search: the control block and the leaf
-    // (1 KB, read unconditionally — cheaper than a second round trip when there is a hit)
-    CK(cudaMemcpyAsync(hc, d_ctl_, pin_off(3) - pin_off(1), cudaMemcpyDeviceToHost, s));
-    d2h_ += (long long)(pin_off(3) - pin_off(1));
+    // one strided read-back of every search's control block and leaf, one synchronisation
+    CK(cudaMemcpy2DAsync(pin + BLOB_CTL, BLOB_STRIDE, static_cast<char*>(d_blob_) + BLOB_CTL,
+                         BLOB_STRIDE, BLOB_ROOT - BLOB_CTL, n, cudaMemcpyDeviceToHost, s));
+    d2h_ += (long long)n * (BLOB_ROOT - BLOB_CTL);
     CK(cudaEventRecord((cudaEvent_t)ev1_, s));
     CK(cudaEventSynchronize((cudaEvent_t)ev1_));
     CK(cudaGetLastError());
-    ticket_base_ = hc->q_tail + 1;
-    if (hc->has_hit && !hc->overflow) {
-        res.found = true;
-        res.leaf = *hl;
-    }
-    if (hc->overflow) res.overflow = true;
-    if (S.mode == MODE_MIN) {
-        if (hc->abort && !hc->overflow) res.aborted = true;
-        union {
-            unsigned long long u;
-            double d;
-        } w;
-        w.u = hc->inc;
-        res.value = w.d;
-    }
-    // ranks must leave every search with the same answer (they replay the same control
-    // flow and all-gather once per search): merge after the local result is complete
-    if (world_ > 1 && ag_) merge_ranks(S, hc, res);
     float kms = 0, ms = 0;
     CK(cudaEventElapsedTime(&kms, (cudaEvent_t)evk0_, (cudaEvent_t)evk1_));
     CK(cudaEventElapsedTime(&ms, (cudaEvent_t)ev0_, (cudaEvent_t)ev1_));
     ksearch_ms_ += kms;
     ++ksearch_n_;
     search_ms_ += ms;
-    st.nodes += (long long)hc->nodes;
-    st.leaves += (long long)hc->leaves;
-    ++st.searches;
-    alg_bytes_ += (long long)hc->leaves * 24LL * S.k;  // k option rows x 3 fp64 per leaf
-    if (tune_.trace)
-        std::fprintf(stderr, "[mosaic] %s k=%d thr=%.17g kernel=%.3fms total=%.3fms nodes=%llu "
-                             "leaves=%llu donated=%llu %s\n",
-                     S.mode == MODE_MIN ? "MIN  " : "FIRST", S.k,
-                     S.mode == MODE_MIN ? ub : S.theta, kms, ms, hc->nodes, hc->leaves,
-                     hc->q_tail - 1, res.found ? "hit" : (res.aborted ? "restart" : ""));
-    return res;
+    unsigned long long tmax = t0;
+    for (int i = 0; i < n; ++i) {
+        const BatchReq& q = reqs[b0 + i];
+        const Spec& S = q.S;
+        const char* blob = pin + (size_t)i * BLOB_STRIDE;
+        const Ctl* hc = reinterpret_cast<const Ctl*>(blob + BLOB_CTL);
+        const Leaf* hl = reinterpret_cast<const Leaf*>(blob + BLOB_LEAF);
+        SearchResult& res = out[b0 + i];
+        res.value = q.ub;
+        tmax = std::max<unsigned long long>(tmax, hc->q_tail);
+        if (hc->has_hit && !hc->overflow) {
+            res.found = true;
+            res.leaf = *hl;
+        }
+        if (hc->overflow) res.overflow = true;
+        if (S.mode == MODE_MIN) {
+            if (hc->abort && !hc->overflow) res.aborted = true;
+            union {
+                unsigned long long u;
+                double d;
+            } w;
+            w.u = hc->inc;
+            res.value = w.d;
+        }
+        SearchStats& st = *q.st;
+        ++st.rounds;
+        st.nodes += (long long)hc->nodes;
+        st.leaves += (long long)hc->leaves;
+        ++st.searches;
+        alg_bytes_ += (long long)hc->leaves * 24LL * S.k;  // k option rows x 3 fp64 per leaf
+        if (tune_.trace)
+            std::fprintf(stderr, "[mosaic] %s k=%d thr=%.17g batch=%d ctas=%d kernel=%.3fms total=%.3fms "
+                                 "nodes=%llu leaves=%llu %s\\n",
+                         S.mode == MODE_MIN ? "MIN  " : "FIRST", S.k,
+                         S.mode == MODE_MIN ? q.ub : S.theta, n, ctas[i], kms, ms, hc->nodes,
+                         hc->leaves, res.found ? "hit" : (res.aborted ? "restart" : ""));
+    }
+    ticket_base_ = tmax + 1;
+    // ranks must leave every search with the same answer (they replay the same control flow
+    // and all-gather once per launch): merge after the local results are complete
+    if (world_ > 1 && ag_) merge_ranks(reqs, b0, b1, out);
 }
 
 void Engine::evaluate(const std::vector<EvalEntry>& ent, const std::vector<int>& gpus,
@@ -453,17 +531,11 @@ void Engine::evaluate(const std::vector<EvalEntry>& ent, const std::vector<int>&
     CK(cudaStreamSynchronize(s));
 }
 
-// One all-gather per search (NCCL through the caller's callback): every rank contributes
-// its outcome; MIN takes the smallest incumbent and restarts everywhere if any rank
-// restarted, FIRST takes the hit that is earliest in reference DFS order.
-struct RankRecord {
-    int has_hit, aborted, overflow, pad;
-    double inc;
-    unsigned long long nodes, leaves;
-    HitPath path;
-    Leaf leaf;
-};
-
+// Multi-GPU: ranks search disjoint option-prefix shards of every search of a launch and
+// exchange one RankRecord per search (one all-gather per launch through the caller's
+// callback).  MIN takes the smallest incumbent (its argmin leaf from the rank holding it,
+// lowest rank on ties) and restarts everywhere if any rank restarted; FIRST takes the hit
+// that is earliest in reference DFS order.
 static int host_path_cmp(const HitPath& a, const HitPath& b, int k) {
     for (int l = 0; l < k; ++l) {
         if (a.opt[l] != b.opt[l]) return a.opt[l] < b.opt[l] ? -1 : 1;
@@ -473,33 +545,11 @@ static int host_path_cmp(const HitPath& a, const HitPath& b, int k) {
     return 0;
 }
 
-void Engine::merge_ranks(const Spec& S, const void* ctl_host, SearchResult& res) {
-    const Ctl* hc = reinterpret_cast<const Ctl*>(ctl_host);
-    if (!ag_) throw std::runtime_error("multi-GPU search without an all-gather");
-    std::vector<RankRecord> all(world_);
-    RankRecord mine;
-    std::memset(&mine, 0, sizeof mine);
-    mine.has_hit = res.found ? 1 : 0;
-    mine.aborted = res.aborted ? 1 : 0;
-    mine.overflow = res.overflow ? 1 : 0;
-    union {
-        unsigned long long u;
-        double d;
-    } w;
-    w.u = hc->inc;
-    mine.inc = w.d;
-    mine.nodes = hc->nodes;
-    mine.leaves = hc->leaves;
-    if (res.found) {
-        CK(cudaMemcpy(&mine.path, d_best_, sizeof(HitPath), cudaMemcpyDeviceToHost));
-        mine.leaf = res.leaf;
-    }
-    if (ag_(ag_user_, &mine, all.data(), sizeof(RankRecord)) != 0)
-        throw std::runtime_error("all-gather failed");
+int merge_rank_records(const RankRecord* all, int world, int mode, int k, SearchResult& res) {
     int win = -1, minr = -1;
     double best = POS_INF;
     bool aborted = false, overflow = false;
-    for (int r = 0; r < world_; ++r) {
+    for (int r = 0; r < world; ++r) {
         const RankRecord& x = all[r];
         aborted |= x.aborted != 0;
         overflow |= x.overflow != 0;
@@ -507,19 +557,65 @@ void Engine::merge_ranks(const Spec& S, const void* ctl_host, SearchResult& res)
             best = x.inc;
             minr = r;
         }
-        if (x.has_hit && (win < 0 || host_path_cmp(x.path, all[win].path, S.k) < 0)) win = r;
+        if (x.has_hit && (win < 0 || host_path_cmp(x.path, all[win].path, k) < 0)) win = r;
     }
     res.overflow = overflow;
-    if (S.mode == MODE_MIN) {
-        // T* is the smallest incumbent; its leaf (the argmin the planner canonicalises)
-        // comes from the rank that holds it (lowest rank on ties)
+    if (mode == MODE_MIN) {
         res.aborted = aborted;
         res.value = best;
         res.found = all[minr].has_hit != 0;
         if (res.found) res.leaf = all[minr].leaf;
-    } else {
-        res.found = win >= 0;
-        if (win >= 0) res.leaf = all[win].leaf;
+        return minr;
+    }
+    res.found = win >= 0;
+    if (win >= 0) res.leaf = all[win].leaf;
+    return win;
+}
+
+void Engine::merge_ranks(const std::vector<BatchReq>& reqs, size_t b0, size_t b1,
+                         std::vector<SearchResult>& out) {
+    if (!ag_) throw std::runtime_error("multi-GPU search without an all-gather");
+    const size_t n = b1 - b0;
+    const char* pin = reinterpret_cast<const char*>(h_pin_);
+    std::vector<RankRecord> mine(n), all(n * world_);
+    std::vector<char> need_path(n, 0);
+    for (size_t i = 0; i < n; ++i) need_path[i] = out[b0 + i].found;
+    HitPath* hbest = reinterpret_cast<HitPath*>(h_best_);
+    bool any = false;
+    for (size_t i = 0; i < n; ++i) any |= need_path[i] != 0;
+    if (any) {
+        CK(cudaMemcpyAsync(hbest, d_best_, n * sizeof(HitPath), cudaMemcpyDeviceToHost,
+                           S_(stream_)));
+        CK(cudaStreamSynchronize(S_(stream_)));
+    }
+    for (size_t i = 0; i < n; ++i) {
+        const Ctl* hc = reinterpret_cast<const Ctl*>(pin + i * BLOB_STRIDE + BLOB_CTL);
+        const SearchResult& res = out[b0 + i];
+        RankRecord& m = mine[i];
+        std::memset(&m, 0, sizeof m);
+        m.has_hit = res.found ? 1 : 0;
+        m.aborted = res.aborted ? 1 : 0;
+        m.overflow = res.overflow ? 1 : 0;
+        union {
+            unsigned long long u;
+            double d;
+        } w;
+        w.u = hc->inc;
+        m.inc = w.d;
+        m.nodes = hc->nodes;
+        m.leaves = hc->leaves;
+        if (res.found) {
+            m.path = hbest[i];
+            m.leaf = res.leaf;
+        }
+    }
+    // all-gather of n records per rank: rank r's records land at all[r * n .. r * n + n)
+    if (ag_(ag_user_, mine.data(), all.data(), n * sizeof(RankRecord)) != 0)
+        throw std::runtime_error("all-gather failed");
+    std::vector<RankRecord> per(world_);
+    for (size_t i = 0; i < n; ++i) {
+        for (int r = 0; r < world_; ++r) per[r] = all[(size_t)r * n + i];
+        merge_rank_records(per.data(), world_, reqs[b0 + i].S.mode, reqs[b0 + i].S.k, out[b0 + i]);
     }
 }
 

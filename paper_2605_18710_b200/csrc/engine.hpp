@@ -1,6 +1,7 @@
 // engine.hpp — device search engine (sm_100a) used by the host planner.
 #pragma once
 #include <cstdint>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -21,6 +22,29 @@ struct SearchResult {
     bool aborted = false;    // MIN: incumbent fell below abort_below
     bool overflow = false;   // a level needed more than MAXB blocks
 };
+
+// One search of a batched launch (Engine::search_batch).
+struct BatchReq {
+    Spec S;
+    double ub = POS_INF;           // MIN: incumbent upper bound
+    double abort_below = 0.0;      // MIN: restart when the incumbent drops below
+    const HitPath* seed_path = nullptr;  // FIRST: a leaf known to satisfy theta ...
+    const Leaf* seed_leaf = nullptr;     // ... as a path in this search's order
+    SearchStats* st = nullptr;     // counters of the caller
+};
+
+// What a rank contributes to the merge of one sharded search (one all-gather per launch:
+// sizeof(RankRecord) ~ 4.2 KB per search — HitPath 3,120 B + Leaf 1,064 B + flags).
+struct RankRecord {
+    int has_hit, aborted, overflow, pad;
+    double inc;
+    unsigned long long nodes, leaves;
+    HitPath path;
+    Leaf leaf;
+};
+// The merge rule the engine applies to every sharded search (exported through the C ABI
+// for the multi-process CPU tests).  Returns the winning rank (-1: no FIRST hit).
+int merge_rank_records(const RankRecord* all, int world, int mode, int k, SearchResult& res);
 
 struct EvalEntry {  // device evaluator input (one per allocation entry)
     int row;        // option row (base, B) of this entry
@@ -63,6 +87,7 @@ struct Tuning {
     int shard_level = -1;   // override of the sharded option-prefix level (-1: default)
     int ring_per_walker = 16;  // cursor-ring slots per resident walker
     int trace = 0;          // one stderr line per device search
+    int spec_k = 4;         // GAHC: batch-evaluate a round's candidates of up to spec_k modules
     // measurement only (tools/): search rank share_rank's share of a share_world-way
     // sharded search on this one device, without merging — NOT the stage's answer
     int share_rank = 0, share_world = 1;
@@ -80,6 +105,9 @@ class Engine {
     // seed (FIRST only): a leaf known to satisfy theta, as a path in this search's order
     SearchResult search(const Spec& S, double ub, double abort_below, SearchStats& st,
                         const HitPath* seed_path = nullptr, const Leaf* seed_leaf = nullptr);
+    // Independent searches in as few launches as possible (one per MAXBATCH / resident grid):
+    // each gets its own CTA range, control block and ring slice (search_kernel.cuh).
+    std::vector<SearchResult> search_batch(std::vector<BatchReq>& reqs);
     // Batched stage_time (K1): per allocation, entries [off[i], off[i+1]).
     void evaluate(const std::vector<EvalEntry>& ent, const std::vector<int>& gpus,
                   const std::vector<long long>& off, const std::vector<double>& base,
@@ -138,7 +166,12 @@ class Engine {
 
   private:
     void ensure_front(long long n);
-    void merge_ranks(const Spec& S, const void* ctl_host, SearchResult& res);
+    void kernel_for(const std::vector<BatchReq>& reqs, size_t b0, size_t b1, const void** kfn,
+                    size_t* smem, long long* grid);
+    void launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, const void* kfn,
+                      size_t smem, long long grid_cap, std::vector<SearchResult>& out);
+    void merge_ranks(const std::vector<BatchReq>& reqs, size_t b0, size_t b1,
+                     std::vector<SearchResult>& out);
     int device_;
     int rank_ = 0, world_ = 1;
     AllGatherFn ag_ = nullptr;
@@ -150,18 +183,14 @@ class Engine {
     double *d_base_ = nullptr, *d_B_ = nullptr, *d_fp_ = nullptr, *d_bound_ = nullptr;
     int *d_d_ = nullptr, *d_u_ = nullptr;
     int n_rows_ = 0;
-    void* d_blob_ = nullptr;  // Spec | Ctl | Leaf | root Cont (pin_off layout)
-    void* d_root_ = nullptr;
-    void* d_spec_ = nullptr;
-    void* d_ctl_ = nullptr;
-    void* d_leaf_ = nullptr;
+    void* d_blob_ = nullptr;  // MAXBATCH x (Spec | Ctl | Leaf | root Cont), BLOB_STRIDE apart
     void* d_front_[1] = {nullptr};
     int* d_ready_ = nullptr;
-    void* d_best_ = nullptr;
-    long long grid_ = 0;
-    // [generic, specialised MIN, specialised FIRST]
-    size_t grid_smem_[3] = {0, 0, 0}, smem_attr_[3] = {0, 0, 0};
-    long long grid_k_[3] = {0, 0, 0};
+    void* d_best_ = nullptr;  // MAXBATCH HitPaths
+    void* h_best_ = nullptr;  // pinned mirror (seeds in, rank merge out)
+    // [generic, specialised MIN, specialised FIRST, specialised any-mode]
+    size_t smem_attr_[4] = {0, 0, 0, 0};
+    std::map<long long, long long> grid_cache_;  // (kernel, smem) -> resident CTAs
     Tuning tune_;
     unsigned long long ticket_base_ = 0;
     long long dev_bytes_ = 0;

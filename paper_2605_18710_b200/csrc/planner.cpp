@@ -234,15 +234,72 @@ std::vector<Entry> Planner::leaf_entries(const std::vector<int>& order, const Le
     return out;
 }
 
-StageResult Planner::stage_eval(uint64_t mask) {
-    StageResult res;
+bool Planner::prep_first(const std::vector<int>& order, bool filter, double theta, SearchOp& op,
+                         mg::SearchStats& st, const std::vector<Entry>* seed, double seed_value) {
+    mg::SearchReq q;
+    q.mode = MODE_FIRST;
+    q.use_filter = filter;
+    q.theta = theta;
+    q.level_module = order;
+    op.req = mg::BatchReq{};
+    if (!mg::build_spec(M_, q, op.req.S)) return false;
+    const bool seeded = seed && make_seed(*seed, order, filter, theta, seed_value, op.hp, op.sl);
+    if (seed && eng_->tuning().trace)
+        std::fprintf(stderr, "[mosaic] FIRST seed %s (theta=%.17g value=%.17g)\n",
+                     seeded ? "applied" : "rejected", theta, seed_value);
+    op.req.ub = POS_INF;
+    op.req.abort_below = 0.0;
+    op.req.seed_path = seeded ? &op.hp : nullptr;
+    op.req.seed_leaf = seeded ? &op.sl : nullptr;
+    op.req.st = &st;
+    return true;
+}
+
+// MIN request: fail-first order (fewest viable options first; any order is valid for MIN).
+bool Planner::prep_min(const std::vector<int>& mods, double ub, SearchOp& op, mg::SearchStats& st,
+                       std::vector<int>& order) {
+    const double thp = ub >= POS_INF ? POS_INF : ub * (1.0 - mg::TIE_EPS);
+    std::vector<std::pair<int, int>> cnt;
+    for (int m : mods) {
+        int c = 0;
+        for (const auto& r : M_.rows[m]) {
+            double lb = r.base;
+            if (M_.nonneg()) {
+                lb = r.base + M_.e1;
+                if (M_.include_self) lb = lb + M_.e2 * r.B;
+            }
+            if (!M_.nonneg() || lb <= thp) ++c;
+        }
+        cnt.push_back({c, m});
+    }
+    std::stable_sort(cnt.begin(), cnt.end());
+    mg::SearchReq q;
+    q.mode = MODE_MIN;
+    q.ub = ub;
+    order.clear();
+    for (auto& [c, m] : cnt) order.push_back(m);
+    q.level_module = order;
+    op.req = mg::BatchReq{};
+    if (!mg::build_spec(M_, q, op.req.S)) return false;
+    op.req.ub = ub;
+    op.req.abort_below = ub >= POS_INF ? POS_INF : ub * (1.0 - 1e-4);
+    op.req.st = &st;
+    return true;
+}
+
+// stage_eval (stage_eval.hpp:302-382) as a coroutine: the reference's tau schedule (doubling,
+// bisection, confirmation) with every FeasibilitySearch::run it would make replayed, in
+// order; each one is a device FIRST search, or is decided from T* (one MIN proof) without
+// a search.
+StageJob Planner::stage_eval_job(uint64_t mask, StageResult* out) {
+    StageResult& res = *out;
     const auto mods = mask_modules(mask);
     if ((int)mods.size() > mg::MAXK) throw Error(TOO_LARGE, "stage larger than 12 modules");
     for (int m : mods) {
         check_rows(m);
         if (opts_[m].empty()) {
             res.status = MODULE_NO_OPTION;
-            return res;
+            co_return;
         }
     }
     const Interference& im = P_.im;
@@ -268,57 +325,86 @@ StageResult Planner::stage_eval(uint64_t mask) {
     double Tstar = POS_INF;
     std::vector<Entry> argmin;  // an allocation reaching Tstar
     long long probes = 0;
-    // FeasibilitySearch::run(tau) replayed: first leaf in fail-first DFS order.
-    auto run_probe = [&](double tau, Leaf& leaf, std::vector<int>& order) -> bool {
-        ++probes;
-        const double th = tau * (1.0 + 1e-12);
-        std::vector<std::pair<int, int>> cnt;
-        for (int m : mods) {
-            int c = 0;
-            for (const auto& r : M_.rows[m])
-                if (r.bound <= th) ++c;
-            if (c == 0) return false;
-            cnt.push_back({c, m});
-        }
-        // T* lies in [Tstar*(1 - TIE_EPS - rounding), Tstar]: below that band no leaf can
-        // reach tau; inside it the probe is decided by an exact FIRST search.
-        if (nonneg && have_T && th < Tstar * (1.0 - 1e-13)) return false;
-        std::stable_sort(cnt.begin(), cnt.end());
-        order.clear();
-        for (auto& [c, m] : cnt) order.push_back(m);
-        // seed with the argmin allocation when it is known to satisfy this probe
-        const bool seed = nonneg && have_T && !argmin.empty() && Tstar <= th;
-        return first_leaf(order, true, th, leaf, res.st, seed ? &argmin : nullptr, Tstar);
-    };
-    auto run = [&](double tau, Leaf& leaf, std::vector<int>& order) -> bool {
-        const bool ok = run_probe(tau, leaf, order);
-        res.probe_tau.push_back(tau);
-        res.probe_ok.push_back(ok ? 1 : 0);
-        return ok;
-    };
+    SearchOp op;
+    // FeasibilitySearch::run(tau) replayed: the first leaf in fail-first DFS order.
+    // T* lies in [Tstar*(1 - TIE_EPS - rounding), Tstar]: below that band no leaf reaches
+    // tau; inside it the probe is decided by an exact FIRST search, seeded with the argmin.
+#define MG_RUN_PROBE(TAU, LEAF, ORDER, OK)                                                  \
+    do {                                                                                   \
+        const double tau_ = (TAU);                                                         \
+        ++probes;                                                                          \
+        bool ok_ = false;                                                                  \
+        const double th_ = tau_ * (1.0 + 1e-12);                                           \
+        std::vector<std::pair<int, int>> cnt_;                                             \
+        bool none_ = false;                                                                \
+        for (int m_ : mods) {                                                              \
+            int c_ = 0;                                                                    \
+            for (const auto& r_ : M_.rows[m_])                                             \
+                if (r_.bound <= th_) ++c_;                                                 \
+            if (c_ == 0) none_ = true;                                                     \
+            cnt_.push_back({c_, m_});                                                      \
+        }                                                                                  \
+        if (!none_ && !(nonneg && have_T && th_ < Tstar * (1.0 - 1e-13))) {                \
+            std::stable_sort(cnt_.begin(), cnt_.end());                                    \
+            ORDER.clear();                                                                 \
+            for (auto& [c_, m_] : cnt_) ORDER.push_back(m_);                               \
+            const bool seed_ = nonneg && have_T && !argmin.empty() && Tstar <= th_;        \
+            if (prep_first(ORDER, true, th_, op, res.st, seed_ ? &argmin : nullptr, Tstar)) { \
+                const mg::SearchResult sr_ = co_await SearchAwait{&op};                    \
+                if (sr_.overflow) throw Error(TOO_LARGE, "stage needs more than 128 GPU blocks"); \
+                if (sr_.found) {                                                           \
+                    LEAF = sr_.leaf;                                                       \
+                    ok_ = true;                                                            \
+                }                                                                          \
+            }                                                                              \
+        }                                                                                  \
+        res.probe_tau.push_back(tau_);                                                     \
+        res.probe_ok.push_back(ok_ ? 1 : 0);                                               \
+        OK = ok_;                                                                          \
+    } while (0)
     Leaf best, cur;
     std::vector<int> best_order, cur_order;
-    bool ok = run(tau_hi, best, best_order);
+    bool ok = false;
+    MG_RUN_PROBE(tau_hi, best, best_order, ok);
     for (int attempt = 0; !ok && attempt < 60; ++attempt) {
         tau_hi *= 2.0;
-        ok = run(tau_hi, best, best_order);
+        MG_RUN_PROBE(tau_hi, best, best_order, ok);
     }
     res.probes = probes;
     if (!ok) {
         res.status = INFEASIBLE;
-        return res;
+        co_return;
     }
     double t_best = best.value;
     if (nonneg) {
+        // T*: one MIN proof below the first leaf's value, restarted with re-derived static
+        // bounds whenever the incumbent drops by more than 1e-4
         argmin = leaf_entries(best_order, best);
-        Tstar = min_value(mods, t_best, res.st, &argmin);
+        double ub = t_best;
+        std::vector<int> morder;
+        while (true) {
+            if (!prep_min(mods, ub, op, res.st, morder)) {
+                Tstar = ub;
+                break;
+            }
+            const mg::SearchResult r = co_await SearchAwait{&op};
+            if (r.overflow) throw Error(TOO_LARGE, "stage needs more than 128 GPU blocks");
+            if (r.found && r.leaf.nb > 0) argmin = leaf_entries(morder, r.leaf);
+            if (r.aborted) {
+                ub = r.value;
+                continue;
+            }
+            Tstar = r.value;
+            break;
+        }
         have_T = true;
     }
     double lo = std::min(tau_lo, t_best);
     while (t_best - lo > P_.bisect_rel_tol * std::abs(t_best)) {
         double mid = 0.5 * (lo + t_best);
         if (mid >= t_best * (1.0 - 1e-12)) break;
-        if (run(mid, cur, cur_order)) {
+        MG_RUN_PROBE(mid, cur, cur_order, ok);
+        if (ok) {
             best = cur;
             best_order = cur_order;
             t_best = best.value;
@@ -329,17 +415,115 @@ StageResult Planner::stage_eval(uint64_t mask) {
     for (int guard = 0; guard < 1000; ++guard) {
         double probe = t_best * (1.0 - 1e-9);
         if (probe <= lo) break;
-        if (!run(probe, cur, cur_order)) break;
+        MG_RUN_PROBE(probe, cur, cur_order, ok);
+        if (!ok) break;
         best = cur;
         best_order = cur_order;
         t_best = best.value;
     }
+#undef MG_RUN_PROBE
     res.status = OK;
     res.stage_time = t_best;
     res.entries = leaf_entries(best_order, best);
     res.probes = probes;
-    return res;
 }
+
+// ExactStageSolver::solve (oracle.hpp:86-103) as a coroutine: FIRST(inf) for an incumbent,
+// MIN for I*, then the tie band resolved exactly — FIRST(theta) yields a leaf of value
+// v <= theta; lower theta below v until no leaf remains: then v == T* and the last leaf is
+// the first argmin in module-index DFS order (the reference's strict '<', oracle.hpp:120).
+StageJob Planner::exact_stage_job(uint64_t mask, StageResult* out) {
+    StageResult& res = *out;
+    const auto mods = mask_modules(mask);
+    if ((int)mods.size() > mg::MAXK) throw Error(TOO_LARGE, "stage larger than 12 modules");
+    for (int m : mods) {
+        check_rows(m);
+        if (opts_[m].empty()) {
+            res.status = INFEASIBLE;  // ExactStageSolver returns nullopt (oracle.hpp:91-92)
+            co_return;
+        }
+    }
+    SearchOp op;
+    if (!prep_first(mods, false, POS_INF, op, res.st)) {
+        res.status = INFEASIBLE;
+        co_return;
+    }
+    mg::SearchResult r = co_await SearchAwait{&op};
+    if (r.overflow) throw Error(TOO_LARGE, "stage needs more than 128 GPU blocks");
+    if (!r.found) {
+        res.status = INFEASIBLE;
+        co_return;
+    }
+    double T = r.leaf.value;
+    std::vector<int> morder;
+    while (true) {
+        if (!prep_min(mods, T, op, res.st, morder)) break;
+        r = co_await SearchAwait{&op};
+        if (r.overflow) throw Error(TOO_LARGE, "stage needs more than 128 GPU blocks");
+        if (r.aborted) {
+            T = r.value;
+            continue;
+        }
+        T = r.value;
+        break;
+    }
+    if (!prep_first(mods, false, T, op, res.st)) throw Error(CUDA, "exact search lost the argmin leaf");
+    r = co_await SearchAwait{&op};
+    if (r.overflow) throw Error(TOO_LARGE, "stage needs more than 128 GPU blocks");
+    if (!r.found) throw Error(CUDA, "exact search lost the argmin leaf");
+    Leaf lf = r.leaf;
+    for (int guard = 0; guard < 64; ++guard) {
+        const double below = std::nextafter(lf.value, -POS_INF);
+        if (!prep_first(mods, false, below, op, res.st)) break;
+        r = co_await SearchAwait{&op};
+        if (r.overflow) throw Error(TOO_LARGE, "stage needs more than 128 GPU blocks");
+        if (!r.found) break;
+        lf = r.leaf;
+    }
+    res.status = OK;
+    res.stage_time = lf.value;
+    res.entries = leaf_entries(mods, lf);
+}
+
+// Advance every job to its next device search; run each wave of pending searches as one
+// batched launch; repeat until all jobs are done.  The first exception is rethrown.
+void Planner::run_jobs(std::vector<StageJob>& jobs) {
+    for (auto& j : jobs) j.h.resume();
+    std::vector<mg::BatchReq> reqs;
+    std::vector<StageJob*> who;
+    while (true) {
+        reqs.clear();
+        who.clear();
+        for (auto& j : jobs)
+            if (!j.h.done() && j.h.promise().op) {
+                reqs.push_back(j.h.promise().op->req);
+                who.push_back(&j);
+            }
+        if (reqs.empty()) break;
+        std::vector<mg::SearchResult> res = eng_->search_batch(reqs);
+        for (size_t i = 0; i < who.size(); ++i) {
+            auto& pr = who[i]->h.promise();
+            pr.op->res = res[i];
+            pr.op = nullptr;
+            who[i]->h.resume();
+        }
+    }
+    for (auto& j : jobs)
+        if (j.h.promise().exc) std::rethrow_exception(j.h.promise().exc);
+}
+
+std::vector<StageResult> Planner::stage_batch(const std::vector<uint64_t>& masks, bool exact) {
+    std::vector<StageResult> out(masks.size());
+    std::vector<StageJob> jobs;
+    jobs.reserve(masks.size());
+    for (size_t i = 0; i < masks.size(); ++i)
+        jobs.push_back(exact ? exact_stage_job(masks[i], &out[i])
+                             : stage_eval_job(masks[i], &out[i]));
+    run_jobs(jobs);
+    return out;
+}
+
+StageResult Planner::stage_eval(uint64_t mask) { return std::move(stage_batch({mask}, false)[0]); }
 
 // core.hpp:281-351: partition coverage, dependency order, per-GPU quota sum <= 1 + 1e-9,
 // per-GPU memory <= capacity * (1 + 1e-12) with footprint = lookup(d, a).memory + base.
@@ -450,41 +634,7 @@ StageResult Planner::feasible(uint64_t mask, double tau) {
     return res;
 }
 
-StageResult Planner::exact_stage(uint64_t mask) {
-    StageResult res;
-    const auto mods = mask_modules(mask);
-    if ((int)mods.size() > mg::MAXK) throw Error(TOO_LARGE, "stage larger than 12 modules");
-    for (int m : mods) {
-        check_rows(m);
-        if (opts_[m].empty()) {
-            res.status = INFEASIBLE;  // ExactStageSolver returns nullopt (oracle.hpp:91-92)
-            return res;
-        }
-    }
-    Leaf first;
-    if (!first_leaf(mods, false, POS_INF, first, res.st)) {
-        res.status = INFEASIBLE;
-        return res;
-    }
-    // MIN returns I* with T* in [I*(1 - TIE_EPS - rounding), I*].  Resolve the band
-    // exactly: FIRST(theta) yields a leaf of value v <= theta; keep lowering theta below v
-    // until no leaf remains — then v == T* and the last FIRST(T*) leaf is the first argmin
-    // in module-index DFS order, i.e. ExactStageSolver's strict-'<' result (oracle.hpp:120).
-    double T = min_value(mods, first.value, res.st);
-    Leaf lf;
-    if (!first_leaf(mods, false, T, lf, res.st))
-        throw Error(CUDA, "exact search lost the argmin leaf");
-    for (int guard = 0; guard < 64; ++guard) {
-        Leaf lower;
-        const double below = std::nextafter(lf.value, -POS_INF);
-        if (!first_leaf(mods, false, below, lower, res.st)) break;
-        lf = lower;
-    }
-    res.status = OK;
-    res.stage_time = lf.value;
-    res.entries = leaf_entries(mods, lf);
-    return res;
-}
+StageResult Planner::exact_stage(uint64_t mask) { return std::move(stage_batch({mask}, true)[0]); }
 
 std::optional<StageResult> Planner::evaluate_cached(uint64_t mask, bool* hit, PlanResult& pr) {
     if (P_.enable_cache) {
@@ -497,11 +647,17 @@ std::optional<StageResult> Planner::evaluate_cached(uint64_t mask, bool* hit, Pl
     }
     if (hit) *hit = false;
     pr.stage_eval_calls++;
-    StageResult r = stage_eval(mask);
-    pr.st.nodes += r.st.nodes;
-    pr.st.leaves += r.st.leaves;
-    pr.st.searches += r.st.searches;
-    pr.st.rounds += r.st.rounds;
+    StageResult r;
+    auto sp = spec_.find(mask);
+    if (sp != spec_.end()) {
+        r = sp->second;  // computed ahead in this round's batch (deterministic: same result)
+    } else {
+        r = stage_eval(mask);
+        pr.st.nodes += r.st.nodes;
+        pr.st.leaves += r.st.leaves;
+        pr.st.searches += r.st.searches;
+        pr.st.rounds += r.st.rounds;
+    }
     if (r.status == MODULE_NO_OPTION)
         throw Error(MODULE_NO_OPTION, "module has no feasible deployment option");
     if (r.status != OK) return std::nullopt;
@@ -510,15 +666,41 @@ std::optional<StageResult> Planner::evaluate_cached(uint64_t mask, bool* hit, Pl
     return r;
 }
 
+// Evaluate `masks` (not cached, not yet computed) as one batch ahead of the reference's
+// sequential candidate loop; the loop then consumes the results in its own order.
+void Planner::speculate(const std::vector<uint64_t>& masks, PlanResult& pr) {
+    std::vector<uint64_t> todo;
+    for (uint64_t m : masks)
+        if ((!P_.enable_cache || !cache_.count(m)) && !spec_.count(m) &&
+            std::find(todo.begin(), todo.end(), m) == todo.end())
+            todo.push_back(m);
+    if (todo.empty()) return;
+    std::vector<StageResult> rs = stage_batch(todo, false);
+    for (size_t i = 0; i < todo.size(); ++i) {
+        pr.st.nodes += rs[i].st.nodes;
+        pr.st.leaves += rs[i].st.leaves;
+        pr.st.searches += rs[i].st.searches;
+        pr.st.rounds += rs[i].st.rounds;
+        spec_.emplace(todo[i], std::move(rs[i]));
+    }
+}
+
 PlanResult Planner::solve() {
     const double t0 = now_s();
     PlanResult pr;
     const int n = (int)P_.modules.size();
     if (n == 0) throw Error(EMPTY, "model graph has no modules");
     clear_cache();
+    spec_.clear();
     auto reach = reachability_masks(P_);
     std::vector<uint64_t> masks;
     std::vector<StageResult> results;
+    {
+        // round 0: every singleton in one batch
+        std::vector<uint64_t> singles;
+        for (int m : topological_order(P_)) singles.push_back(uint64_t(1) << m);
+        speculate(singles, pr);
+    }
     for (int m : topological_order(P_)) {
         uint64_t mask = uint64_t(1) << m;
         auto r = evaluate_cached(mask, nullptr, pr);
@@ -557,6 +739,23 @@ PlanResult Planner::solve() {
         std::sort(pairs.begin(), pairs.end(), [&](const auto& a, const auto& b) {
             return order_lt(masks[a.first], masks[a.second], masks[b.first], masks[b.second]);
         });
+        {
+            // A1: every candidate the reference may evaluate this round, in one batch.  A
+            // candidate with t_x + t_y - t_lb <= 0 is pruned whatever delta_best becomes (it
+            // only grows from 0); large module sets are left to the sequential loop, which
+            // skips the ones the reference prunes.
+            std::vector<uint64_t> cands;
+            for (auto [x, y] : pairs) {
+                const uint64_t mm = masks[x] | masks[y];
+                if (P_.enable_prune) {
+                    double t_lb = 0.0;
+                    for (int m : mask_modules(mm)) t_lb = std::max(t_lb, min_base[m]);
+                    if (results[x].stage_time + results[y].stage_time - t_lb <= 0.0) continue;
+                }
+                if (std::popcount(mm) <= eng_->tuning().spec_k) cands.push_back(mm);
+            }
+            speculate(cands, pr);
+        }
         double delta_best = 0.0;
         int best_idx = -1;
         StageResult best_merged;
@@ -607,6 +806,7 @@ PlanResult Planner::solve() {
         pr.stages.push_back(results[i]);
         pr.iteration_time += results[i].stage_time;
     }
+    spec_.clear();
     pr.status = OK;
     pr.elapsed = now_s() - t0;
     return pr;

@@ -11,7 +11,9 @@
 // the reference's control flow (which tau to probe next, which merge to apply) and
 // converts winning leaves back into StageAllocations.
 #pragma once
+#include <coroutine>
 #include <cstdint>
+#include <exception>
 #include <memory>
 #include <optional>
 #include <string>
@@ -74,6 +76,52 @@ struct PlanResult {
     double elapsed = 0.0;
 };
 
+// A stage computation (stage_eval / exact_stage) written as a coroutine that suspends at
+// every device search it needs: many of them advance together and each wave of their
+// searches is one batched launch (Planner::run_jobs, Engine::search_batch).
+struct SearchOp {
+    mg::BatchReq req;
+    mg::HitPath hp;  // seed storage (req.seed_path / seed_leaf point here)
+    mg::Leaf sl;
+    mg::SearchResult res;
+};
+
+struct StageJob {
+    struct promise_type {
+        SearchOp* op = nullptr;  // the search this job waits for (null: running or done)
+        std::exception_ptr exc;
+        StageJob get_return_object() {
+            return StageJob{std::coroutine_handle<promise_type>::from_promise(*this)};
+        }
+        std::suspend_always initial_suspend() noexcept { return {}; }
+        std::suspend_always final_suspend() noexcept { return {}; }
+        void return_void() noexcept {}
+        void unhandled_exception() noexcept { exc = std::current_exception(); }
+    };
+    std::coroutine_handle<promise_type> h;
+    explicit StageJob(std::coroutine_handle<promise_type> x = {}) : h(x) {}
+    StageJob(StageJob&& o) noexcept : h(o.h) { o.h = {}; }
+    StageJob& operator=(StageJob&& o) noexcept {
+        if (h) h.destroy();
+        h = o.h;
+        o.h = {};
+        return *this;
+    }
+    StageJob(const StageJob&) = delete;
+    ~StageJob() {
+        if (h) h.destroy();
+    }
+};
+
+struct SearchAwait {
+    SearchOp* op;
+    bool await_ready() const noexcept { return false; }
+    void await_suspend(std::coroutine_handle<StageJob::promise_type> h) const noexcept {
+        h.promise().op = op;
+    }
+    mg::SearchResult await_resume() const noexcept { return op->res; }
+};
+
 class Planner {
   public:
     Planner(Problem P, int device);
@@ -82,6 +130,9 @@ class Planner {
 
     StageResult stage_eval(uint64_t mask);
     StageResult exact_stage(uint64_t mask);
+    // Batched (mosaic_gpu_search): the module sets' computations advance together, one launch
+    // per wave of device searches.  exact = ExactStageSolver semantics, else stage_eval.
+    std::vector<StageResult> stage_batch(const std::vector<uint64_t>& masks, bool exact);
     StageResult feasible(uint64_t mask, double tau);
     PlanResult solve();
     // validate_plan (core.hpp:281-351) with the footprint oracle; "" when valid, else the
@@ -123,6 +174,15 @@ class Planner {
   private:
     void check_rows(int m) const;
     bool ensure_rate_tables();  // false when they would not fit (then the row path is used)
+    StageJob stage_eval_job(uint64_t mask, StageResult* out);
+    StageJob exact_stage_job(uint64_t mask, StageResult* out);
+    void run_jobs(std::vector<StageJob>& jobs);
+    // FIRST probe request (false: some level has no usable option, no leaf can exist)
+    bool prep_first(const std::vector<int>& order, bool filter, double theta, SearchOp& op,
+                    mg::SearchStats& st, const std::vector<Entry>* seed = nullptr,
+                    double seed_value = 0.0);
+    bool prep_min(const std::vector<int>& mods, double ub, SearchOp& op, mg::SearchStats& st,
+                  std::vector<int>& order);
     bool first_leaf(const std::vector<int>& order, bool filter, double theta, mg::Leaf& leaf,
                     mg::SearchStats& st, const std::vector<Entry>* seed = nullptr,
                     double seed_value = 0.0);
@@ -135,6 +195,7 @@ class Planner {
                    double theta, double value, mg::HitPath& hp, mg::Leaf& lf) const;
     std::vector<Entry> leaf_entries(const std::vector<int>& order, const mg::Leaf& lf) const;
     std::optional<StageResult> evaluate_cached(uint64_t mask, bool* hit, PlanResult& pr);
+    void speculate(const std::vector<uint64_t>& masks, PlanResult& pr);
 
     Problem P_;
     mg::Model M_;
@@ -144,6 +205,9 @@ class Planner {
     std::unordered_map<uint64_t, StageResult> cache_;
     std::vector<uint64_t> cache_order_;
     int rate_tables_ = 0;  // 0 not built yet, 1 built, -1 too large for this problem
+    // stage_eval results computed speculatively for GAHC candidates the reference prunes
+    // (not in the EvalCache; moved there when the reference would evaluate them)
+    std::unordered_map<uint64_t, StageResult> spec_;
 };
 
 }  // namespace mosaic_b200

@@ -202,7 +202,26 @@ struct WarpHooks {
 
 constexpr int WPC = 4;  // walkers (warps) per CTA
 
+// A launch runs up to MAXBATCH independent searches (one per module set of a GAHC round /
+// probe wave): search s owns CTAs [cta_off[s], cta_off[s+1]), its own Spec, control block,
+// hit path, leaf, root piece and a private slice of the cursor ring at q_off[s].
+constexpr int MAXBATCH = 64;
+struct BatchMap {
+    int n;
+    int cta_off[MAXBATCH + 1];
+    long long q_off[MAXBATCH];
+};
+
 constexpr size_t SMEM_SPEC = (sizeof(Spec) + 15) & ~size_t(15);
+
+// Per-search staging blob (host pinned and device mirror): Spec | Ctl | Leaf | root Cont,
+// each 256-B aligned; searches of a batch are BLOB_STRIDE apart.
+constexpr size_t blob_align(size_t x) { return (x + 255) & ~size_t(255); }
+constexpr size_t BLOB_SPEC = 0;
+constexpr size_t BLOB_CTL = BLOB_SPEC + blob_align(sizeof(Spec));
+constexpr size_t BLOB_LEAF = BLOB_CTL + blob_align(sizeof(Ctl));
+constexpr size_t BLOB_ROOT = BLOB_LEAF + blob_align(sizeof(Leaf));
+constexpr size_t BLOB_STRIDE = BLOB_ROOT + blob_align(sizeof(Cont));
 
 // dynamic shared memory of one CTA for a stage of k modules over G GPUs
 static inline size_t smem_bytes(int G, int k, bool lean) {
@@ -218,10 +237,27 @@ static inline size_t smem_bytes(int G, int k, bool lean) {
 //          seqlock, and work that lies after it is abandoned.
 __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NAME(const Spec* Sg, Rows R, Cont* Q, int* ready,
                                                      Ctl* ctl, HitPath* best, Leaf* leaf_out,
-                                                     const Cont* root, long long slot0,
+                                                     const Cont* root, const BatchMap map,
                                                      int ready0) {
-    (void)slot0;
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int sid_sh;
+    if (threadIdx.x == 0) {
+        int s = 0;
+        while (s + 1 < map.n && (int)blockIdx.x >= map.cta_off[s + 1]) ++s;
+        sid_sh = s;
+    }
+    __syncthreads();
+    {
+        // this CTA's search: its slice of every per-search array (blob stride = BLOB_STRIDE)
+        const int sid = sid_sh;
+        Sg = reinterpret_cast<const Spec*>(reinterpret_cast<const char*>(Sg) + sid * BLOB_STRIDE);
+        ctl = reinterpret_cast<Ctl*>(reinterpret_cast<char*>(ctl) + sid * BLOB_STRIDE);
+        leaf_out = reinterpret_cast<Leaf*>(reinterpret_cast<char*>(leaf_out) + sid * BLOB_STRIDE);
+        root = reinterpret_cast<const Cont*>(reinterpret_cast<const char*>(root) + sid * BLOB_STRIDE);
+        best += sid;
+        Q += map.q_off[sid];
+        ready += map.q_off[sid];
+    }
     Spec& S = *reinterpret_cast<Spec*>(smem);
     {
         const int n = sizeof(Spec) / 4;

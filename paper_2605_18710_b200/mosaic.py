@@ -154,7 +154,8 @@ EXPORTS = [
     "mosaic_gpu_feasible", "mosaic_gpu_plan_stage", "mosaic_gpu_solve",
     "mosaic_gpu_brute_force", "mosaic_gpu_trace_rounds", "mosaic_gpu_trace_round",
     "mosaic_gpu_trace_cand", "mosaic_gpu_clear_cache", "mosaic_gpu_set_shard",
-    "mosaic_gpu_merge_records", "mosaic_gpu_launch_count", "mosaic_gpu_search_ms",
+    "mosaic_gpu_rank_record_size", "mosaic_gpu_rank_record", "mosaic_gpu_merge_ranks",
+    "mosaic_gpu_search", "mosaic_gpu_launch_count", "mosaic_gpu_search_ms",
     "mosaic_gpu_reset_counters", "mosaic_gpu_synth_problem", "mosaic_gpu_free_problem",
     "mosaic_gpu_own_launches", "mosaic_gpu_ksearch_ms", "mosaic_gpu_ksearch_launches",
     "mosaic_gpu_h2d_bytes", "mosaic_gpu_d2h_bytes", "mosaic_gpu_mark", "mosaic_gpu_marked_ms", "mosaic_gpu_alg_bytes", "mosaic_gpu_stage_min",
@@ -201,7 +202,15 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                             P(C.c_double)]),
         "mosaic_gpu_clear_cache": (None, [vp]),
         "mosaic_gpu_set_shard": (C.c_int, [vp, C.c_int, C.c_int, ALLGATHER_FN, vp]),
-        "mosaic_gpu_merge_records": (C.c_int, [vp, C.c_int, C.c_int, P(C.c_int)]),
+        "mosaic_gpu_rank_record_size": (C.c_size_t, []),
+        "mosaic_gpu_rank_record": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                             P(C.c_uint16), P(C.c_uint16), P(C.c_uint16),
+                                             C.c_double]),
+        "mosaic_gpu_merge_ranks": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, P(C.c_int),
+                                             P(C.c_int), P(C.c_double), P(C.c_int), P(C.c_int),
+                                             P(C.c_double)]),
+        "mosaic_gpu_search": (C.c_int, [vp, P(C.c_uint64), C.c_int64, C.c_int,
+                                        P(StageResultC)]),
         "mosaic_gpu_launch_count": (C.c_int64, [vp]),
         "mosaic_gpu_search_ms": (C.c_double, [vp]),
         "mosaic_gpu_reset_counters": (None, [vp]),
@@ -476,6 +485,22 @@ class Planner:
         if r.status == MODULE_NO_OPTION:
             raise StageInfeasibleError("module has no feasible deployment option")
         return self._stage(r) if r.status == OK else None
+
+    def search(self, module_sets: Sequence[Sequence[int]], exact: bool = False
+               ) -> list[Optional[StageEvalResult]]:
+        """Batched stage_eval (or ExactStageSolver::solve with exact=True) of many module sets
+        (mosaic_gpu_search): the computations advance together, one launch per wave."""
+        n = len(module_sets)
+        masks = (C.c_uint64 * max(1, n))(*[self._mask(m) for m in module_sets])
+        out = (StageResultC * max(1, n))()
+        _raise(load_library().mosaic_gpu_search(self._ctx, masks, n, 1 if exact else 0, out))
+        res = []
+        for i in range(n):
+            r = out[i]
+            if r.status == MODULE_NO_OPTION and not exact:
+                raise StageInfeasibleError("module has no feasible deployment option")
+            res.append(self._stage(r) if r.status == OK else None)
+        return res
 
     def exact_stage(self, modules: Sequence[int]) -> Optional[StageEvalResult]:
         r = StageResultC()
@@ -780,12 +805,38 @@ def candidate_options(planner: Planner, module: int) -> list[CandidateOption]:
     return planner.candidate_options(module)
 
 
-def merge_records(records: bytes, world: int, mode: int) -> int:
-    """Winner index among per-rank 16-byte {u64 key, f64 value} records."""
-    w = C.c_int()
+MAXB = 128  # GPU blocks per search level (search_core.cuh)
+
+
+def rank_record(has_hit: bool, inc: float, path=(), aborted: bool = False,
+                overflow: bool = False, leaf_value: float = 0.0) -> bytes:
+    """One rank's RankRecord of a sharded search (Engine::merge_ranks): path = [(option,
+    [block counts...]) per level] of its FIRST hit / argmin leaf."""
+    L = load_library()
+    buf = C.create_string_buffer(L.mosaic_gpu_rank_record_size())
+    k = len(path)
+    opt = (C.c_uint16 * max(1, k))(*[o for o, _ in path])
+    nb = (C.c_uint16 * max(1, k))(*[len(x) for _, x in path])
+    x = (C.c_uint16 * (max(1, k) * MAXB))()
+    for l, (_, xs) in enumerate(path):
+        for b, v in enumerate(xs):
+            x[l * MAXB + b] = v
+    _raise(L.mosaic_gpu_rank_record(buf, int(has_hit), int(aborted), int(overflow), inc, k,
+                                    opt, nb, x, leaf_value))
+    return buf.raw
+
+
+def merge_ranks(records: bytes, world: int, mode: int, k: int) -> dict:
+    """The engine's merge of one sharded search over `world` concatenated RankRecords:
+    mode 0 MIN, 1 FIRST (include/mosaic_gpu.h, mosaic_gpu_merge_ranks)."""
+    w, f, a, o = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    v, lv = C.c_double(), C.c_double()
     buf = C.create_string_buffer(records, len(records))
-    _raise(load_library().mosaic_gpu_merge_records(buf, world, mode, C.byref(w)))
-    return w.value
+    _raise(load_library().mosaic_gpu_merge_ranks(buf, world, mode, k, C.byref(w), C.byref(f),
+                                                 C.byref(v), C.byref(a), C.byref(o),
+                                                 C.byref(lv)))
+    return {"winner": w.value, "found": bool(f.value), "value": v.value,
+            "aborted": bool(a.value), "overflow": bool(o.value), "leaf_value": lv.value}
 
 
 # ---------------------------------------------------------------------------

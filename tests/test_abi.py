@@ -67,8 +67,19 @@ def test_create_without_gpu_fails_loudly():
         mosaic.Planner.from_spec("cfg1")
 
 
-def test_merge_records():
-    import struct
-    recs = b"".join(struct.pack("<Qd", k, v) for k, v in [(5, 0.3), (2, 0.5), (9, 0.3)])
-    assert mosaic.merge_records(recs, 3, 0) == 0  # MIN: smallest value, then key
-    assert mosaic.merge_records(recs, 3, 1) == 1  # FIRST: smallest key
+def test_merge_ranks_rules():
+    # MIN: smallest incumbent, lowest rank on ties; a restart on any rank restarts all
+    recs = b"".join(mosaic.rank_record(True, v, [(1, [2])], aborted=(i == 2), leaf_value=v)
+                    for i, v in enumerate([0.3, 0.5, 0.3]))
+    m = mosaic.merge_ranks(recs, 3, 0, 1)
+    assert (m["winner"], m["value"], m["aborted"], m["leaf_value"]) == (0, 0.3, True, 0.3)
+    # FIRST: the hit earliest in reference DFS order — smaller option first, then the larger
+    # take count of the first differing block; ranks without a hit never win
+    recs = b"".join([mosaic.rank_record(True, 0.0, [(2, [4]), (0, [1, 3])], leaf_value=1.0),
+                     mosaic.rank_record(False, 0.0),
+                     mosaic.rank_record(True, 0.0, [(2, [4]), (0, [2, 0])], leaf_value=2.0),
+                     mosaic.rank_record(True, 0.0, [(3, [4]), (0, [4, 0])], leaf_value=3.0)])
+    f = mosaic.merge_ranks(recs, 4, 1, 2)
+    assert (f["winner"], f["found"], f["leaf_value"]) == (2, True, 2.0)
+    none = b"".join(mosaic.rank_record(False, 0.0) for _ in range(2))
+    assert mosaic.merge_ranks(none, 2, 1, 1)["found"] is False
