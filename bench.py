@@ -356,10 +356,10 @@ def main() -> None:
             return
         # one batched stage search (mosaic_gpu_search): the stage_evals advance together,
         # one launch per wave of their device searches
-        rs = pl.search([mask_bits(m["mask"]) for m in mine])
-        for m, r in zip(mine, rs):
+        ts = pl.search([mask_bits(m["mask"]) for m in mine], times_only=True)
+        for m, t in zip(mine, ts):
             # identical work: every stage time equals the reference's, bit for bit
-            assert r is not None and r.stage_time == want[m["mask"]], (m["mask"], r)
+            assert t == want[m["mask"]], (m["mask"], t)
 
     # ---- device-resident: tables already in HBM, time the sample ----
     pl = mosaic.Planner.from_spec(WORKLOAD, device=local)

@@ -161,11 +161,13 @@ int mosaic_gpu_evaluate_stats(mosaic_gpu_ctx* ctx, double* kernel_ms, int64_t* l
  * out[i] = stage_eval (MOSAIC_SEARCH_STAGE_EVAL) or ExactStageSolver::solve
  * (MOSAIC_SEARCH_EXACT) of module set masks[i].  The n computations advance together;
  * every wave of their device searches (tau probes, MIN proofs) is ONE batched launch in
- * which each search owns a slice of the resident grid.  Per-mask status in out[i].status. */
+ * which each search owns a slice of the resident grid.  Each of out (full results),
+ * stage_time_out and status_out (per-mask MOSAIC_OK / _INFEASIBLE / _MODULE_NO_OPTION) may be
+ * NULL. */
 #define MOSAIC_SEARCH_STAGE_EVAL 0
 #define MOSAIC_SEARCH_EXACT 1
 int mosaic_gpu_search(mosaic_gpu_ctx* ctx, const uint64_t* masks, int64_t n, int mode,
-                      mosaic_gpu_stage_result* out);
+                      mosaic_gpu_stage_result* out, double* stage_time_out, int32_t* status_out);
 
 /* stage_eval / ExactStageSolver::solve / FeasibilitySearch::run for one module set. */
 int mosaic_gpu_stage_eval(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_result* out);
@@ -282,7 +284,8 @@ int mosaic_gpu_merge_ranks(const void* records, int world, int mode, int k, int*
 /* Search-engine knobs for experiments (tools/tune.py); defaults are the measured best and
  * nothing reads the environment.  Keys: don_depth, don_period (power of two), backoff_ns,
  * small_tree, deep_after, lookahead, small_grid, generic_kernel, shard_level,
- * ring_per_walker, trace, spec_k (GAHC candidates up to this many modules are batched), and the measurement-only share_rank / share_world (search one
+ * ring_per_walker, trace, spec_k (GAHC candidates up to this many modules are batched),
+ * restart_k (MIN proofs of stages with at least this many modules restart on a big drop), and the measurement-only share_rank / share_world (search one
  * rank's share of a sharded search on this device, unmerged: NOT the stage's answer).
  * MOSAIC_INVALID_ARGUMENT for an unknown key. */
 int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value);

@@ -249,14 +249,18 @@ int mosaic_gpu_stage_eval(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_r
 }
 
 int mosaic_gpu_search(mosaic_gpu_ctx* ctx, const uint64_t* masks, int64_t n, int mode,
-                      mosaic_gpu_stage_result* out) {
+                      mosaic_gpu_stage_result* out, double* stage_time_out, int32_t* status_out) {
     return guard([&] {
-        if (!ctx || (n > 0 && (!masks || !out))) throw Error(MOSAIC_RANGE, "null argument");
+        if (!ctx || (n > 0 && !masks)) throw Error(MOSAIC_RANGE, "null argument");
         if (mode != MOSAIC_SEARCH_STAGE_EVAL && mode != MOSAIC_SEARCH_EXACT)
             throw Error(MOSAIC_INVALID_ARGUMENT, "mode must be MOSAIC_SEARCH_STAGE_EVAL or _EXACT");
         std::vector<uint64_t> ms(masks, masks + n);
         std::vector<StageResult> rs = ctx->pl->stage_batch(ms, mode == MOSAIC_SEARCH_EXACT);
-        for (int64_t i = 0; i < n; ++i) fill_stage(rs[i], out + i);
+        for (int64_t i = 0; i < n; ++i) {
+            if (out) fill_stage(rs[i], out + i);
+            if (stage_time_out) stage_time_out[i] = rs[i].status == OK ? rs[i].stage_time : 0.0;
+            if (status_out) status_out[i] = rs[i].status;
+        }
         return MOSAIC_OK;
     });
 }
@@ -477,6 +481,7 @@ int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value) {
         else if (k == "ring_per_walker") t.ring_per_walker = (int)std::max(1LL, v);
         else if (k == "trace") t.trace = v != 0;
         else if (k == "spec_k") t.spec_k = (int)v;
+        else if (k == "restart_k") t.restart_k = (int)v;
         else if (k == "share_rank") t.share_rank = (int)v;
         else if (k == "share_world") t.share_world = (int)std::max(1LL, v);
         else throw Error(MOSAIC_INVALID_ARGUMENT, "unknown tuning key " + k);

@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -118,36 +119,72 @@ __global__ void __launch_bounds__(32 * EVAL_WARPS)
 // ---------------------------------------------------------------------------
 static inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Per-device pool of the engine's launch resources (stream, events, staging blobs, cursor
+// ring): contexts come and go (one per problem), the resources stay, so creating a context
+// costs no cudaMalloc / cudaMallocHost / ring clearing after the first one on a device.
+struct EngineRes {
+    int device = -1;
+    void *stream = nullptr, *ev[6] = {};
+    void *d_blob = nullptr, *h_pin = nullptr, *d_best = nullptr, *h_best = nullptr;
+    void* front = nullptr;
+    int* ready = nullptr;
+    long long front_cap = 0;
+    unsigned long long ticket_base = 0;  // ring tickets keep counting across contexts
+};
+static std::mutex g_pool_mu;
+static std::vector<EngineRes> g_pool;
+
 Engine::Engine(int device) : device_(device) {
     CK(cudaSetDevice(device));
-    cudaStream_t s;
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    stream_ = s;
-    cudaEvent_t a, b;
-    CK(cudaEventCreate(&a));
-    CK(cudaEventCreate(&b));
-    ev0_ = a;
-    ev1_ = b;
-    cudaEvent_t c, d, e, f;
-    CK(cudaEventCreate(&c));
-    CK(cudaEventCreate(&d));
-    CK(cudaEventCreate(&e));
-    CK(cudaEventCreate(&f));
-    evk0_ = c;
-    evk1_ = d;
-    evm0_ = e;
-    evm1_ = f;
-    // per-search staging blobs (Spec | Ctl | Leaf | root Cont) for a whole batch: one upload
-    // and one strided read-back per launch
-    CK(cudaMalloc(&d_blob_, MAXBATCH * BLOB_STRIDE));
-    CK(cudaMallocHost(&h_pin_, MAXBATCH * BLOB_STRIDE));
-    CK(cudaMalloc(&d_best_, MAXBATCH * sizeof(HitPath)));
-    CK(cudaMallocHost(&h_best_, MAXBATCH * sizeof(HitPath)));
-    dev_bytes_ += (long long)(MAXBATCH * (BLOB_STRIDE + sizeof(HitPath)));
+    EngineRes r;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        for (size_t i = 0; i < g_pool.size(); ++i)
+            if (g_pool[i].device == device) {
+                r = g_pool[i];
+                g_pool.erase(g_pool.begin() + i);
+                break;
+            }
+    }
+    if (r.device < 0) {
+        r.device = device;
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        r.stream = s;
+        for (auto& e : r.ev) {
+            cudaEvent_t x;
+            CK(cudaEventCreate(&x));
+            e = x;
+        }
+        // per-search staging blobs (Spec | Ctl | Leaf | root Cont) for a whole batch: one
+        // upload and one strided read-back per launch
+        CK(cudaMalloc(&r.d_blob, MAXBATCH * BLOB_STRIDE));
+        CK(cudaMallocHost(&r.h_pin, MAXBATCH * BLOB_STRIDE));
+        CK(cudaMalloc(&r.d_best, MAXBATCH * sizeof(HitPath)));
+        CK(cudaMallocHost(&r.h_best, MAXBATCH * sizeof(HitPath)));
+    }
+    stream_ = r.stream;
+    ev0_ = r.ev[0];
+    ev1_ = r.ev[1];
+    evk0_ = r.ev[2];
+    evk1_ = r.ev[3];
+    evm0_ = r.ev[4];
+    evm1_ = r.ev[5];
+    d_blob_ = r.d_blob;
+    h_pin_ = r.h_pin;
+    d_best_ = r.d_best;
+    h_best_ = r.h_best;
+    d_front_[0] = r.front;
+    d_ready_ = r.ready;
+    front_cap_ = r.front_cap;
+    ticket_base_ = r.ticket_base;
+    dev_bytes_ += (long long)(MAXBATCH * (BLOB_STRIDE + sizeof(HitPath))) +
+                  front_cap_ * (long long)(sizeof(Cont) + sizeof(int));
 }
 
 Engine::~Engine() {
     cudaSetDevice(device_);
+    cudaStreamSynchronize(S_(stream_));
     free_eval();
     cudaFree(d_base_);
     cudaFree(d_B_);
@@ -155,19 +192,25 @@ Engine::~Engine() {
     cudaFree(d_bound_);
     cudaFree(d_d_);
     cudaFree(d_u_);
-    cudaFree(d_blob_);
-    cudaFree(d_front_[0]);
-    cudaFree(d_ready_);
-    cudaFree(d_best_);
-    cudaFreeHost(h_pin_);
-    cudaFreeHost(h_best_);
-    cudaEventDestroy((cudaEvent_t)ev0_);
-    cudaEventDestroy((cudaEvent_t)ev1_);
-    cudaEventDestroy((cudaEvent_t)evk0_);
-    cudaEventDestroy((cudaEvent_t)evk1_);
-    cudaEventDestroy((cudaEvent_t)evm0_);
-    cudaEventDestroy((cudaEvent_t)evm1_);
-    cudaStreamDestroy(S_(stream_));
+    EngineRes r;
+    r.device = device_;
+    r.stream = stream_;
+    r.ev[0] = ev0_;
+    r.ev[1] = ev1_;
+    r.ev[2] = evk0_;
+    r.ev[3] = evk1_;
+    r.ev[4] = evm0_;
+    r.ev[5] = evm1_;
+    r.d_blob = d_blob_;
+    r.h_pin = h_pin_;
+    r.d_best = d_best_;
+    r.h_best = h_best_;
+    r.front = d_front_[0];
+    r.ready = d_ready_;
+    r.front_cap = front_cap_;
+    r.ticket_base = ticket_base_;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool.push_back(r);
 }
 
 void Engine::upload_rows(const Model& M) {
@@ -464,7 +507,7 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         alg_bytes_ += (long long)hc->leaves * 24LL * S.k;  // k option rows x 3 fp64 per leaf
         if (tune_.trace)
             std::fprintf(stderr, "[mosaic] %s k=%d thr=%.17g batch=%d ctas=%d kernel=%.3fms total=%.3fms "
-                                 "nodes=%llu leaves=%llu %s\\n",
+                                 "nodes=%llu leaves=%llu %s\n",
                          S.mode == MODE_MIN ? "MIN  " : "FIRST", S.k,
                          S.mode == MODE_MIN ? q.ub : S.theta, n, ctas[i], kms, ms, hc->nodes,
                          hc->leaves, res.found ? "hit" : (res.aborted ? "restart" : ""));

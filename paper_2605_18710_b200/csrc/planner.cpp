@@ -282,7 +282,10 @@ bool Planner::prep_min(const std::vector<int>& mods, double ub, SearchOp& op, mg
     op.req = mg::BatchReq{};
     if (!mg::build_spec(M_, q, op.req.S)) return false;
     op.req.ub = ub;
-    op.req.abort_below = ub >= POS_INF ? POS_INF : ub * (1.0 - 1e-4);
+    // restart with re-derived static bounds once the incumbent drops by >1e-4 — worth a new
+    // launch only for large stages; small ones finish in the same wave
+    const bool restart = (int)mods.size() >= eng_->tuning().restart_k;
+    op.req.abort_below = !restart ? 0.0 : (ub >= POS_INF ? POS_INF : ub * (1.0 - 1e-4));
     op.req.st = &st;
     return true;
 }

@@ -210,7 +210,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                              P(C.c_int), P(C.c_double), P(C.c_int), P(C.c_int),
                                              P(C.c_double)]),
         "mosaic_gpu_search": (C.c_int, [vp, P(C.c_uint64), C.c_int64, C.c_int,
-                                        P(StageResultC)]),
+                                        P(StageResultC), P(C.c_double), P(C.c_int32)]),
         "mosaic_gpu_launch_count": (C.c_int64, [vp]),
         "mosaic_gpu_search_ms": (C.c_double, [vp]),
         "mosaic_gpu_reset_counters": (None, [vp]),
@@ -486,14 +486,24 @@ class Planner:
             raise StageInfeasibleError("module has no feasible deployment option")
         return self._stage(r) if r.status == OK else None
 
-    def search(self, module_sets: Sequence[Sequence[int]], exact: bool = False
-               ) -> list[Optional[StageEvalResult]]:
+    def search(self, module_sets: Sequence[Sequence[int]], exact: bool = False,
+               times_only: bool = False):
         """Batched stage_eval (or ExactStageSolver::solve with exact=True) of many module sets
-        (mosaic_gpu_search): the computations advance together, one launch per wave."""
+        (mosaic_gpu_search): the computations advance together, one launch per wave.
+        times_only: just the stage times (None where infeasible), no allocations."""
         n = len(module_sets)
         masks = (C.c_uint64 * max(1, n))(*[self._mask(m) for m in module_sets])
+        if times_only:
+            t = (C.c_double * max(1, n))()
+            stt = (C.c_int32 * max(1, n))()
+            _raise(load_library().mosaic_gpu_search(self._ctx, masks, n, 1 if exact else 0,
+                                                    None, t, stt))
+            if not exact and any(stt[i] == MODULE_NO_OPTION for i in range(n)):
+                raise StageInfeasibleError("module has no feasible deployment option")
+            return [t[i] if stt[i] == OK else None for i in range(n)]
         out = (StageResultC * max(1, n))()
-        _raise(load_library().mosaic_gpu_search(self._ctx, masks, n, 1 if exact else 0, out))
+        _raise(load_library().mosaic_gpu_search(self._ctx, masks, n, 1 if exact else 0, out,
+                                                None, None))
         res = []
         for i in range(n):
             r = out[i]
