@@ -475,7 +475,6 @@ int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value) {
         else if (k == "small_tree") t.small_tree = value;
         else if (k == "deep_after") t.deep_after = v;
         else if (k == "lookahead") t.lookahead = (int)v;
-        else if (k == "small_grid") t.small_grid = (int)std::max(1LL, v);
         else if (k == "generic_kernel") t.generic_kernel = v != 0;
         else if (k == "shard_level") t.shard_level = (int)v;
         else if (k == "ring_per_walker") t.ring_per_walker = (int)std::max(1LL, v);

@@ -331,7 +331,7 @@ std::vector<SearchResult> Engine::search_batch(std::vector<BatchReq>& reqs) {
         long long grid_cap;
         size_t b1 = std::min(reqs.size(), b0 + (size_t)MAXBATCH);
         kernel_for(reqs, b0, b1, &kfn, &smem, &grid_cap);
-        b1 = std::min<size_t>(b1, b0 + (size_t)std::max<long long>(1, grid_cap / std::max(1, tune_.small_grid)));
+        b1 = std::min<size_t>(b1, b0 + (size_t)std::max<long long>(1, grid_cap));
         launch_chunk(reqs, b0, b1, kfn, smem, grid_cap, out);
         b0 = b1;
     }
@@ -357,7 +357,7 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         for (int l = 0; l < S.k; ++l) tuples *= (double)(S.lvl_n[l] > 0 ? S.lvl_n[l] : 1);
         small[i] = tuples * S.G <= tune_.small_tree;
         if (small[i]) {
-            ctas[i] = (int)std::min<long long>(tune_.small_grid, std::max<long long>(1, grid_cap / n));
+            ctas[i] = 1;  // one walker owns the whole tree (solo mode, search_kernel.cuh)
             small_total += ctas[i];
         } else {
             ++n_big;

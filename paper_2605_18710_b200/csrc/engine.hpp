@@ -77,12 +77,11 @@ struct Tuning {
     int don_depth = 3;      // donate levels <= k-1-don_depth (measured best on cfg5)
     int don_period = 4;     // power of two; control reads every 4 steps (tools/knob_solve.sh)
     int backoff_cap = 2048; // ns, idle walkers polling back-off cap (measured)
-    double small_tree = 2e5;  // option tuples x G below which small_grid CTAs run the search
+    double small_tree = 2e5;  // option tuples x G below which one walker runs the search alone
     long long deep_after = 16384;  // steps on one piece before deeper hand-overs are allowed
     // child look-ahead (can every remaining level still place an option?): off by default —
     // the lane-parallel option screen at the next level does the same job for less
     int lookahead = 0;
-    int small_grid = 8;     // CTAs for small trees
     int generic_kernel = 0; // never use the specialised kernels
     int shard_level = -1;   // override of the sharded option-prefix level (-1: default)
     int ring_per_walker = 16;  // cursor-ring slots per resident walker

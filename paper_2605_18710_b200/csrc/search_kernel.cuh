@@ -50,6 +50,12 @@ struct WarpHooks {
     int don_period;
     int may_donate;
     long long deep_after;
+    // solo: the only walker of its search (no hand-overs): control state it alone writes is
+    // kept in registers, so the DFS makes no L2 round trips for it
+    int solo;
+    int local_abort;
+    int has_hit_local;
+    double abort_below;
 
     __device__ bool hit_precedes() {  // lane 0 only
         int v0 = *(volatile int*)&ctl->ver;
@@ -67,6 +73,17 @@ struct WarpHooks {
         // global control state is read only every don_period steps: a per-step L2 round
         // trip (broadcast from lane 0) was the single hottest stall of the walker loop
         if ((steps & (unsigned)(don_period - 1)) != 0) return 0;
+        if (solo) {
+            int code = 0;
+            if (lane_id() == 0) {
+                if (local_abort)
+                    code = 2;
+                else if (mode == MODE_FIRST && has_hit_local &&
+                         path_precedes_rest((const HitPath*)best, *w, cur_level))
+                    code = 2;
+            }
+            return __shfl_sync(FULLW, code, 0);
+        }
         int code = 0;
         if (lane_id() == 0) {
             if (*(volatile int*)&ctl->abort) {
@@ -148,7 +165,7 @@ struct WarpHooks {
     }
     __device__ double thr(const Spec& S) {
         if (mode != MODE_MIN) return S.thp;
-        if ((refresh++ & 15) == 0) {
+        if (!solo && (refresh++ & 15) == 0) {
             double I = bcast_inc();
             inc_cache = I < inc_cache ? I : inc_cache;
         }
@@ -156,7 +173,7 @@ struct WarpHooks {
         return t < S.thp ? t : S.thp;
     }
     __device__ double incumbent() {  // refreshed every 16 calls, like thr()
-        if ((refresh++ & 15) == 0) {
+        if (!solo && (refresh++ & 15) == 0) {
             double I = bcast_inc();
             inc_cache = I < inc_cache ? I : inc_cache;
         }
@@ -165,7 +182,10 @@ struct WarpHooks {
     __device__ void improve(double v) {
         if (lane_id() == 0) {
             atomicMin(&ctl->inc, (unsigned long long)__double_as_longlong(v));
-            if (v < ctl->abort_below) atomicExch(&ctl->abort, 1);
+            if (v < abort_below) {
+                atomicExch(&ctl->abort, 1);
+                local_abort = 1;
+            }
         }
         if (v < inc_cache) inc_cache = v;
         __syncwarp();
@@ -174,7 +194,10 @@ struct WarpHooks {
     __device__ void improve_leaf(const Walk& wk, int j, double v) {
         if (lane_id() == 0) {
             atomicMin(&ctl->inc, (unsigned long long)__double_as_longlong(v));
-            if (v < ctl->abort_below) atomicExch(&ctl->abort, 1);
+            if (v < abort_below) {
+                atomicExch(&ctl->abort, 1);
+                local_abort = 1;
+            }
             while (atomicCAS(&ctl->lock, 0, 1) != 0) __nanosleep(64);
             __threadfence();
             if (!ctl->has_hit || v < ctl->leaf_val) {
@@ -268,12 +291,49 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
     }
     const int wid = threadIdx.x >> 5;
     const int lane = lane_id();
+    // no hand-overs (small trees): the first warp of the search's first CTA walks the whole
+    // tree alone, everyone else leaves at once
+    const bool solo = !S.donate;
+    if (solo && ((int)blockIdx.x != map.cta_off[sid_sh] || wid != 0)) return;
     const size_t wbytes = walk_layout(S.G, S.k, MG_SPECIALIZE).bytes;
     unsigned char* wbase = smem + SMEM_SPEC + wid * wbytes;
     Walk& w = *reinterpret_cast<Walk*>(wbase);
     if (lane == 0) walk_carve(w, wbase, S.G, S.k, MG_SPECIALIZE);
     __syncwarp();
     unsigned long long nodes = 0, leaves = 0;
+    if (solo) {
+        load_cont_warp(*root, w, MG_MODE(S) == MODE_FIRST);
+        WarpHooks h;
+        h.ctl = ctl;
+        h.mode = MG_MODE(S);
+        h.steps = 0;
+        h.refresh = 0;
+        h.leaf_out = leaf_out;
+        h.best = best;
+        h.q = Q;
+        h.ready = ready;
+        h.nodes = 0;
+        h.leaves = 0;
+        h.w = &w;
+        h.cur_level = 0;
+        h.don_period = S.don_period;
+        h.may_donate = 0;
+        h.deep_after = S.deep_after;
+        h.solo = 1;
+        h.local_abort = 0;
+        h.has_hit_local = ctl->has_hit;
+        h.abort_below = ctl->abort_below;
+        h.inc_cache = POS_INF;
+        h.inc_cache = h.bcast_inc();
+        dfs_warp(S, R, w, root->depth, h);
+        __syncwarp();
+        if (lane == 0) {
+            ctl->outstanding = 0;
+            atomicAdd(&ctl->nodes, h.nodes);
+            atomicAdd(&ctl->leaves, h.leaves);
+        }
+        return;
+    }
     while (true) {
         long long ticket = -1;
         if (lane == 0) {
@@ -330,6 +390,10 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
         h.don_period = S.don_period;
         h.may_donate = S.donate;
         h.deep_after = S.deep_after;
+        h.solo = 0;
+        h.local_abort = 0;
+        h.has_hit_local = 0;
+        h.abort_below = ctl->abort_below;
         h.inc_cache = POS_INF;
         h.inc_cache = h.bcast_inc();
         const int d0 = piece.depth;

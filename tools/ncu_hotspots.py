@@ -6,6 +6,7 @@ import re
 import sys
 
 sass_csv, line_dump = sys.argv[1], sys.argv[2]
+KNAME = sys.argv[3] if len(sys.argv) > 3 else 'k_search'
 src = {}
 for f in ['search_core.cuh', 'search_warp.cuh', 'engine.cu']:
     lines = open('paper_2605_18710_b200/csrc/' + f).read().split('\n')
@@ -28,13 +29,13 @@ for line in open(line_dump):
         cur = (m.group(1).split('/')[-1], int(m.group(2)))
         continue
     m = re.match(r'\s+/\*([0-9a-f]{4,})\*/\s+(.*?);', line)
-    if m and fnm and 'k_search' in fnm:
+    if m and fnm and KNAME in fnm:
         addr2[int(m.group(1), 16)] = cur
         ops[int(m.group(1), 16)] = m.group(2).split()[0] if m.group(2).split() else ''
 rows = list(csv.reader(open(sass_csv)))
-hdr = rows[1]
+hdr = next(r for r in rows if r and r[0] == 'Address')
 ia, iss, isrc = hdr.index('Address'), hdr.index('Warp Stall Sampling (All Samples)'), hdr.index('Source')
-base = int(rows[2][ia], 16)
+base = int(next(r for r in rows if r and r[0].startswith('0x'))[ia], 16)
 byline, byfn, tot, bad = collections.Counter(), collections.Counter(), 0.0, 0
 for r in rows[2:]:
     if len(r) < len(hdr):
