@@ -774,10 +774,12 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                 continue;
             }
             if (!first_comp_warp(w, o0, nb, dd)) continue;
+            __syncwarp();  // every lane has read ph[j] (loop head) before lane 0 rewrites it
             if (lane == 0) w.ph[j] = 1;
             __syncwarp();
         } else {
             if (!next_comp_warp(w, o0, nb)) {
+                __syncwarp();
                 if (lane == 0) w.ph[j] = 0;
                 __syncwarp();
                 continue;
