@@ -355,7 +355,7 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         const Spec& S = reqs[b0 + i].S;
         double tuples = 1.0;
         for (int l = 0; l < S.k; ++l) tuples *= (double)(S.lvl_n[l] > 0 ? S.lvl_n[l] : 1);
-        small[i] = tuples * S.G <= tune_.small_tree;
+        small[i] = reqs[b0 + i].force_solo || tuples * S.G <= tune_.small_tree;
         if (small[i]) {
             ctas[i] = 1;  // one walker owns the whole tree (solo mode, search_kernel.cuh)
             small_total += ctas[i];
@@ -392,6 +392,7 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
             hs->shard_rank = tune_.share_rank;
             hs->shard_world = tune_.share_world;
         }
+        if (q.force_solo) hs->shard_world = 1;  // a sequential replay is never sharded
         // option prefixes (o_0, o_1, o_2) are hashed to ranks: at 8 ranks the largest share of
         // the dominant cfg5 proof is 1.15x the mean (pairs: 1.3x)
         hs->shard_level = S.k >= 3 ? 2 : S.k - 1;

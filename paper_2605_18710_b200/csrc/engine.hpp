@@ -31,6 +31,7 @@ struct BatchReq {
     const HitPath* seed_path = nullptr;  // FIRST: a leaf known to satisfy theta ...
     const Leaf* seed_leaf = nullptr;     // ... as a path in this search's order
     SearchStats* st = nullptr;     // counters of the caller
+    bool force_solo = false;       // one walker in DFS order whatever the tree size
 };
 
 // What a rank contributes to the merge of one sharded search (one all-gather per launch:

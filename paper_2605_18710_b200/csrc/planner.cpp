@@ -447,6 +447,37 @@ StageJob Planner::exact_stage_job(uint64_t mask, StageResult* out) {
         }
     }
     SearchOp op;
+    if (!M_.nonneg()) {
+        // With a negative coefficient ExactStageSolver's option cut (`lb >= best_time_`,
+        // lb = base latency, oracle.hpp:127-139) is not a bound: its answer is the best leaf
+        // its sequential DFS happens to visit.  Replayed exactly: one walker in the
+        // reference's DFS order, the same cut against the running incumbent, strict
+        // improvements (the first argmin among visited leaves, oracle.hpp:120).
+        mg::SearchReq q;
+        q.mode = MODE_MIN;
+        q.ub = POS_INF;
+        q.level_module = mods;
+        op.req = mg::BatchReq{};
+        if (!mg::build_spec(M_, q, op.req.S)) {
+            res.status = INFEASIBLE;
+            co_return;
+        }
+        op.req.S.seq_cut = 1;
+        op.req.ub = POS_INF;
+        op.req.abort_below = 0.0;
+        op.req.force_solo = true;
+        op.req.st = &res.st;
+        const mg::SearchResult sr = co_await SearchAwait{&op};
+        if (sr.overflow) throw Error(TOO_LARGE, "stage needs more than 128 GPU blocks");
+        if (!sr.found) {
+            res.status = INFEASIBLE;
+            co_return;
+        }
+        res.status = OK;
+        res.stage_time = sr.leaf.value;
+        res.entries = leaf_entries(mods, sr.leaf);
+        co_return;
+    }
     if (!prep_first(mods, false, POS_INF, op, res.st)) {
         res.status = INFEASIBLE;
         co_return;

@@ -93,7 +93,10 @@ struct Spec {
     int don_max_level_tail;        //   ... or <= this once a walker ran deep_after steps on a piece
     long long deep_after;
     int lookahead;
-    int donate;                    // 0: never hand work over (small trees on a few CTAs)                 // child look-ahead depth in levels (0: off, see dfs_warp)
+    int donate;                    // 0: never hand work over (one walker owns the tree)
+    int seq_cut;                   // MIN, models with negative coefficients: skip an option whose
+                                   //   base latency reaches the incumbent (ExactStageSolver's
+                                   //   sequential cut, oracle.hpp:127-139); solo walker only
     int don_period;                // check for idle walkers every don_period option steps (2^n)
     int backoff_cap_ns;            // idle walkers poll the queue with back-off up to this
     int env_n[MAXK + 1];           // product-term envelope over unplaced levels >= j

@@ -541,6 +541,10 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                     const unsigned mk = w.vmask[j] >> (o - w.vbase[j]);
                     if (mk) {
                         o += __ffs(mk) - 1;
+                        if (!MG_NONNEG(S) && S.seq_cut && !(R.base[off + o] < h.incumbent())) {
+                            ++o;  // the reference's `lb >= best_time_` skip (oracle.hpp:137)
+                            continue;
+                        }
                         got = true;
                         break;
                     }
@@ -559,6 +563,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                             (unsigned)S.shard_rank)
                         continue;
                     if (w.used[j] + R.d[r] * R.u[r] + S.suffix_min[j + 1] > GL) continue;
+                    if (!MG_NONNEG(S) && S.seq_cut && !(R.base[r] < h.incumbent())) continue;
                     got = true;
                     break;
                 }
@@ -720,7 +725,8 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                     return 1;
                 } else {
                     const double I = h.incumbent();
-                    const double Ie = I * (1.0 - TIE_EPS);
+                    // sequential-cut replay: strict improvements only, no tie band
+                    const double Ie = (!MG_NONNEG(S) && S.seq_cut) ? I : I * (1.0 - TIE_EPS);
                     if (!last_feasible_warp(w, o0, nb, dd, Ie, false, rest, take)) continue;
                     double hiv = Ie;
                     while (true) {

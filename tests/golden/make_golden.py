@@ -149,6 +149,22 @@ def stime_edge() -> None:
     dump("stime_edge.json", out)
 
 
+def exact_negative() -> None:
+    """ExactStageSolver with negative interference coefficients: its option cut
+    (oracle.hpp:127-139) is not a bound there, so its answer depends on the sequential DFS —
+    every module set of small instances, two negative models."""
+    out = []
+    for inst, n in [("cfg1", 2), ("random:11:4:8", 4), ("cfg2", 3)]:
+        for extra in (["e=1e-3,-2e-4,5e-4"], ["e=2e-3,1e-3,-4e-4"], ["e=-1e-4,3e-4,2e-4"]):
+            for mask in range(1, 1 << n):
+                try:  # the cut is weak for these models: sets the CPU cannot finish are skipped
+                    r = ref(inst, "exact", str(mask), "levels=4", *extra, timeout=20)
+                except subprocess.TimeoutExpired:
+                    continue
+                out.append({"inst": inst, "extra": extra, "mask": mask, "r": r})
+    dump("exact_negative.json", out)
+
+
 def presets() -> None:
     # acceptance.cpp:171-198 (C5): all presets at 8 GPUs, with and without prune+cache
     out = []
