@@ -305,6 +305,13 @@ def main() -> None:
     ap.add_argument("--same-device", action="store_true",
                     help="every rank uses cuda:0 (sharding test on a single GPU)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch under torchrun on this node (the driver's own launch
+        # sets WORLD_SIZE and lands below)
+        os.execvp(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                   "--nproc-per-node", str(args.gpus), "--master-addr",
+                                   "127.0.0.1", "--master-port", str(29400 + os.getpid() % 500),
+                                   os.path.abspath(__file__)] + sys.argv[1:])
     if args.impl == "reference":
         reference_arm(args)
         return
