@@ -147,12 +147,14 @@ def _probe_jobs(name: str, sh: dict, c: dict) -> list:
     return out
 
 
-def ref(jobs: int, cap: float, probe_k: int) -> None:
+def ref(jobs: int, cap: float, probe_k: int, only: str | None = None) -> None:
     with open(GPU_OUT) as f:
         traj = json.load(f)
     done = _done_keys()
     todo = []
     for name, sh in traj.items():
+        if only and name != only:
+            continue
         lv = f"levels={sh['levels']}"
         for c in sh["cache"]:
             todo.append((c["k"], f"{name}|stage|{c['mask']}",
@@ -162,6 +164,8 @@ def ref(jobs: int, cap: float, probe_k: int) -> None:
         if sh["spec"] != "cfg5":
             todo.append((4.5, f"{name}|solve", [sh["spec"], "solve", lv]))
     todo = [j for j in sorted(todo, key=lambda j: j[0]) if j[1] not in done]
+    if only:  # a second runner for one shape: leave its full solve to the main runner
+        todo = [j for j in todo if not j[1].endswith("|solve")]
     print(f"{len(todo)} jobs ({len(done)} already recorded), {jobs} workers, cap {cap:.0f}s",
           flush=True)
     with cf.ThreadPoolExecutor(jobs) as ex:
@@ -184,6 +188,13 @@ def status() -> None:
             r = recs.get(key)
             if r is None:
                 st = "pending"
+                for p in ("feas_last_ok", "feas_conf"):
+                    q = recs.get(f"{name}|{p}|{c['mask']}")
+                    if q:
+                        ok = ("out" in q and float.fromhex(q["out"].get("t", "0x0p+0")) ==
+                              float.fromhex(c["t"])) if p == "feas_last_ok" else "out" in q
+                        st += f"; {p} " + (f"> {q['timeout']:.0f}s" if "timeout" in q else
+                                          f"{q['wall_s']:.1f}s" + (" MATCH" if ok else " DIFF"))
             elif "timeout" in r:
                 st = f"> {r['timeout']:.0f}s"
                 for p in ("feas_last_ok", "feas_conf"):
@@ -205,12 +216,13 @@ if __name__ == "__main__":
     ap.add_argument("out", nargs="?")
     ap.add_argument("--jobs", type=int, default=max(1, (os.cpu_count() or 2) - 2))
     ap.add_argument("--cap", type=float, default=36000.0)
+    ap.add_argument("--only", help="restrict to one shape (e.g. preset:ofasys:8:64@L10)")
     ap.add_argument("--probe-k", type=int, default=5,
                     help="also pin the deciding probes of masks with >= this many modules")
     a = ap.parse_args()
     if a.phase == "gpu":
         gpu(a.out)
     elif a.phase == "ref":
-        ref(a.jobs, a.cap, a.probe_k)
+        ref(a.jobs, a.cap, a.probe_k, a.only)
     else:
         status()
