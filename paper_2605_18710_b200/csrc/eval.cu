@@ -216,61 +216,91 @@ __global__ void __launch_bounds__(32 * KE_WARPS, 4)
                 }
             }
             __syncwarp();
-            // per GPU hosting a self entry: its delta, then max into the entry's key.  The
-            // fp64 max runs as two 32-bit atomicMax passes over the order-preserving key
-            // (high words, then low words among the GPUs that reached the high maximum).
             unsigned used = 0u;
-            for (int g = lane; g < G; g += 32) {
-                const unsigned m = mask[g];
-                unsigned sm = m & selfm;
-                if (!sm) continue;
-                if (self_in) {
-                    const double v = ke_delta(P, eB, m, 0u);
-                    dl[g] = v;
+            unsigned long long rk = 0ULL;
+            if (self_in && G <= 128) {
+                // <= 4 GPUs per lane, in registers: each GPU hosting a self entry gets ONE
+                // delta (its resident set, entry order); each self entry's max over its GPUs
+                // is a lane-local max then a warp max of the order-preserving 64-bit key
+                // (high words, then low words among the lanes holding the high maximum)
+                unsigned mloc[4];
+                unsigned long long kloc[4];
+                #pragma unroll
+                for (int s = 0; s < 4; ++s) {
+                    const int g = lane + 32 * s;
+                    unsigned m = g < G ? mask[g] : 0u;
+                    if (!(m & selfm)) m = 0u;
+                    mloc[s] = m;
                     used |= m;
-                    const unsigned hi = (unsigned)(ke_key(v) >> 32);
-                    while (sm) {
-                        const int e = __ffs(sm) - 1;
-                        sm &= sm - 1;
-                        atomicMax(&whi[e], hi);
-                    }
-                } else {
-                    while (sm) {
-                        const int e = __ffs(sm) - 1;
-                        sm &= sm - 1;
-                        const unsigned r = m & ~esm[e];
-                        used |= r;
-                        atomicMax(&whi[e], (unsigned)(ke_key(ke_delta(P, eB, r, 0u)) >> 32));
+                    kloc[s] = m ? ke_key(ke_delta(P, eB, m, 0u)) : 0ULL;
+                }
+                for (int e = 0; e < ne; ++e) {
+                    if (!(selfm >> e & 1u)) continue;
+                    unsigned long long k = 0ULL;
+                    #pragma unroll
+                    for (int s = 0; s < 4; ++s)
+                        if ((mloc[s] >> e & 1u) && kloc[s] > k) k = kloc[s];
+                    const unsigned hi = __reduce_max_sync(KE_FULL, (unsigned)(k >> 32));
+                    const unsigned lo = __reduce_max_sync(
+                        KE_FULL, (unsigned)(k >> 32) == hi ? (unsigned)k : 0u);
+                    if (lane == e) rk = (unsigned long long)hi << 32 | lo;
+                }
+            } else {
+                // per GPU hosting a self entry: its delta, then max into the entry's key.  The
+                // fp64 max runs as two 32-bit atomicMax passes over the order-preserving key
+                // (high words, then low words among the GPUs that reached the high maximum).
+                for (int g = lane; g < G; g += 32) {
+                    const unsigned m = mask[g];
+                    unsigned sm = m & selfm;
+                    if (!sm) continue;
+                    if (self_in) {
+                        const double v = ke_delta(P, eB, m, 0u);
+                        dl[g] = v;
+                        used |= m;
+                        const unsigned hi = (unsigned)(ke_key(v) >> 32);
+                        while (sm) {
+                            const int e = __ffs(sm) - 1;
+                            sm &= sm - 1;
+                            atomicMax(&whi[e], hi);
+                        }
+                    } else {
+                        while (sm) {
+                            const int e = __ffs(sm) - 1;
+                            sm &= sm - 1;
+                            const unsigned r = m & ~esm[e];
+                            used |= r;
+                            atomicMax(&whi[e], (unsigned)(ke_key(ke_delta(P, eB, r, 0u)) >> 32));
+                        }
                     }
                 }
-            }
-            __syncwarp();
-            for (int g = lane; g < G; g += 32) {
-                const unsigned m = mask[g];
-                unsigned sm = m & selfm;
-                if (!sm) continue;
-                if (self_in) {
-                    const unsigned long long k = ke_key(dl[g]);
-                    const unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
-                    while (sm) {
-                        const int e = __ffs(sm) - 1;
-                        sm &= sm - 1;
-                        if (whi[e] == hi) atomicMax(&wlo[e], lo);
-                    }
-                } else {
-                    while (sm) {
-                        const int e = __ffs(sm) - 1;
-                        sm &= sm - 1;
-                        const unsigned long long k = ke_key(ke_delta(P, eB, m & ~esm[e], 0u));
-                        if (whi[e] == (unsigned)(k >> 32)) atomicMax(&wlo[e], (unsigned)k);
+                __syncwarp();
+                for (int g = lane; g < G; g += 32) {
+                    const unsigned m = mask[g];
+                    unsigned sm = m & selfm;
+                    if (!sm) continue;
+                    if (self_in) {
+                        const unsigned long long k = ke_key(dl[g]);
+                        const unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
+                        while (sm) {
+                            const int e = __ffs(sm) - 1;
+                            sm &= sm - 1;
+                            if (whi[e] == hi) atomicMax(&wlo[e], lo);
+                        }
+                    } else {
+                        while (sm) {
+                            const int e = __ffs(sm) - 1;
+                            sm &= sm - 1;
+                            const unsigned long long k = ke_key(ke_delta(P, eB, m & ~esm[e], 0u));
+                            if (whi[e] == (unsigned)(k >> 32)) atomicMax(&wlo[e], (unsigned)k);
+                        }
                     }
                 }
+                __syncwarp();
+                rk = (unsigned long long)whi[lane] << 32 | wlo[lane];
             }
-            __syncwarp();
             used = __reduce_or_sync(KE_FULL, used);
             // rectified_latency = base of the self entry + its worst GPU delta (an entry
             // without GPUs keeps the reference's -1e300 seed)
-            const unsigned long long rk = (unsigned long long)whi[lane] << 32 | wlo[lane];
             double rl = r_base + (rk ? ke_unkey(rk) : KE_NEG);
             const bool miss = (is_self && isnan(r_base)) || (has && (used >> lane & 1u) && isnan(eB[lane]));
             rl = __shfl_sync(KE_FULL, rl, __ffs(same) - 1);

@@ -8,7 +8,7 @@ import sys
 sass_csv, line_dump = sys.argv[1], sys.argv[2]
 KNAME = sys.argv[3] if len(sys.argv) > 3 else 'k_search'
 src = {}
-for f in ['search_core.cuh', 'search_warp.cuh', 'engine.cu']:
+for f in ['search_core.cuh', 'search_warp.cuh', 'engine.cu', 'search_kernel.cuh']:
     lines = open('paper_2605_18710_b200/csrc/' + f).read().split('\n')
     cur, m = '?', []
     for l in lines:
