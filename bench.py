@@ -389,8 +389,19 @@ def main() -> None:
     value = SAMPLE_LEAVES * args.steps / (t_max / 1000.0) if t_max > 0 else 0.0
 
     # ---- time to the best plan: the full solve (frontier sharded over ranks) ----
+    plane = None
     if world > 1:
-        pl.set_shard(rank, world, allgather_bytes)
+        if args.dist_backend == "nccl":
+            # the library's own data plane: one NCCL communicator from a unique id rank 0 makes
+            idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+            if rank == 0:
+                idt.copy_(torch.frombuffer(bytearray(mosaic.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(idt, 0)
+            pl.set_shard_nccl(rank, world, bytes(idt.cpu().numpy().tobytes()))
+            plane = "in-library NCCL all-gather per batched launch"
+        else:
+            pl.set_shard(rank, world, allgather_bytes)
+            plane = f"caller all-gather over {args.dist_backend} per batched launch"
     for _ in range(max(1, args.warmup)):
         res = pl.solve()
     solve_ms = []
@@ -467,7 +478,8 @@ def main() -> None:
                                                         f"GPU(s); solve frontier sharded"),
         "same_config": headline,
         "time_to_best_plan_s": ttbp, "best_plan_iteration_time": best_plan,
-        "full_solve": {"stage_eval_calls": searches_per_solve, "median_ms": ttbp * 1000.0},
+        "full_solve": {"stage_eval_calls": searches_per_solve, "median_ms": ttbp * 1000.0,
+                       "data_plane": plane},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "timing": "host wall clock, create+sample+readback"},
         "gpu_launches": ctr["own_launches"],

@@ -268,6 +268,15 @@ typedef int (*mosaic_gpu_allgather_fn)(void* user, const void* send, void* recv,
 int mosaic_gpu_set_shard(mosaic_gpu_ctx* ctx, int rank, int world, mosaic_gpu_allgather_fn fn,
                          void* user);
 
+/* The same sharding with the data plane INSIDE the library: rank 0 calls mosaic_gpu_nccl_id
+ * (NCCL_UNIQUE_ID_BYTES = 128 bytes), the caller hands those bytes to every rank (any
+ * out-of-band channel), every rank calls mosaic_gpu_set_shard_nccl; the library then builds a
+ * NCCL communicator (libnccl.so.2, loaded at run time) and runs one ncclAllGather of the
+ * launch's RankRecords per batched launch on the context's stream — no callback.  world = 1
+ * is allowed (the merge path runs on one rank). */
+int mosaic_gpu_nccl_id(void* id_out, size_t cap);
+int mosaic_gpu_set_shard_nccl(mosaic_gpu_ctx* ctx, int rank, int world, const void* nccl_id);
+
 /* The merge every sharded search goes through (Engine::merge_ranks), exported for the
  * multi-process CPU tests: world records of mosaic_gpu_rank_record_size() bytes, built with
  * mosaic_gpu_rank_record (x is k rows of 128 block counts).  mode 0 = MIN (smallest

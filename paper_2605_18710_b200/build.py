@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX_HOST", "g++")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["engine.cu", "eval.cu", "pack.cu", "sim.cu"]
+CU_SOURCES = ["engine.cu", "eval.cu", "nccl_plane.cu", "pack.cu", "sim.cu"]
 # engine_fast.cu is compiled once per search mode (specialised MIN / FIRST kernels)
 CU_VARIANTS = [("engine_fast.cu", "engine_fast_min", ["-DMG_FAST_MODE=0"]),
                ("engine_fast.cu", "engine_fast_first", ["-DMG_FAST_MODE=1"]),
@@ -67,7 +67,7 @@ def build(verbose_ptxas: bool = False) -> str:
             _run([CXX, "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-Wall",
                   "-I/usr/local/cuda/include", "-c", s, "-o", o])
     if _newer(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fPIC"])
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fPIC", "-ldl"])
     return LIB
 
 

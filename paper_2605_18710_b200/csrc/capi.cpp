@@ -490,6 +490,25 @@ int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value) {
 
 int64_t mosaic_gpu_device_bytes(mosaic_gpu_ctx* ctx) { return ctx->pl->engine().device_bytes(); }
 
+int mosaic_gpu_nccl_id(void* id_out, size_t cap) {
+    return guard([&] {
+        if (!id_out || cap < mg::nccl_id_bytes())
+            throw Error(MOSAIC_INVALID_ARGUMENT, "id buffer smaller than NCCL_UNIQUE_ID_BYTES");
+        mg::nccl_unique_id(id_out);
+        return MOSAIC_OK;
+    });
+}
+
+int mosaic_gpu_set_shard_nccl(mosaic_gpu_ctx* ctx, int rank, int world, const void* nccl_id) {
+    return guard([&] {
+        if (!ctx || !nccl_id) throw Error(MOSAIC_RANGE, "null argument");
+        ctx->pl->engine().set_shard_nccl(rank, world, nccl_id);
+        ctx->rank = rank;
+        ctx->world = world;
+        return MOSAIC_OK;
+    });
+}
+
 size_t mosaic_gpu_rank_record_size(void) { return sizeof(mg::RankRecord); }
 
 int mosaic_gpu_rank_record(void* rec, int has_hit, int aborted, int overflow, double inc, int k,

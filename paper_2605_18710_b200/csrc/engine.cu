@@ -186,6 +186,7 @@ Engine::~Engine() {
     cudaSetDevice(device_);
     cudaStreamSynchronize(S_(stream_));
     free_eval();
+    free_nccl();
     cudaFree(d_base_);
     cudaFree(d_B_);
     cudaFree(d_fp_);
@@ -516,7 +517,7 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
     ticket_base_ = tmax + 1;
     // ranks must leave every search with the same answer (they replay the same control flow
     // and all-gather once per launch): merge after the local results are complete
-    if (world_ > 1 && ag_) merge_ranks(reqs, b0, b1, out);
+    if ((world_ > 1 && ag_) || nccl_comm_) merge_ranks(reqs, b0, b1, out);
 }
 
 void Engine::evaluate(const std::vector<EvalEntry>& ent, const std::vector<int>& gpus,
@@ -618,7 +619,7 @@ int merge_rank_records(const RankRecord* all, int world, int mode, int k, Search
 
 void Engine::merge_ranks(const std::vector<BatchReq>& reqs, size_t b0, size_t b1,
                          std::vector<SearchResult>& out) {
-    if (!ag_) throw std::runtime_error("multi-GPU search without an all-gather");
+    if (!ag_ && !nccl_comm_) throw std::runtime_error("multi-GPU search without an all-gather");
     const size_t n = b1 - b0;
     const char* pin = reinterpret_cast<const char*>(h_pin_);
     std::vector<RankRecord> mine(n), all(n * world_);
@@ -654,7 +655,9 @@ void Engine::merge_ranks(const std::vector<BatchReq>& reqs, size_t b0, size_t b1
         }
     }
     // all-gather of n records per rank: rank r's records land at all[r * n .. r * n + n)
-    if (ag_(ag_user_, mine.data(), all.data(), n * sizeof(RankRecord)) != 0)
+    if (nccl_comm_)
+        nccl_allgather(mine.data(), all.data(), n * sizeof(RankRecord));
+    else if (ag_(ag_user_, mine.data(), all.data(), n * sizeof(RankRecord)) != 0)
         throw std::runtime_error("all-gather failed");
     std::vector<RankRecord> per(world_);
     for (size_t i = 0; i < n; ++i) {

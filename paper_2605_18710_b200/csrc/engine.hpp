@@ -46,6 +46,8 @@ struct RankRecord {
 // The merge rule the engine applies to every sharded search (exported through the C ABI
 // for the multi-process CPU tests).  Returns the winning rank (-1: no FIRST hit).
 int merge_rank_records(const RankRecord* all, int world, int mode, int k, SearchResult& res);
+size_t nccl_id_bytes();
+void nccl_unique_id(void* out);  // ncclGetUniqueId through the run-time loaded NCCL
 
 struct EvalEntry {  // device evaluator input (one per allocation entry)
     int row;        // option row (base, B) of this entry
@@ -131,11 +133,14 @@ class Engine {
     // fn == nullptr with world > 1: measure this rank's share only (no merge; the result
     // is NOT the stage's answer — used to simulate shard balance on one device)
     void set_shard(int rank, int world, AllGatherFn fn, void* user) {
+        free_nccl();
         rank_ = rank;
         world_ = world;
         ag_ = fn;
         ag_user_ = user;
     }
+    // the in-library data plane: a NCCL communicator from a unique id (nccl_plane.cu)
+    void set_shard_nccl(int rank, int world, const void* nccl_id);
     Tuning& tuning() { return tune_; }
     // bytes of device memory the engine holds (option table, ring, control blocks)
     long long device_bytes() const { return dev_bytes_; }
@@ -173,6 +178,11 @@ class Engine {
                       size_t smem, long long grid_cap, std::vector<SearchResult>& out);
     void merge_ranks(const std::vector<BatchReq>& reqs, size_t b0, size_t b1,
                      std::vector<SearchResult>& out);
+    void nccl_allgather(const void* send, void* recv, size_t bytes);
+    void free_nccl();
+    void* nccl_comm_ = nullptr;
+    void* d_rec_ = nullptr;
+    size_t rec_cap_ = 0;
     int device_;
     int rank_ = 0, world_ = 1;
     AllGatherFn ag_ = nullptr;

@@ -155,7 +155,8 @@ EXPORTS = [
     "mosaic_gpu_brute_force", "mosaic_gpu_trace_rounds", "mosaic_gpu_trace_round",
     "mosaic_gpu_trace_cand", "mosaic_gpu_clear_cache", "mosaic_gpu_set_shard",
     "mosaic_gpu_rank_record_size", "mosaic_gpu_rank_record", "mosaic_gpu_merge_ranks",
-    "mosaic_gpu_search", "mosaic_gpu_launch_count", "mosaic_gpu_search_ms",
+    "mosaic_gpu_search", "mosaic_gpu_nccl_id", "mosaic_gpu_set_shard_nccl",
+    "mosaic_gpu_launch_count", "mosaic_gpu_search_ms",
     "mosaic_gpu_reset_counters", "mosaic_gpu_synth_problem", "mosaic_gpu_free_problem",
     "mosaic_gpu_own_launches", "mosaic_gpu_ksearch_ms", "mosaic_gpu_ksearch_launches",
     "mosaic_gpu_h2d_bytes", "mosaic_gpu_d2h_bytes", "mosaic_gpu_mark", "mosaic_gpu_marked_ms", "mosaic_gpu_alg_bytes", "mosaic_gpu_stage_min",
@@ -203,6 +204,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "mosaic_gpu_clear_cache": (None, [vp]),
         "mosaic_gpu_set_shard": (C.c_int, [vp, C.c_int, C.c_int, ALLGATHER_FN, vp]),
         "mosaic_gpu_rank_record_size": (C.c_size_t, []),
+        "mosaic_gpu_nccl_id": (C.c_int, [vp, C.c_size_t]),
+        "mosaic_gpu_set_shard_nccl": (C.c_int, [vp, C.c_int, C.c_int, vp]),
         "mosaic_gpu_rank_record": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                              P(C.c_uint16), P(C.c_uint16), P(C.c_uint16),
                                              C.c_double]),
@@ -743,6 +746,12 @@ class Planner:
                         [(tau[i], bool(ok[i])) for i in range(npb.value)]))
         return out
 
+    def set_shard_nccl(self, rank: int, world: int, nccl_id: bytes) -> None:
+        """Shard every device search over `world` ranks with the library's own NCCL
+        communicator (mosaic_gpu_set_shard_nccl); nccl_id from nccl_unique_id() on rank 0."""
+        buf = C.create_string_buffer(bytes(nccl_id), len(nccl_id))
+        _raise(load_library().mosaic_gpu_set_shard_nccl(self._ctx, rank, world, buf))
+
     def set_shard(self, rank: int, world: int, allgather=None) -> None:
         """allgather(send: bytes) -> list[bytes] over ranks (torch.distributed in bench.py)."""
         if world <= 1:
@@ -816,6 +825,13 @@ def candidate_options(planner: Planner, module: int) -> list[CandidateOption]:
 
 
 MAXB = 128  # GPU blocks per search level (search_core.cuh)
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (128 bytes, to hand to every rank)."""
+    buf = C.create_string_buffer(128)
+    _raise(load_library().mosaic_gpu_nccl_id(buf, 128))
+    return buf.raw
 
 
 def rank_record(has_hit: bool, inc: float, path=(), aborted: bool = False,

@@ -43,3 +43,17 @@ def test_bench_spawns_ranks_for_gpus_flag():
     assert line["n_gpus"] == 2 and line["same_config"] is True and line["value"] > 0
     traj = load_golden("trajectory_gpu.json")["cfg5@L32"]
     assert line["best_plan_iteration_time"] == hexf(traj["iteration_time"])
+
+
+def test_in_library_nccl_plane_world1():
+    # the library's own NCCL communicator (mosaic_gpu_nccl_id / mosaic_gpu_set_shard_nccl):
+    # with one rank the full merge path (record upload, ncclAllGather, merge) runs on every
+    # batched launch and the plans must not change
+    from paper_2605_18710_b200 import mosaic
+    gold = load_golden("configs.json")
+    for w in ("cfg3", "cfg4"):
+        pl = mosaic.Planner.from_spec(w, device=0)
+        pl.set_shard_nccl(0, 1, mosaic.nccl_unique_id())
+        r = pl.solve()
+        assert r.plan.predicted_iteration_time == hexf(gold[w]["solve"]["iteration_time"])
+        pl.close()
