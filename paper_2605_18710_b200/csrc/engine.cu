@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -282,6 +283,19 @@ SearchResult Engine::search(const Spec& S, double ub, double abort_below, Search
     return search_batch(one)[0];
 }
 
+// The dynamic shared-memory limit is a property of the kernel function (process-wide), so it is
+// only ever raised: several contexts (problems of different sizes) share the kernels.
+static void raise_smem_attr(const void* kfn, size_t smem) {
+    static std::mutex mu;
+    static std::map<const void*, size_t> set;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = set[kfn];
+    if (smem > cur) {
+        CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cur = smem;
+    }
+}
+
 // Kernel, shared memory and resident grid for (kernel index, smem bytes).
 void Engine::kernel_for(const std::vector<BatchReq>& reqs, size_t b0, size_t b1,
                         const void** kfn, size_t* smem, long long* grid) {
@@ -307,10 +321,7 @@ void Engine::kernel_for(const std::vector<BatchReq>& reqs, size_t b0, size_t b1,
     const long long key = (long long)ki << 40 | (long long)*smem;
     auto it = grid_cache_.find(key);
     if (it == grid_cache_.end()) {
-        if (*smem > smem_attr_[ki]) {
-            CK(cudaFuncSetAttribute(*kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
-            smem_attr_[ki] = *smem;
-        }
+        raise_smem_attr(*kfn, *smem);
         int per_sm = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, *kfn, 32 * WPC, *smem));
         int sms = 148;
@@ -358,7 +369,9 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         for (int l = 0; l < S.k; ++l) tuples *= (double)(S.lvl_n[l] > 0 ? S.lvl_n[l] : 1);
         small[i] = reqs[b0 + i].force_solo || tuples * S.G <= tune_.small_tree;
         if (small[i]) {
-            ctas[i] = 1;  // one walker owns the whole tree (solo mode, search_kernel.cuh)
+            // one walker owns the whole tree (solo mode, search_kernel.cuh); with several ranks
+            // a small search runs whole on ONE rank (its owner) instead of sharded everywhere
+            ctas[i] = sharded() && owner_of(i) != rank_ ? 0 : 1;
             small_total += ctas[i];
         } else {
             ++n_big;
@@ -393,7 +406,7 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
             hs->shard_rank = tune_.share_rank;
             hs->shard_world = tune_.share_world;
         }
-        if (q.force_solo) hs->shard_world = 1;  // a sequential replay is never sharded
+        if (small[i]) hs->shard_world = 1;  // solo searches are never sharded (owner runs it)
         // option prefixes (o_0, o_1, o_2) are hashed to ranks: at 8 ranks the largest share of
         // the dominant cfg5 proof is 1.15x the mean (pairs: 1.3x)
         hs->shard_level = S.k >= 3 ? 2 : S.k - 1;
@@ -459,7 +472,8 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         int* a3 = d_ready_;
         int a9 = (int)(t0 + 1);
         void* args[] = {&a0, &R, &Q, &a3, &a4, &a5, &a6, &a7, &map, &a9};
-        CK(cudaLaunchKernel(kfn, dim3((unsigned)map.cta_off[n]), dim3(32 * WPC), args, smem, s));
+        if (map.cta_off[n] > 0)  // (every search of the launch may belong to other ranks)
+            CK(cudaLaunchKernel(kfn, dim3((unsigned)map.cta_off[n]), dim3(32 * WPC), args, smem, s));
     }
     CK(cudaEventRecord((cudaEvent_t)evk1_, s));
     ++launches_;
@@ -517,7 +531,12 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
     ticket_base_ = tmax + 1;
     // ranks must leave every search with the same answer (they replay the same control flow
     // and all-gather once per launch): merge after the local results are complete
-    if ((world_ > 1 && ag_) || nccl_comm_) merge_ranks(reqs, b0, b1, out);
+    if (sharded()) {
+        owned_.assign(n, -1);
+        for (int i = 0; i < n; ++i)
+            if (small[i]) owned_[i] = owner_of(i);
+        merge_ranks(reqs, b0, b1, out);
+    }
 }
 
 void Engine::evaluate(const std::vector<EvalEntry>& ent, const std::vector<int>& gpus,
@@ -661,6 +680,17 @@ void Engine::merge_ranks(const std::vector<BatchReq>& reqs, size_t b0, size_t b1
         throw std::runtime_error("all-gather failed");
     std::vector<RankRecord> per(world_);
     for (size_t i = 0; i < n; ++i) {
+        if (owned_[i] >= 0) {
+            // a whole search run by its owner rank: its record is the answer
+            const RankRecord& x = all[(size_t)owned_[i] * n + i];
+            SearchResult& res = out[b0 + i];
+            res.overflow = x.overflow != 0;
+            res.aborted = x.aborted != 0;
+            res.found = x.has_hit != 0;
+            if (res.found) res.leaf = x.leaf;
+            if (reqs[b0 + i].S.mode == MODE_MIN) res.value = x.inc;
+            continue;
+        }
         for (int r = 0; r < world_; ++r) per[r] = all[(size_t)r * n + i];
         merge_rank_records(per.data(), world_, reqs[b0 + i].S.mode, reqs[b0 + i].S.k, out[b0 + i]);
     }

@@ -179,6 +179,10 @@ class Engine {
     void merge_ranks(const std::vector<BatchReq>& reqs, size_t b0, size_t b1,
                      std::vector<SearchResult>& out);
     void nccl_allgather(const void* send, void* recv, size_t bytes);
+    bool sharded() const { return (world_ > 1 && ag_) || nccl_comm_; }
+    // owner rank of the i-th search of a launch (every rank builds the same launches)
+    int owner_of(int i) const { return world_ > 1 ? i % world_ : 0; }
+    std::vector<int> owned_;  // per search of the current launch: owner rank, -1 = sharded
     void free_nccl();
     void* nccl_comm_ = nullptr;
     void* d_rec_ = nullptr;
@@ -199,8 +203,6 @@ class Engine {
     int* d_ready_ = nullptr;
     void* d_best_ = nullptr;  // MAXBATCH HitPaths
     void* h_best_ = nullptr;  // pinned mirror (seeds in, rank merge out)
-    // [generic, specialised MIN, specialised FIRST, specialised any-mode]
-    size_t smem_attr_[4] = {0, 0, 0, 0};
     std::map<long long, long long> grid_cache_;  // (kernel, smem) -> resident CTAs
     Tuning tune_;
     unsigned long long ticket_base_ = 0;

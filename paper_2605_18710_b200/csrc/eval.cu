@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -469,8 +470,17 @@ void Engine::set_rate_tables(const std::vector<double>& base, const std::vector<
         evb_ = b;
     }
     ev_smem_ = KE_WARPS * ke_warp_bytes(G);
-    CKE(cudaFuncSetAttribute(k_evaluate, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)ev_smem_));
+    {
+        // a property of the kernel (process-wide): only ever raised, contexts share it
+        static std::mutex mu;
+        static size_t set = 0;
+        std::lock_guard<std::mutex> lk(mu);
+        if (ev_smem_ > set) {
+            CKE(cudaFuncSetAttribute(k_evaluate, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)ev_smem_));
+            set = ev_smem_;
+        }
+    }
     int per_sm = 0, sms = 148;
     CKE(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_evaluate, 32 * KE_WARPS,
                                                       ev_smem_));

@@ -75,3 +75,16 @@ def test_solve_launches_fewer_than_searches():
         c = pl.counters()
         assert c["ksearch_launches"] < r.trace.gpu_searches, (spec, c, r.trace.gpu_searches)
         pl.close()
+
+
+def test_contexts_of_different_sizes_interleave():
+    # kernel attributes (dynamic shared memory) are process-wide: a small problem's context
+    # must not break a larger one created earlier (regression: 'invalid argument' launches)
+    big = mosaic.Planner.from_spec("cfg5", device=0)
+    small = mosaic.Planner.from_spec("cfg3", device=0)
+    a = big.stage_eval([0, 1, 2, 3])
+    small.solve()
+    b = big.stage_eval([0, 1, 2, 3])
+    assert a.stage_time == b.stage_time
+    small.close()
+    big.close()
