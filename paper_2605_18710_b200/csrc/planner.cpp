@@ -522,9 +522,12 @@ StageJob Planner::exact_stage_job(uint64_t mask, StageResult* out) {
 // Advance every job to its next device search; run each wave of pending searches as one
 // batched launch; repeat until all jobs are done.  The first exception is rethrown.
 void Planner::run_jobs(std::vector<StageJob>& jobs) {
+    const bool trace = eng_->tuning().trace;
+    double t_host = 0.0, t_dev = 0.0, t0 = now_s();
     for (auto& j : jobs) j.h.resume();
     std::vector<mg::BatchReq> reqs;
     std::vector<StageJob*> who;
+    int waves = 0;
     while (true) {
         reqs.clear();
         who.clear();
@@ -534,7 +537,12 @@ void Planner::run_jobs(std::vector<StageJob>& jobs) {
                 who.push_back(&j);
             }
         if (reqs.empty()) break;
+        const double t1 = now_s();
+        t_host += t1 - t0;
         std::vector<mg::SearchResult> res = eng_->search_batch(reqs);
+        t0 = now_s();
+        t_dev += t0 - t1;
+        ++waves;
         for (size_t i = 0; i < who.size(); ++i) {
             auto& pr = who[i]->h.promise();
             pr.op->res = res[i];
@@ -542,6 +550,10 @@ void Planner::run_jobs(std::vector<StageJob>& jobs) {
             who[i]->h.resume();
         }
     }
+    t_host += now_s() - t0;
+    if (trace)
+        std::fprintf(stderr, "[mosaic] batch of %zu: %d waves, host %.3f ms, launches %.3f ms\n",
+                     jobs.size(), waves, 1e3 * t_host, 1e3 * t_dev);
     for (auto& j : jobs)
         if (j.h.promise().exc) std::rethrow_exception(j.h.promise().exc);
 }
