@@ -397,8 +397,19 @@ def main() -> None:
             if rank == 0:
                 idt.copy_(torch.frombuffer(bytearray(mosaic.nccl_unique_id()), dtype=torch.uint8))
             dist.broadcast(idt, 0)
-            pl.set_shard_nccl(rank, world, bytes(idt.cpu().numpy().tobytes()))
-            plane = "in-library NCCL all-gather per batched launch"
+            try:
+                pl.set_shard_nccl(rank, world, bytes(idt.cpu().numpy().tobytes()))
+                ok = 1
+            except mosaic.MosaicError as e:  # reported in the line, never silent
+                print(f"[bench] in-library NCCL plane unavailable: {e}", file=sys.stderr)
+                ok = 0
+            flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag[0]):
+                plane = "in-library NCCL all-gather per batched launch"
+            else:
+                pl.set_shard(rank, world, allgather_bytes)
+                plane = "caller all-gather over torch.distributed (in-library NCCL failed)"
         else:
             pl.set_shard(rank, world, allgather_bytes)
             plane = f"caller all-gather over {args.dist_backend} per batched launch"
