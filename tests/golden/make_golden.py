@@ -149,6 +149,27 @@ def stime_edge() -> None:
     dump("stime_edge.json", out)
 
 
+def random_solves() -> None:
+    """Full GAHC solves of medium random instances (4-6 modules, 16-64 GPUs, L=10): the
+    regime where device searches use shared walkers and GAHC rounds are batched.  Instances
+    the CPU cannot solve in 60 s are skipped."""
+    import concurrent.futures as cf
+    jobs = []
+    for seed in range(1, 61):
+        n = 4 + seed % 3
+        g = [16, 32, 64][(seed // 3) % 3]
+        jobs.append(f"random:{seed}:{n}:{g}")
+
+    def run(inst):
+        try:
+            return ref(inst, "solve", timeout=60)
+        except subprocess.TimeoutExpired:
+            return None
+    with cf.ThreadPoolExecutor(2) as ex:
+        out = [r for r in ex.map(run, jobs) if r is not None]
+    dump("random_solves.json", out)
+
+
 def exact_negative() -> None:
     """ExactStageSolver with negative interference coefficients: its option cut
     (oracle.hpp:127-139) is not a bound there, so its answer depends on the sequential DFS —
