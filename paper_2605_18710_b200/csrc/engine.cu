@@ -131,6 +131,8 @@ struct EngineRes {
     int* ready = nullptr;
     long long front_cap = 0;
     unsigned long long ticket_base = 0;  // ring tickets keep counting across contexts
+    void *d_rows = nullptr, *h_rows = nullptr;  // option-table arena (+ pinned staging)
+    size_t rows_cap = 0;
 };
 static std::mutex g_pool_mu;
 static std::vector<EngineRes> g_pool;
@@ -179,6 +181,9 @@ Engine::Engine(int device) : device_(device) {
     d_ready_ = r.ready;
     front_cap_ = r.front_cap;
     ticket_base_ = r.ticket_base;
+    d_rows_ = r.d_rows;
+    h_rows_ = r.h_rows;
+    rows_cap_ = r.rows_cap;
     dev_bytes_ += (long long)(MAXBATCH * (BLOB_STRIDE + sizeof(HitPath))) +
                   front_cap_ * (long long)(sizeof(Cont) + sizeof(int));
 }
@@ -188,12 +193,6 @@ Engine::~Engine() {
     cudaStreamSynchronize(S_(stream_));
     free_eval();
     free_nccl();
-    cudaFree(d_base_);
-    cudaFree(d_B_);
-    cudaFree(d_fp_);
-    cudaFree(d_bound_);
-    cudaFree(d_d_);
-    cudaFree(d_u_);
     EngineRes r;
     r.device = device_;
     r.stream = stream_;
@@ -211,47 +210,61 @@ Engine::~Engine() {
     r.ready = d_ready_;
     r.front_cap = front_cap_;
     r.ticket_base = ticket_base_;
+    r.d_rows = d_rows_;
+    r.h_rows = h_rows_;
+    r.rows_cap = rows_cap_;
     std::lock_guard<std::mutex> lk(g_pool_mu);
     g_pool.push_back(r);
 }
 
 void Engine::upload_rows(const Model& M) {
     CK(cudaSetDevice(device_));
-    std::vector<double> base, B, fp, bound;
-    std::vector<int> d, u;
+    size_t n = 0;
+    for (const auto& rows : M.rows) n += rows.size();
+    n_rows_ = (int)n;
+    // one pooled allocation carved into the six SoA arrays, one staged upload
+    const size_t nn = std::max<size_t>(1, n);
+    const size_t bytes = nn * 40 + 256;
+    if (rows_cap_ < bytes) {
+        cudaFree(d_rows_);
+        if (h_rows_) cudaFreeHost(h_rows_);
+        d_rows_ = h_rows_ = nullptr;
+        dev_bytes_ -= (long long)rows_cap_;
+        rows_cap_ = 0;
+        CK(cudaMalloc(&d_rows_, bytes));
+        CK(cudaMallocHost(&h_rows_, bytes));
+        rows_cap_ = bytes;
+        dev_bytes_ += (long long)bytes;
+    }
+    char* h = static_cast<char*>(h_rows_);
+    double* hb = reinterpret_cast<double*>(h);
+    double* hB = hb + nn;
+    double* hf = hB + nn;
+    double* hbd = hf + nn;
+    int* hd = reinterpret_cast<int*>(hbd + nn);
+    int* hu = hd + nn;
+    size_t i = 0;
     for (const auto& rows : M.rows)
         for (const auto& r : rows) {
-            base.push_back(r.base);
-            B.push_back(r.B);
-            fp.push_back(r.fp);
-            bound.push_back(r.bound);
-            d.push_back(r.d);
-            u.push_back(r.u);
+            hb[i] = r.base;
+            hB[i] = r.B;
+            hf[i] = r.fp;
+            hbd[i] = r.bound;
+            hd[i] = r.d;
+            hu[i] = r.u;
+            ++i;
         }
-    n_rows_ = (int)base.size();
-    h2d_ += (long long)base.size() * 40;
-    size_t n = std::max<size_t>(1, base.size());
-    cudaFree(d_base_);
-    cudaFree(d_B_);
-    cudaFree(d_fp_);
-    cudaFree(d_bound_);
-    cudaFree(d_d_);
-    cudaFree(d_u_);
-    CK(cudaMalloc(&d_base_, n * 8));
-    CK(cudaMalloc(&d_B_, n * 8));
-    CK(cudaMalloc(&d_fp_, n * 8));
-    CK(cudaMalloc(&d_bound_, n * 8));
-    CK(cudaMalloc(&d_d_, n * 4));
-    CK(cudaMalloc(&d_u_, n * 4));
-    dev_bytes_ += (long long)n * 40;
-    if (!base.empty()) {
-        CK(cudaMemcpy(d_base_, base.data(), base.size() * 8, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(d_B_, B.data(), B.size() * 8, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(d_fp_, fp.data(), fp.size() * 8, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(d_bound_, bound.data(), bound.size() * 8, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(d_d_, d.data(), d.size() * 4, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(d_u_, u.data(), u.size() * 4, cudaMemcpyHostToDevice));
-    }
+    char* d = static_cast<char*>(d_rows_);
+    d_base_ = reinterpret_cast<double*>(d);
+    d_B_ = d_base_ + nn;
+    d_fp_ = d_B_ + nn;
+    d_bound_ = d_fp_ + nn;
+    d_d_ = reinterpret_cast<int*>(d_bound_ + nn);
+    d_u_ = d_d_ + nn;
+    cudaStream_t s = S_(stream_);
+    CK(cudaMemcpyAsync(d, h, nn * 40, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    h2d_ += (long long)n * 40;
 }
 
 // The cursor ring only has to hold the pieces in flight: donations happen when the queue

@@ -196,6 +196,8 @@ class Engine {
     void* ev1_ = nullptr;
     // device buffers
     double *d_base_ = nullptr, *d_B_ = nullptr, *d_fp_ = nullptr, *d_bound_ = nullptr;
+    void *d_rows_ = nullptr, *h_rows_ = nullptr;  // pooled: the SoA arrays live in d_rows_
+    size_t rows_cap_ = 0;
     int *d_d_ = nullptr, *d_u_ = nullptr;
     int n_rows_ = 0;
     void* d_blob_ = nullptr;  // MAXBATCH x (Spec | Ctl | Leaf | root Cont), BLOB_STRIDE apart

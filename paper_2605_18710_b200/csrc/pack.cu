@@ -9,7 +9,10 @@
 // surface grids.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstring>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -214,6 +217,43 @@ std::vector<GenPoint> generate_surfaces_device(const std::vector<GenWorkload>& w
     return res;
 }
 
+namespace {
+struct Arena {
+    int device = -1;
+    void *host = nullptr, *dev = nullptr, *stream = nullptr;
+    size_t cap = 0;
+};
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+std::mutex g_arena_mu;
+std::vector<Arena*> g_arenas;
+
+// The calling thread holds g_arena_mu while it uses the arena (pack_options_device).
+Arena& arena(int device, size_t bytes) {
+    Arena* a = nullptr;
+    for (Arena* x : g_arenas)
+        if (x->device == device) a = x;
+    if (!a) {
+        a = new Arena;
+        a->device = device;
+        cudaStream_t s;
+        CKP(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        a->stream = s;
+        g_arenas.push_back(a);
+    }
+    if (a->cap < bytes) {
+        if (a->host) cudaFreeHost(a->host);
+        if (a->dev) cudaFree(a->dev);
+        a->host = a->dev = nullptr;
+        a->cap = 0;
+        const size_t c = std::max(bytes, (size_t)1 << 20);
+        CKP(cudaMallocHost(&a->host, c));
+        CKP(cudaMalloc(&a->dev, c));
+        a->cap = c;
+    }
+    return *a;
+}
+}  // namespace
+
 std::vector<std::vector<PackedRow>> pack_options_device(const std::vector<PackInput>& mods, int G,
                                                         int L, double cap, int device,
                                                         long long* h2d_bytes,
@@ -222,6 +262,7 @@ std::vector<std::vector<PackedRow>> pack_options_device(const std::vector<PackIn
     const int M = (int)mods.size();
     std::vector<std::vector<PackedRow>> res(M);
     if (M == 0) return res;
+    std::lock_guard<std::mutex> lk(g_arena_mu);
     std::vector<PackSurf> hs(M);
     std::vector<double> lat, bw, mem;
     for (int m = 0; m < M; ++m) {
@@ -242,43 +283,46 @@ std::vector<std::vector<PackedRow>> pack_options_device(const std::vector<PackIn
     for (const auto& in : mods)
         if ((long long)L * (long long)in.dv.size() > PK_MAXROWS)
             throw std::runtime_error("quota_levels x d values exceed the packing kernel");
-    PackSurf* ds;
-    double *dl, *db, *dm;
-    int *dc, *derr;
-    PRow* dout;
-    const size_t npts = std::max<size_t>(1, lat.size());
-    CKP(cudaMalloc(&ds, sizeof(PackSurf) * M));
-    CKP(cudaMalloc(&dl, 8 * npts));
-    CKP(cudaMalloc(&db, 8 * npts));
-    CKP(cudaMalloc(&dm, 8 * npts));
-    CKP(cudaMalloc(&dc, sizeof(int) * M));
-    CKP(cudaMalloc(&derr, sizeof(int) * M));
-    CKP(cudaMalloc(&dout, sizeof(PRow) * PK_MAXROWS * M));
-    CKP(cudaMemcpy(ds, hs.data(), sizeof(PackSurf) * M, cudaMemcpyHostToDevice));
-    CKP(cudaMemcpy(dl, lat.data(), 8 * lat.size(), cudaMemcpyHostToDevice));
-    CKP(cudaMemcpy(db, bw.data(), 8 * bw.size(), cudaMemcpyHostToDevice));
-    CKP(cudaMemcpy(dm, mem.data(), 8 * mem.size(), cudaMemcpyHostToDevice));
-    CKP(cudaMemset(derr, 0, sizeof(int) * M));
-    if (h2d_bytes) *h2d_bytes += (long long)(sizeof(PackSurf) * M + 24 * lat.size());
-    k_pack_options<<<M, PK_THREADS>>>(ds, dl, db, dm, G, L, cap, dc, derr, dout);
+    // one staging arena per device (pinned host + device, grow-only, reused by every context
+    // created afterwards): one upload, one kernel, one read-back, one synchronisation
+    const size_t npts = lat.size();
+    const size_t o_surf = 0;
+    const size_t o_lat = align_up(o_surf + sizeof(PackSurf) * M);
+    const size_t o_bw = o_lat + 8 * npts;
+    const size_t o_mem = o_bw + 8 * npts;
+    const size_t in_bytes = align_up(o_mem + 8 * npts);
+    const size_t o_cnt = in_bytes;
+    const size_t o_err = o_cnt + sizeof(int) * M;
+    const size_t o_rows = align_up(o_err + sizeof(int) * M);
+    const size_t total = o_rows + sizeof(PRow) * PK_MAXROWS * M;
+    Arena& ar = arena(device, total);
+    char* h = static_cast<char*>(ar.host);
+    char* d = static_cast<char*>(ar.dev);
+    std::memcpy(h + o_surf, hs.data(), sizeof(PackSurf) * M);
+    std::memcpy(h + o_lat, lat.data(), 8 * npts);
+    std::memcpy(h + o_bw, bw.data(), 8 * npts);
+    std::memcpy(h + o_mem, mem.data(), 8 * npts);
+    cudaStream_t st = static_cast<cudaStream_t>(ar.stream);
+    CKP(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, st));
+    CKP(cudaMemsetAsync(d + o_err, 0, sizeof(int) * M, st));
+    if (h2d_bytes) *h2d_bytes += (long long)in_bytes;
+    k_pack_options<<<M, PK_THREADS, 0, st>>>(
+        reinterpret_cast<const PackSurf*>(d + o_surf), reinterpret_cast<const double*>(d + o_lat),
+        reinterpret_cast<const double*>(d + o_bw), reinterpret_cast<const double*>(d + o_mem), G, L,
+        cap, reinterpret_cast<int*>(d + o_cnt), reinterpret_cast<int*>(d + o_err),
+        reinterpret_cast<PRow*>(d + o_rows));
     CKP(cudaGetLastError());
+    CKP(cudaMemcpyAsync(h + o_cnt, d + o_cnt, total - o_cnt, cudaMemcpyDeviceToHost, st));
+    CKP(cudaStreamSynchronize(st));
     std::vector<int> counts(M), errs(M);
-    std::vector<PRow> rows((size_t)PK_MAXROWS * M);
-    CKP(cudaMemcpy(counts.data(), dc, sizeof(int) * M, cudaMemcpyDeviceToHost));
-    CKP(cudaMemcpy(errs.data(), derr, sizeof(int) * M, cudaMemcpyDeviceToHost));
-    CKP(cudaMemcpy(rows.data(), dout, sizeof(PRow) * rows.size(), cudaMemcpyDeviceToHost));
-    cudaFree(ds);
-    cudaFree(dl);
-    cudaFree(db);
-    cudaFree(dm);
-    cudaFree(dc);
-    cudaFree(derr);
-    cudaFree(dout);
+    std::memcpy(counts.data(), h + o_cnt, sizeof(int) * M);
+    std::memcpy(errs.data(), h + o_err, sizeof(int) * M);
+    const PRow* rows = reinterpret_cast<const PRow*>(h + o_rows);
     if (range_err) range_err->assign(errs.begin(), errs.end());
     for (int m = 0; m < M; ++m) {
         if (counts[m] < 0) throw std::runtime_error("too many candidate options for one module");
         for (int i = 0; i < counts[m]; ++i) {
-            const PRow& r = rows[(size_t)m * PK_MAXROWS + i];
+            const PRow& r = rows[(size_t)m * PK_MAXROWS + i];  // (arena: read before unlock)
             res[m].push_back(PackedRow{r.d, r.u, r.base, r.B, r.fp});
         }
     }
