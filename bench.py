@@ -94,10 +94,13 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()  # the first sample lands before the timed region starts
+            while not self.rows and time.time() - t0 < 3.0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -375,15 +378,15 @@ def main() -> None:
     barrier()
     pl.reset_counters()
     dev_ms = []
-    with Clocks(local) as clk:
-        for _ in range(args.steps):
-            flush_l2(torch, dev)
-            barrier()
-            pl.mark(0)
-            run_sample(pl)
-            pl.mark(1)
-            dev_ms.append(pl.marked_ms())
+    clk = Clocks(local).__enter__()  # sampled through both timed legs (sample and full solve)
+    for _ in range(args.steps):
+        flush_l2(torch, dev)
         barrier()
+        pl.mark(0)
+        run_sample(pl)
+        pl.mark(1)
+        dev_ms.append(pl.marked_ms())
+    barrier()
     ctr = pl.counters()
     t_max = max_over_ranks(sum(dev_ms))
     value = SAMPLE_LEAVES * args.steps / (t_max / 1000.0) if t_max > 0 else 0.0
@@ -423,6 +426,7 @@ def main() -> None:
         res = pl.solve()
         pl.mark(1)
         solve_ms.append(pl.marked_ms())
+    clk.__exit__(None, None, None)
     ttbp = max_over_ranks(statistics.median(solve_ms)) / 1000.0
     if not headline:
         # no reference-equivalent count for the other configs: device leaves per second
