@@ -134,3 +134,27 @@ def test_evaluate_edge_shapes_and_errors():
     with pytest.raises(mosaic.OracleTooLargeError):
         pl.evaluate(big, gpus, np.array([0, 65], dtype=np.int64), np.zeros(1))
     pl.close()
+
+
+def test_evaluate_many_entries_deferred_path():
+    # > 32 entries: the CTA kernel defers the allocation to the warp kernel; both paths must
+    # agree with the per-call row path (other quota granularity: the first evaluator kernel)
+    pl = planner("cfg5")
+    L = pl.quota_levels
+    rng = np.random.default_rng(5)
+    allocs_a, allocs_b = [], []
+    for n_ent in (31, 32, 33, 40, 64):
+        ea, eb = [], []
+        for i in range(n_ent):
+            m = int(rng.integers(0, 8))
+            d = int(rng.choice([1, 2, 4, 8]))
+            u = int(rng.integers(8, L + 1))
+            g = sorted(int(x) for x in rng.choice(128, size=d, replace=False))
+            ea.append(mosaic.Entry(m, mosaic.DeploymentOption(d, u, L), g))
+            eb.append(mosaic.Entry(m, mosaic.DeploymentOption(d, 2 * u, 2 * L), g))
+        allocs_a.append(mosaic.StageAllocation(ea))
+        allocs_b.append(mosaic.StageAllocation(eb))
+    sa, ra = pl.stage_time(allocs_a, with_rectified=True)
+    sb, rb = pl.stage_time(allocs_b, with_rectified=True)
+    assert sa == sb and ra == rb
+    pl.close()
