@@ -478,7 +478,7 @@ int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value) {
         else if (k == "generic_kernel") t.generic_kernel = v != 0;
         else if (k == "shard_level") t.shard_level = (int)v;
         else if (k == "ring_per_walker") t.ring_per_walker = (int)std::max(1LL, v);
-        else if (k == "trace") t.trace = v != 0;
+        else if (k == "trace") t.trace = (int)v;  // 1 per search, 2 per launch
         else if (k == "spec_k") t.spec_k = (int)v;
         else if (k == "restart_k") t.restart_k = (int)v;
         else if (k == "share_rank") t.share_rank = (int)v;

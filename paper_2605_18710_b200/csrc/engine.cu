@@ -11,6 +11,7 @@
 //              rows); the common case runs K1 on the ABI layout (eval.cu).
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <climits>
 #include <cstdlib>
 #include <cstdio>
@@ -367,6 +368,7 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
                           size_t smem, long long grid_cap, std::vector<SearchResult>& out) {
     cudaStream_t s = S_(stream_);
     const int n = (int)(b1 - b0);
+    const auto c0 = std::chrono::steady_clock::now();
     Rows R{d_base_, d_B_, d_fp_, d_bound_, d_d_, d_u_};
     char* pin = reinterpret_cast<char*>(h_pin_);
     HitPath* hbest = reinterpret_cast<HitPath*>(h_best_);
@@ -496,7 +498,9 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
                          BLOB_STRIDE, BLOB_ROOT - BLOB_CTL, n, cudaMemcpyDeviceToHost, s));
     d2h_ += (long long)n * (BLOB_ROOT - BLOB_CTL);
     CK(cudaEventRecord((cudaEvent_t)ev1_, s));
+    const auto c1 = std::chrono::steady_clock::now();
     CK(cudaEventSynchronize((cudaEvent_t)ev1_));
+    const auto c2 = std::chrono::steady_clock::now();
     CK(cudaGetLastError());
     float kms = 0, ms = 0;
     CK(cudaEventElapsedTime(&kms, (cudaEvent_t)evk0_, (cudaEvent_t)evk1_));
@@ -534,7 +538,7 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         st.leaves += (long long)hc->leaves;
         ++st.searches;
         alg_bytes_ += (long long)hc->leaves * 24LL * S.k;  // k option rows x 3 fp64 per leaf
-        if (tune_.trace)
+        if (tune_.trace == 1)
             std::fprintf(stderr, "[mosaic] %s k=%d thr=%.17g batch=%d ctas=%d kernel=%.3fms total=%.3fms "
                                  "nodes=%llu leaves=%llu %s\n",
                          S.mode == MODE_MIN ? "MIN  " : "FIRST", S.k,
@@ -542,6 +546,13 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
                          hc->leaves, res.found ? "hit" : (res.aborted ? "restart" : ""));
     }
     ticket_base_ = tmax + 1;
+    if (tune_.trace == 2) {
+        const auto c3 = std::chrono::steady_clock::now();
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        std::fprintf(stderr, "[mosaic] launch of %d: host prep %.1f us, wait %.1f us (stream %.1f us, "
+                             "kernel %.1f us), post %.1f us\n",
+                     n, us(c0, c1), us(c1, c2), 1e3 * ms, 1e3 * kms, us(c2, c3));
+    }
     // ranks must leave every search with the same answer (they replay the same control flow
     // and all-gather once per launch): merge after the local results are complete
     if (sharded()) {
