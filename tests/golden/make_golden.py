@@ -149,6 +149,49 @@ def stime_edge() -> None:
     dump("stime_edge.json", out)
 
 
+def stime_large_g() -> None:
+    """K1 on clusters beyond 128 GPUs (the shared-atomics path of k_evaluate): random
+    allocations of random instances at G = 256, 512, 1024, scored by the reference."""
+    rng = random.Random(4242)
+    out = []
+    for inst, n, g in [("random:5:4:256", 4, 256), ("random:6:5:512", 5, 512),
+                       ("random:7:3:1024", 3, 1024)]:
+        opts = ref(inst, "options")["modules"]
+        for t in range(30):
+            k = rng.randint(1, n)
+            mods = sorted(rng.sample(range(n), k))
+            ents = []
+            for m in mods:
+                rows = opts[m]["rows"]
+                d, u = rows[rng.randrange(len(rows))][:2]
+                gp = sorted(rng.sample(range(g), d))
+                ents.append((m, d, u, gp))
+            spec = ";".join(f"{m}:{d}:{u}:{'.'.join(map(str, gp))}" for m, d, u, gp in ents)
+            for extra in ([], ["noself"]):
+                r = ref(inst, "stime", spec, *extra)
+                out.append({"inst": inst, "extra": extra, "entries": ents, "t": r.get("t")})
+    dump("stime_large_g.json", out)
+
+
+def large_clusters() -> None:
+    """stage_eval (and solve where the CPU finishes in 120 s) beyond 128 GPUs: random
+    instances at G = 256 and 512 (blocks stay <= 128 per level for these stages)."""
+    out = []
+    for inst, n in [("random:5:4:256", 4), ("random:9:3:512", 3)]:
+        for mask in range(1, 1 << n):
+            if bin(mask).count("1") > 2:
+                continue
+            try:
+                out.append(ref(inst, "stage", str(mask), timeout=120))
+            except subprocess.TimeoutExpired:
+                pass
+        try:
+            out.append(ref(inst, "solve", timeout=120))
+        except subprocess.TimeoutExpired:
+            pass
+    dump("large_clusters.json", out)
+
+
 def random_solves() -> None:
     """Full GAHC solves of medium random instances (4-6 modules, 16-64 GPUs, L=10): the
     regime where device searches use shared walkers and GAHC rounds are batched.  Instances

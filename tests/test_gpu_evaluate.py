@@ -158,3 +158,18 @@ def test_evaluate_many_entries_deferred_path():
     sb, rb = pl.stage_time(allocs_b, with_rectified=True)
     assert sa == sb and ra == rb
     pl.close()
+
+
+def test_large_clusters_match_reference_bits():
+    # G = 256 / 512 / 1024: the shared-memory bitmap path of k_evaluate
+    rows = load_golden("stime_large_g.json")
+    groups = {}
+    for row in rows:
+        groups.setdefault((row["inst"], tuple(row["extra"])), []).append(row)
+    for (inst, extra), rs in groups.items():
+        pl = planner(inst, extra=list(extra))
+        allocs = [mosaic.StageAllocation(
+            [mosaic.Entry(m, mosaic.DeploymentOption(d, u, pl.quota_levels), gp)
+             for m, d, u, gp in r["entries"]]) for r in rs]
+        assert pl.stage_time(allocs) == [hexf(r["t"]) for r in rs], (inst, extra)
+        pl.close()
