@@ -546,7 +546,7 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
                          hc->leaves, res.found ? "hit" : (res.aborted ? "restart" : ""));
     }
     ticket_base_ = tmax + 1;
-    if (tune_.trace == 2) {
+    if (tune_.trace >= 2) {
         const auto c3 = std::chrono::steady_clock::now();
         auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
         std::fprintf(stderr, "[mosaic] launch of %d: host prep %.1f us, wait %.1f us (stream %.1f us, "

@@ -78,6 +78,23 @@ Planner::Planner(Problem P, int device) : P_(std::move(P)) {
         M_.row_off.push_back(off);
         off += (int)rows.size();
     }
+    mg::build_index(M_);
+    tau_mins_.assign(P_.modules.size(), {0.0, 0.0});
+    for (size_t m = 0; m < P_.modules.size(); ++m) {
+        double lo = std::numeric_limits<double>::max();
+        double solo = std::numeric_limits<double>::max();
+        for (const auto& c : opts_[m]) {
+            double bound = c.base;
+            if (P_.im.non_negative()) {
+                bound += P_.im.e1;
+                if (P_.include_self) bound += P_.im.e2 * c.B;
+            }
+            lo = std::min(lo, bound);
+            double delta = P_.include_self ? P_.im.delta(c.B, c.B) : P_.im.delta(0.0, 0.0);
+            solo = std::min(solo, c.base + delta);
+        }
+        tau_mins_[m] = {lo, solo};
+    }
     eng_ = std::make_unique<mg::Engine>(device);
     eng_->upload_rows(M_);
 }
@@ -166,7 +183,7 @@ bool Planner::first_leaf(const std::vector<int>& order, bool filter, double thet
     mg::HitPath hp;
     Leaf sl;
     const bool seeded = seed && make_seed(*seed, order, filter, theta, seed_value, hp, sl);
-    if (seed && eng_->tuning().trace)
+    if (seed && eng_->tuning().trace == 1)
         std::fprintf(stderr, "[mosaic] FIRST seed %s (theta=%.17g value=%.17g)\n",
                      seeded ? "applied" : "rejected", theta, seed_value);
     mg::SearchResult r = eng_->search(S, POS_INF, 0.0, st, seeded ? &hp : nullptr,
@@ -244,7 +261,7 @@ bool Planner::prep_first(const std::vector<int>& order, bool filter, double thet
     op.req = mg::BatchReq{};
     if (!mg::build_spec(M_, q, op.req.S)) return false;
     const bool seeded = seed && make_seed(*seed, order, filter, theta, seed_value, op.hp, op.sl);
-    if (seed && eng_->tuning().trace)
+    if (seed && eng_->tuning().trace == 1)
         std::fprintf(stderr, "[mosaic] FIRST seed %s (theta=%.17g value=%.17g)\n",
                      seeded ? "applied" : "rejected", theta, seed_value);
     op.req.ub = POS_INF;
@@ -261,15 +278,11 @@ bool Planner::prep_min(const std::vector<int>& mods, double ub, SearchOp& op, mg
     const double thp = ub >= POS_INF ? POS_INF : ub * (1.0 - mg::TIE_EPS);
     std::vector<std::pair<int, int>> cnt;
     for (int m : mods) {
-        int c = 0;
-        for (const auto& r : M_.rows[m]) {
-            double lb = r.base;
-            if (M_.nonneg()) {
-                lb = r.base + M_.e1;
-                if (M_.include_self) lb = lb + M_.e2 * r.B;
-            }
-            if (!M_.nonneg() || lb <= thp) ++c;
-        }
+        // lb = (base + e1) + e2 B is exactly the row's filter bound with non-negative
+        // coefficients: count rows with bound <= thp in the bound-sorted index
+        const auto& b = M_.index[m].bound;
+        const int c = M_.nonneg() ? (int)(std::upper_bound(b.begin(), b.end(), thp) - b.begin())
+                                  : (int)M_.rows[m].size();
         cnt.push_back({c, m});
     }
     std::stable_sort(cnt.begin(), cnt.end());
@@ -307,22 +320,12 @@ StageJob Planner::stage_eval_job(uint64_t mask, StageResult* out) {
     }
     const Interference& im = P_.im;
     const bool nonneg = im.non_negative();
+    // tau_lo = max_m min bound, tau_hi = sum_m min solo rectified latency (stage_eval.hpp:
+    // 318-335, 290-295): per-module minima computed once per problem (tau_mins_)
     double tau_lo = 0.0, tau_hi = 0.0;
     for (int m : mods) {
-        double lo = std::numeric_limits<double>::max();
-        double solo = std::numeric_limits<double>::max();
-        for (const auto& c : opts_[m]) {
-            double bound = c.base;
-            if (nonneg) {
-                bound += im.e1;
-                if (P_.include_self) bound += im.e2 * c.B;
-            }
-            lo = std::min(lo, bound);
-            double delta = P_.include_self ? im.delta(c.B, c.B) : im.delta(0.0, 0.0);
-            solo = std::min(solo, c.base + delta);
-        }
-        if (nonneg) tau_lo = std::max(tau_lo, lo);
-        tau_hi += solo;
+        if (nonneg) tau_lo = std::max(tau_lo, tau_mins_[m].first);
+        tau_hi += tau_mins_[m].second;
     }
     bool have_T = false;
     double Tstar = POS_INF;
@@ -341,9 +344,8 @@ StageJob Planner::stage_eval_job(uint64_t mask, StageResult* out) {
         std::vector<std::pair<int, int>> cnt_;                                             \
         bool none_ = false;                                                                \
         for (int m_ : mods) {                                                              \
-            int c_ = 0;                                                                    \
-            for (const auto& r_ : M_.rows[m_])                                             \
-                if (r_.bound <= th_) ++c_;                                                 \
+            const auto& b_ = M_.index[m_].bound; /* rows with bound <= th, sorted */       \
+            const int c_ = (int)(std::upper_bound(b_.begin(), b_.end(), th_) - b_.begin()); \
             if (c_ == 0) none_ = true;                                                     \
             cnt_.push_back({c_, m_});                                                      \
         }                                                                                  \

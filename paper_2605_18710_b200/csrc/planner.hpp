@@ -205,6 +205,8 @@ class Planner {
     std::unordered_map<uint64_t, StageResult> cache_;
     std::vector<uint64_t> cache_order_;
     int rate_tables_ = 0;  // 0 not built yet, 1 built, -1 too large for this problem
+    // per module: (min filter bound, min solo rectified latency) — stage_eval's tau_lo / tau_hi
+    std::vector<std::pair<double, double>> tau_mins_;
     // stage_eval results computed speculatively for GAHC candidates the reference prunes
     // (not in the EvalCache; moved there when the reference would evaluate them)
     std::unordered_map<uint64_t, StageResult> spec_;

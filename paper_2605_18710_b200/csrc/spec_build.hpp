@@ -20,6 +20,17 @@ struct OptRow {
     double base, B, fp, bound;
 };
 
+// Per module, the rows re-sorted by filter bound with prefix aggregates: with non-negative
+// coefficients a row is usable at threshold t iff bound <= t, so the per-level summary
+// build_spec needs (min quota demand, min solo bandwidth, all options full-width) is one
+// binary search instead of a scan over the module's options.
+struct BoundIndex {
+    std::vector<double> bound;   // ascending
+    std::vector<int> min_dem;    // prefix min of d*u
+    std::vector<double> min_B;   // prefix min of B
+    std::vector<int> not_full;   // prefix count of d != G
+};
+
 struct Model {
     int G = 1, L = 10;
     double cap = 80e9, e1 = 0, e2 = 0, e3 = 0;
@@ -27,7 +38,30 @@ struct Model {
     bool nonneg() const { return e1 >= 0 && e2 >= 0 && (additive || e3 >= 0); }
     std::vector<std::vector<OptRow>> rows;  // per module, candidate_options order
     std::vector<int> row_off;               // per module offset into the flat table
+    std::vector<BoundIndex> index;          // build_index(); empty: build_spec scans
 };
+
+inline void build_index(Model& M) {
+    M.index.assign(M.rows.size(), {});
+    for (size_t m = 0; m < M.rows.size(); ++m) {
+        std::vector<const OptRow*> v;
+        for (const auto& r : M.rows[m]) v.push_back(&r);
+        std::stable_sort(v.begin(), v.end(),
+                         [](const OptRow* a, const OptRow* b) { return a->bound < b->bound; });
+        BoundIndex& ix = M.index[m];
+        int dem = INT32_MAX, nf = 0;
+        double bm = POS_INF;
+        for (const OptRow* r : v) {
+            dem = std::min(dem, r->d * r->u);
+            bm = std::min(bm, r->B);
+            nf += r->d != M.G;
+            ix.bound.push_back(r->bound);
+            ix.min_dem.push_back(dem);
+            ix.min_B.push_back(bm);
+            ix.not_full.push_back(nf);
+        }
+    }
+}
 
 // Filter bound exactly as FeasibilitySearch::run computes it (stage_eval.hpp:122-127).
 inline double filter_bound(const Model& M, double base, double B) {
@@ -79,7 +113,30 @@ inline bool build_spec(const Model& M, const SearchReq& q, Spec& S) {
 
     std::vector<double> bmin(k, 1.0);
     std::vector<int> forced(k, 1), dmin(k, 0);
-    for (int l = 0; l < k; ++l) {
+    // fast path (non-negative coefficients, index built): the option list stops at the first
+    // row with base + e1 above the threshold (rows are sorted by base latency); a row is usable
+    // iff its bound (= base + e1 [+ e2 B]) is within the threshold — the scan below, exactly
+    const bool fast = S.nonneg && !M.index.empty();
+    const double t_stop = q.use_filter ? q.theta : S.thp;
+    for (int l = 0; l < k && fast; ++l) {
+        const int m = q.level_module[l];
+        const auto& rows = M.rows[m];
+        const BoundIndex& ix = M.index[m];
+        S.lvl_off[l] = M.row_off[m];
+        int lo = 0, hi = (int)rows.size();  // first row with base + e1 > t_stop
+        while (lo < hi) {
+            const int mid = (lo + hi) / 2;
+            if (rows[mid].base + M.e1 > t_stop) hi = mid; else lo = mid + 1;
+        }
+        S.lvl_n[l] = lo;
+        const int c = (int)(std::upper_bound(ix.bound.begin(), ix.bound.end(), t_stop) -
+                            ix.bound.begin());
+        if (c == 0) return false;
+        dmin[l] = ix.min_dem[c - 1];
+        bmin[l] = std::min(1.0, std::max(0.0, ix.min_B[c - 1]));
+        forced[l] = ix.not_full[c - 1] == 0 ? 1 : 0;
+    }
+    for (int l = 0; l < k && !fast; ++l) {
         const int m = q.level_module[l];
         const auto& rows = M.rows[m];
         S.lvl_off[l] = M.row_off[m];

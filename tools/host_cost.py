@@ -13,7 +13,7 @@ sets = [[i for i in range(8) if m["mask"] >> i & 1] for m in S["masks"]]
 pl = mosaic.Planner.from_spec("cfg5", device=0)
 for _ in range(3):
     pl.search(sets, times_only=True)
-pl.set_tuning(trace=1)
+pl.set_tuning(trace=3)
 for _ in range(3):
     t0 = time.perf_counter()
     pl.search(sets, times_only=True)
