@@ -523,7 +523,7 @@ StageJob Planner::exact_stage_job(uint64_t mask, StageResult* out) {
 
 // Advance every job to its next device search; run each wave of pending searches as one
 // batched launch; repeat until all jobs are done.  The first exception is rethrown.
-void Planner::run_jobs(std::vector<StageJob>& jobs) {
+void Planner::run_jobs(std::vector<StageJob>& jobs, std::vector<char>* failed) {
     const bool trace = eng_->tuning().trace;
     double t_host = 0.0, t_dev = 0.0, t0 = now_s();
     for (auto& j : jobs) j.h.resume();
@@ -556,18 +556,24 @@ void Planner::run_jobs(std::vector<StageJob>& jobs) {
     if (trace)
         std::fprintf(stderr, "[mosaic] batch of %zu: %d waves, host %.3f ms, launches %.3f ms\n",
                      jobs.size(), waves, 1e3 * t_host, 1e3 * t_dev);
+    if (failed) {  // tolerant: report which jobs threw instead of rethrowing
+        failed->assign(jobs.size(), 0);
+        for (size_t i = 0; i < jobs.size(); ++i) (*failed)[i] = jobs[i].h.promise().exc != nullptr;
+        return;
+    }
     for (auto& j : jobs)
         if (j.h.promise().exc) std::rethrow_exception(j.h.promise().exc);
 }
 
-std::vector<StageResult> Planner::stage_batch(const std::vector<uint64_t>& masks, bool exact) {
+std::vector<StageResult> Planner::stage_batch(const std::vector<uint64_t>& masks, bool exact,
+                                              std::vector<char>* failed) {
     std::vector<StageResult> out(masks.size());
     std::vector<StageJob> jobs;
     jobs.reserve(masks.size());
     for (size_t i = 0; i < masks.size(); ++i)
         jobs.push_back(exact ? exact_stage_job(masks[i], &out[i])
                              : stage_eval_job(masks[i], &out[i]));
-    run_jobs(jobs);
+    run_jobs(jobs, failed);
     return out;
 }
 
@@ -723,8 +729,12 @@ void Planner::speculate(const std::vector<uint64_t>& masks, PlanResult& pr) {
             std::find(todo.begin(), todo.end(), m) == todo.end())
             todo.push_back(m);
     if (todo.empty()) return;
-    std::vector<StageResult> rs = stage_batch(todo, false);
+    // a candidate whose computation fails is simply not pre-computed: if the reference
+    // evaluates it, the sequential loop recomputes it and raises exactly there
+    std::vector<char> failed;
+    std::vector<StageResult> rs = stage_batch(todo, false, &failed);
     for (size_t i = 0; i < todo.size(); ++i) {
+        if (failed[i]) continue;
         pr.st.nodes += rs[i].st.nodes;
         pr.st.leaves += rs[i].st.leaves;
         pr.st.searches += rs[i].st.searches;

@@ -132,7 +132,8 @@ class Planner {
     StageResult exact_stage(uint64_t mask);
     // Batched (mosaic_gpu_search): the module sets' computations advance together, one launch
     // per wave of device searches.  exact = ExactStageSolver semantics, else stage_eval.
-    std::vector<StageResult> stage_batch(const std::vector<uint64_t>& masks, bool exact);
+    std::vector<StageResult> stage_batch(const std::vector<uint64_t>& masks, bool exact,
+                                         std::vector<char>* failed = nullptr);
     StageResult feasible(uint64_t mask, double tau);
     PlanResult solve();
     // validate_plan (core.hpp:281-351) with the footprint oracle; "" when valid, else the
@@ -176,7 +177,7 @@ class Planner {
     bool ensure_rate_tables();  // false when they would not fit (then the row path is used)
     StageJob stage_eval_job(uint64_t mask, StageResult* out);
     StageJob exact_stage_job(uint64_t mask, StageResult* out);
-    void run_jobs(std::vector<StageJob>& jobs);
+    void run_jobs(std::vector<StageJob>& jobs, std::vector<char>* failed = nullptr);
     // FIRST probe request (false: some level has no usable option, no leaf can exist)
     bool prep_first(const std::vector<int>& order, bool filter, double theta, SearchOp& op,
                     mg::SearchStats& st, const std::vector<Entry>* seed = nullptr,
