@@ -174,6 +174,10 @@ struct WalkLayout {
 // DFS state of one walker.  The header is fixed; the arrays it points to are carved
 // from shared memory right behind it, sized for the stage at hand (walk_layout).
 struct Walk {
+    // the chosen option's row per level, cached in shared memory when the level's option is
+    // set (sel_set): block statistics and contributions read it instead of the option table
+    double sB[MAXK], sBase[MAXK], sFp[MAXK];
+    int sU[MAXK], sDU[MAXK];
     uint16_t opt[MAXK];
     int16_t oc[MAXK];
     int16_t oe[MAXK];  // option range end per level (exclusive)
@@ -258,8 +262,9 @@ MG_HD double envelope(const Spec& S, int j, double P) {
 }
 
 // Exact contribution of one GPU block with resident levels `mask` (all k options set):
-// max over residents m of base_m + delta(residents), module-index order sums.
-MG_HD double contrib(const Spec& S, const Rows& R, const uint16_t* opt, unsigned mask) {
+// max over residents m of base_m + delta(residents), module-index order sums.  The chosen
+// options' rows come from the walk's per-level cache (Walk::sB / sBase).
+MG_HD double contrib(const Spec& S, const Walk& w, unsigned mask) {
     if (!mask) return NEG_INF;
     if (MG_SELF(S)) {
         double s = 0.0, p = 1.0, mb = NEG_INF;
@@ -267,11 +272,10 @@ MG_HD double contrib(const Spec& S, const Rows& R, const uint16_t* opt, unsigned
         for (int pos = 0; pos < S.k; ++pos) {
             int l = S.pos_lvl[pos];
             if (!(mask >> l & 1u)) continue;
-            int r = S.lvl_off[l] + opt[l];
-            double b = R.B[r];
+            double b = w.sB[l];
             s = s + b;
             p = p * b;
-            double ba = R.base[r];
+            double ba = w.sBase[l];
             mb = ba > mb ? ba : mb;
         }
         double dl = S.e1 + S.e2 * s;
@@ -289,7 +293,7 @@ MG_HD double contrib(const Spec& S, const Rows& R, const uint16_t* opt, unsigned
         for (int pos2 = 0; pos2 < S.k; ++pos2) {
             int l2 = S.pos_lvl[pos2];
             if (l2 == l || !(mask >> l2 & 1u)) continue;
-            double b = R.B[S.lvl_off[l2] + opt[l2]];
+            double b = w.sB[l2];
             s = s + b;
             p = p * b;
             ++n;
@@ -297,28 +301,29 @@ MG_HD double contrib(const Spec& S, const Rows& R, const uint16_t* opt, unsigned
         if (n == 0) p = 0.0;
         double dl = S.e1 + S.e2 * s;
         dl = dl + (MG_ADD(S) ? 0.0 : S.e3 * p);
-        double v = R.base[S.lvl_off[l] + opt[l]] + dl;
+        double v = w.sBase[l] + dl;
         best = v > best ? v : best;
     }
     return best;
 }
 
 // contrib() with the option of level `jl` replaced by `ol` (lanes evaluating different
-// last-level options against the same shared walk).
-MG_HD double contrib_o(const Spec& S, const Rows& R, const uint16_t* opt, unsigned mask, int jl,
+// last-level options against the same shared walk): level jl's row from the table.
+MG_HD double contrib_o(const Spec& S, const Rows& R, const Walk& w, unsigned mask, int jl,
                        int ol) {
     if (!mask) return NEG_INF;
+    const int ro = S.lvl_off[jl] + ol;
+    const double oB = R.B[ro], oBase = R.base[ro];
     if (MG_SELF(S)) {
         double s = 0.0, p = 1.0, mb = NEG_INF;
         #pragma unroll 1
         for (int pos = 0; pos < S.k; ++pos) {
             int l = S.pos_lvl[pos];
             if (!(mask >> l & 1u)) continue;
-            int r = S.lvl_off[l] + (l == jl ? ol : opt[l]);
-            double b = R.B[r];
+            double b = l == jl ? oB : w.sB[l];
             s = s + b;
             p = p * b;
-            double ba = R.base[r];
+            double ba = l == jl ? oBase : w.sBase[l];
             mb = ba > mb ? ba : mb;
         }
         double dl = S.e1 + S.e2 * s;
@@ -336,7 +341,7 @@ MG_HD double contrib_o(const Spec& S, const Rows& R, const uint16_t* opt, unsign
         for (int pos2 = 0; pos2 < S.k; ++pos2) {
             int l2 = S.pos_lvl[pos2];
             if (l2 == l || !(mask >> l2 & 1u)) continue;
-            double b = R.B[S.lvl_off[l2] + (l2 == jl ? ol : opt[l2])];
+            double b = l2 == jl ? oB : w.sB[l2];
             s = s + b;
             p = p * b;
             ++n;
@@ -344,7 +349,7 @@ MG_HD double contrib_o(const Spec& S, const Rows& R, const uint16_t* opt, unsign
         if (n == 0) p = 0.0;
         double dl = S.e1 + S.e2 * s;
         dl = dl + (MG_ADD(S) ? 0.0 : S.e3 * p);
-        double v = R.base[S.lvl_off[l] + (l == jl ? ol : opt[l])] + dl;
+        double v = (l == jl ? oBase : w.sBase[l]) + dl;
         best = v > best ? v : best;
     }
     return best;
@@ -379,10 +384,9 @@ MG_HD int opt_test(const Spec& S, const Rows& R, int r, double thr) {
 }
 
 // Stats of a block (levels < nlev in `mask`), accumulated in placement order like
-// FeasibilitySearch::push_module (stage_eval.hpp:224-229).
-MG_HD void block_stats(const Spec& S, const Rows& R, const uint16_t* opt, unsigned mask,
-                       int nlev, int& units, double& mem, double& sum, double& mb,
-                       double& P, double& mbx) {
+// FeasibilitySearch::push_module (stage_eval.hpp:224-229), from the walk's row cache.
+MG_HD void block_stats(const Spec& S, const Walk& w, unsigned mask, int nlev, int& units,
+                       double& mem, double& sum, double& mb, double& P, double& mbx) {
     units = 0;
     mem = 0.0;
     sum = 0.0;
@@ -392,16 +396,27 @@ MG_HD void block_stats(const Spec& S, const Rows& R, const uint16_t* opt, unsign
     #pragma unroll 1
     for (int l = 0; l < nlev; ++l) {
         if (!(mask >> l & 1u)) continue;
-        int r = S.lvl_off[l] + opt[l];
-        units += R.u[r];
-        mem = mem + R.fp[r];
-        sum = sum + R.B[r];
-        P = P * R.B[r];
-        double ba = R.base[r];
+        units += w.sU[l];
+        mem = mem + w.sFp[l];
+        const double b = w.sB[l];
+        sum = sum + b;
+        P = P * b;
+        double ba = w.sBase[l];
         mb = ba > mb ? ba : mb;
-        double bx = ba - S.e2 * R.B[r];
+        double bx = ba - S.e2 * b;
         mbx = bx > mbx ? bx : mbx;
     }
+}
+
+// Set level l's option (lane 0 only) and cache its row for the block statistics.
+MG_HD void sel_set(const Spec& S, const Rows& R, Walk& w, int l, int o) {
+    const int r = S.lvl_off[l] + o;
+    w.opt[l] = (uint16_t)o;
+    w.sB[l] = R.B[r];
+    w.sBase[l] = R.base[r];
+    w.sFp[l] = R.fp[r];
+    w.sU[l] = R.u[r];
+    w.sDU[l] = R.d[r] * R.u[r];
 }
 
 // -1: path H precedes the walk's leaf path (levels 0..j), +1 follows it, 0 equal.

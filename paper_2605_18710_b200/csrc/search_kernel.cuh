@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
     __syncwarp();
     unsigned long long nodes = 0, leaves = 0;
     if (solo) {
-        load_cont_warp(*root, w, MG_MODE(S) == MODE_FIRST);
+        load_cont_warp(S, R, *root, w, MG_MODE(S) == MODE_FIRST);
         WarpHooks h;
         h.ctl = ctl;
         h.mode = MG_MODE(S);
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
         const long long slot = (long long)((unsigned long long)ticket % ctl->q_cap);
         __threadfence();
         const Cont& piece = ticket + 1 == ready0 ? *root : Q[slot];
-        load_cont_warp(piece, w, MG_MODE(S) == MODE_FIRST);
+        load_cont_warp(S, R, piece, w, MG_MODE(S) == MODE_FIRST);
         WarpHooks h;
         h.ctl = ctl;
         h.mode = MG_MODE(S);

@@ -40,7 +40,7 @@ __device__ __forceinline__ void parent_stats_warp(const Spec& S, const Rows& R, 
     const int o0 = w.loff[j];
     #pragma unroll 1
     for (int b = lane_id(); b < w.nb[j]; b += 32)
-        block_stats(S, R, w.opt, w.bmk[o0 + b], j, w.pu[b], w.pm[b], w.psum[b], w.pmb[b], w.pP[b],
+        block_stats(S, w, w.bmk[o0 + b], j, w.pu[b], w.pm[b], w.psum[b], w.pmb[b], w.pP[b],
                     MG_SELF(S) ? mbx_unused : w.pmx[b]);
     __syncwarp();
 }
@@ -222,7 +222,7 @@ __device__ __forceinline__ bool lane_last_feasible(const Spec& S, const Rows& R,
         const bool rok = le ? rv <= t : rv < t;
         bool tok = false;
         if (w.pu[b] + uu <= S.L && !(w.pm[b] + ff > S.cap_slack)) {
-            const double tv = contrib_o(S, R, w.opt, w.bmk[o0 + b] | (1u << j), j, o);
+            const double tv = contrib_o(S, R, w, w.bmk[o0 + b] | (1u << j), j, o);
             tok = le ? tv <= t : tv < t;
         }
         if (rok) {
@@ -262,7 +262,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
     bool rest_ready = !MG_SELF(S);
     if (rest_ready) {
         #pragma unroll 1
-        for (int b = lane; b < nb; b += 32) w.cs[b] = contrib(S, R, w.opt, w.bmk[o0 + b]);
+        for (int b = lane; b < nb; b += 32) w.cs[b] = contrib(S, w, w.bmk[o0 + b]);
         __syncwarp();
     }
     const bool fm = MG_MODE(S) == MODE_FIRST;
@@ -328,7 +328,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
         }
         if (!rest_ready && __any_sync(FULLW, valid && pass)) {
             #pragma unroll 1
-            for (int b = lane; b < nb; b += 32) w.cs[b] = contrib(S, R, w.opt, w.bmk[o0 + b]);
+            for (int b = lane; b < nb; b += 32) w.cs[b] = contrib(S, w, w.bmk[o0 + b]);
             __syncwarp();
             rest_ready = true;
         }
@@ -348,7 +348,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
                             if (rv < hiv && rv > c) c = rv;
                             if (w.pu[b] + uu <= S.L && !(w.pm[b] + ff > S.cap_slack)) {
                                 const double tv =
-                                    contrib_o(S, R, w.opt, w.bmk[o0 + b] | (1u << j), j, o);
+                                    contrib_o(S, R, w, w.bmk[o0 + b] | (1u << j), j, o);
                                 if (tv < hiv && tv > c) c = tv;
                             }
                         }
@@ -383,7 +383,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
             const int dd2 = R.d[r], uu2 = R.u[r];
             const double ff2 = R.fp[r];
             if (lane == 0) {
-                w.opt[j] = (uint16_t)ow;
+                sel_set(S, R, w, j, ow);
                 w.oc[j] = (int16_t)ow;
             }
             __syncwarp();
@@ -392,7 +392,7 @@ __device__ bool last_level_batch(const Spec& S, const Rows& R, Walk& w, int j, i
             for (int b = lane; b < nb; b += 32) {
                 const bool el = w.pu[b] + uu2 <= S.L && !(w.pm[b] + ff2 > S.cap_slack);
                 w.hi[o0 + b] = el ? w.bsz[o0 + b] : 0;
-                w.cb[b] = el ? contrib(S, R, w.opt, w.bmk[o0 + b] | (1u << j)) : POS_INF;
+                w.cb[b] = el ? contrib(S, w, w.bmk[o0 + b] | (1u << j)) : POS_INF;
             }
             __syncwarp();
             const double tfill = fm ? S.theta : __shfl_sync(FULLW, val, win);
@@ -575,7 +575,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
             }
             if (lane == 0) {
                 w.oc[j] = (int16_t)o;
-                w.opt[j] = (uint16_t)o;
+                sel_set(S, R, w, j, o);
             }
             __syncwarp();
             const int r = off + o;
@@ -681,8 +681,8 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                 #pragma unroll 1
                 for (int b = lane; b < nb; b += 32) {
                     const unsigned m = w.bmk[o0 + b];
-                    rest[b] = contrib(S, R, w.opt, m);
-                    take[b] = w.hi[o0 + b] ? contrib(S, R, w.opt, m | (1u << j)) : POS_INF;
+                    rest[b] = contrib(S, w, m);
+                    take[b] = w.hi[o0 + b] ? contrib(S, w, m | (1u << j)) : POS_INF;
                 }
                 __syncwarp();
                 if (fm) {
@@ -799,9 +799,8 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
         }
         const int o1 = w.loff[j + 1];
         const int c1 = w.lcap[j + 1];
-        const int r = S.lvl_off[j] + w.opt[j];
-        const int uu = R.u[r];
-        const double ff = R.fp[r], bo = R.B[r], ba = R.base[r];
+        const int uu = w.sU[j];
+        const double ff = w.sFp[j], bo = w.sB[j], ba = w.sBase[j];
         int carry = 0;
         #pragma unroll 1
         for (int c = 0; c < nb; c += 32) {
@@ -850,7 +849,7 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
         }
         if (lane == 0) {
             w.nb[j + 1] = (uint16_t)m;
-            w.used[j + 1] = w.used[j] + R.d[r] * R.u[r];
+            w.used[j + 1] = w.used[j] + w.sDU[j];
         }
         __syncwarp();
         const double thr = h.thr(S);
@@ -918,7 +917,8 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
 }
 
 // ---- cursor load / store by a whole warp ----
-__device__ __forceinline__ void load_cont_warp(const Cont& c, Walk& w, bool ancestors = true) {
+__device__ __forceinline__ void load_cont_warp(const Spec& S, const Rows& R, const Cont& c, Walk& w,
+                                               bool ancestors = true) {
     const int lane = lane_id();
     const int dep = c.depth;
     const int o = w.loff[dep];
@@ -935,14 +935,14 @@ __device__ __forceinline__ void load_cont_warp(const Cont& c, Walk& w, bool ance
     __syncwarp();
     if (lane == 0) {
         #pragma unroll 1
-        for (int l = 0; l < dep; ++l) w.opt[l] = c.opt[l];
+        for (int l = 0; l < dep; ++l) sel_set(S, R, w, l, c.opt[l]);
         w.nb[dep] = c.nb;
         w.used[dep] = c.used;
         w.ph[dep] = (uint8_t)c.ph;
         w.oc[dep] = c.oc;
         w.oe[dep] = c.oe;
         w.vbase[dep] = -1;
-        if (c.ph) w.opt[dep] = (uint16_t)c.oc;
+        if (c.ph) sel_set(S, R, w, dep, c.oc);
         // only FIRST needs them (hit paths compare every level); MIN skips the rebuild
         #pragma unroll 1
         for (int l = ancestors ? dep - 1 : -1; l >= 0; --l) {
