@@ -291,9 +291,11 @@ int mosaic_gpu_merge_ranks(const void* records, int world, int mode, int k, int*
                            double* leaf_value);
 
 /* Search-engine knobs for experiments (tools/tune.py); defaults are the measured best and
- * nothing reads the environment.  Keys: don_depth, don_period (power of two), backoff_ns,
- * small_tree, deep_after, lookahead, generic_kernel, shard_level,
- * ring_per_walker, trace (1: one line per device search, 2: per launch), spec_k (GAHC candidates up to this many modules are batched),
+ * nothing reads the environment.  Keys: don_depth, don_tail (levels <= k-1-don_tail may be handed
+ * over by long-running pieces), don_period (power of two), backoff_ns, small_tree, deep_after,
+ * lookahead, generic_kernel, shard_level, ring_per_walker, trace (1: one line per device search,
+ * 2: per launch, 3: as 1 plus walker occupancy, a busy-walker timeline, hand-over outcomes and
+ * a log of long pieces of each launch's first search), spec_k (GAHC candidates up to this many modules are batched),
  * restart_k (MIN proofs of stages with at least this many modules restart on a big drop), and the measurement-only share_rank / share_world (search one
  * rank's share of a sharded search on this device, unmerged: NOT the stage's answer).
  * MOSAIC_INVALID_ARGUMENT for an unknown key. */

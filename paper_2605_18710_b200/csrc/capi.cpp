@@ -468,6 +468,7 @@ int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value) {
         const std::string k = key ? key : "";
         const long long v = (long long)value;
         if (k == "don_depth") t.don_depth = (int)v;
+        else if (k == "don_tail") t.don_tail = (int)v;
         else if (k == "don_period") {
             if (v < 1 || (v & (v - 1))) throw Error(MOSAIC_INVALID_ARGUMENT, "don_period: power of two");
             t.don_period = (int)v;

@@ -194,6 +194,7 @@ Engine::~Engine() {
     cudaStreamSynchronize(S_(stream_));
     free_eval();
     free_nccl();
+    if (d_tl_) cudaFree(d_tl_);
     EngineRes r;
     r.device = device_;
     r.stream = stream_;
@@ -429,13 +430,19 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         // donation policy: hand over only shallow levels, when the queue has run dry
         hs->don_max_level = S.k >= 6 ? S.k - 1 - tune_.don_depth : (S.k >= 3 ? S.k - 3 : 0);
         // long-running pieces may also hand over levels <= k-3 (see WarpHooks::abort)
-        hs->don_max_level_tail = S.k - 3 > hs->don_max_level ? S.k - 3 : hs->don_max_level;
+        hs->don_max_level_tail = std::max(hs->don_max_level, S.k - 1 - tune_.don_tail);
         hs->deep_after = tune_.deep_after;
         hs->lookahead = tune_.lookahead;
         hs->don_period = tune_.don_period;
         hs->backoff_cap_ns = tune_.backoff_cap;
         // small trees: hand-overs cost more than they parallelise; the root's walker finishes
         hs->donate = small[i] ? 0 : 1;
+        hs->timeline = nullptr;
+        if (tune_.trace >= 3 && i == 0 && !small[i]) {
+            if (!d_tl_) CK(cudaMalloc(&d_tl_, (2 + TL_BINS + 4 * TL_LOG) * sizeof(unsigned long long)));
+            CK(cudaMemsetAsync(d_tl_, 0, (2 + TL_BINS + 4 * TL_LOG) * sizeof(unsigned long long), s));
+            hs->timeline = static_cast<unsigned long long*>(d_tl_);
+        }
         std::memset(hc, 0, sizeof(Ctl));
         union {
             double d;
@@ -538,14 +545,46 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         st.leaves += (long long)hc->leaves;
         ++st.searches;
         alg_bytes_ += (long long)hc->leaves * 24LL * S.k;  // k option rows x 3 fp64 per leaf
-        if (tune_.trace == 1)
+        if (tune_.trace == 1 || tune_.trace == 3)
             std::fprintf(stderr, "[mosaic] %s k=%d thr=%.17g batch=%d ctas=%d kernel=%.3fms total=%.3fms "
                                  "nodes=%llu leaves=%llu %s\n",
                          S.mode == MODE_MIN ? "MIN  " : "FIRST", S.k,
                          S.mode == MODE_MIN ? q.ub : S.theta, n, ctas[i], kms, ms, hc->nodes,
                          hc->leaves, res.found ? "hit" : (res.aborted ? "restart" : ""));
+        if (tune_.trace == 3 && hc->pieces > 0)
+            std::fprintf(stderr, "[mosaic]       walkers=%u pieces=%llu (hand-over requests %llu, hand-overs "
+                                 "%llu, abandoned %llu) busy %.1f%% of walkers x kernel time\n",
+                         hc->walkers, hc->pieces, hc->dbg[7], hc->dbg[5], hc->dbg[6],
+                         100.0 * hc->busy / std::max(1.0, (double)hc->walkers * kms * 1e6));
     }
     ticket_base_ = tmax + 1;
+    if (tune_.trace >= 3 && n > 0 && !small[0]) {
+        // busy walkers over time (first search of the launch), 1 ms per column
+        std::vector<unsigned long long> tl(2 + TL_BINS + 4 * TL_LOG);
+        CK(cudaMemcpy(tl.data(), d_tl_, tl.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        int last = 0;
+        for (int b = 0; b < TL_BINS; ++b)
+            if (tl[1 + b]) last = b;
+        std::fprintf(stderr, "[mosaic] timeline (mean busy walkers of %d per ms):", ctas[0] * WPC);
+        for (int b = 0; b <= last; b += 4) {
+            unsigned long long sum = 0;
+            for (int i = b; i < b + 4 && i < TL_BINS; ++i) sum += tl[1 + i];
+            std::fprintf(stderr, " %.0f", (double)sum / (4.0 * TL_BIN_NS));
+        }
+        std::fprintf(stderr, "\n");
+        Ctl* hc0 = reinterpret_cast<Ctl*>(pin + BLOB_CTL);
+        std::fprintf(stderr, "[mosaic] requests: ring-full %llu, range<2 %llu, rest-below-max %llu, "
+                             "floor>max %llu, deep %llu; by level:", hc0->dbg[0], hc0->dbg[1],
+                     hc0->dbg[2], hc0->dbg[3], hc0->dbg[4]);
+        for (int l = 0; l < 8; ++l) std::fprintf(stderr, " %llu", hc0->dbg[8 + l]);
+        std::fprintf(stderr, "\n");
+        const unsigned long long nlog = std::min<unsigned long long>(tl[1 + TL_BINS], TL_LOG);
+        for (unsigned long long i = 0; i < nlog; ++i) {
+            const unsigned long long* e = &tl[2 + TL_BINS + 4 * i];
+            std::fprintf(stderr, "[mosaic] piece %.3f %.3f depth=%llu nodes=%llu\n", e[0] * 1e-6,
+                         e[1] * 1e-6, e[2], e[3]);
+        }
+    }
     if (tune_.trace >= 2) {
         const auto c3 = std::chrono::steady_clock::now();
         auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };

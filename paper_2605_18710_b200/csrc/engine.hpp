@@ -78,6 +78,7 @@ enum {
 // environment — experiments set them through mosaic_gpu_set_tuning().
 struct Tuning {
     int don_depth = 3;      // donate levels <= k-1-don_depth (measured best on cfg5)
+    int don_tail = 2;       // long-running pieces: levels <= k-1-don_tail
     int don_period = 4;     // power of two; control reads every 4 steps (tools/knob_solve.sh)
     int backoff_cap = 2048; // ns, idle walkers polling back-off cap (measured)
     double small_tree = 2e5;  // option tuples x G below which one walker runs the search alone
@@ -186,6 +187,7 @@ class Engine {
     void free_nccl();
     void* nccl_comm_ = nullptr;
     void* d_rec_ = nullptr;
+    void* d_tl_ = nullptr;  // trace >= 3: busy-walker timeline of the last launch
     size_t rec_cap_ = 0;
     int device_;
     int rank_ = 0, world_ = 1;

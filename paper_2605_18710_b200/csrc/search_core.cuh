@@ -74,6 +74,9 @@ constexpr double POS_INF = 1.0e300;
 // I* with T* in [I*(1 - TIE_EPS - rounding), I*].  Callers resolve a probe inside that
 // band with an exact FIRST search (planner.cpp).
 constexpr double TIE_EPS = 1e-14;
+constexpr int TL_BINS = 4096;
+constexpr unsigned long long TL_BIN_NS = 250000;  // 0.25 ms bins (trace timeline)
+constexpr int TL_LOG = 65536;  // trace timeline: pieces longer than 2 ms, 4 words each
 
 enum { MODE_MIN = 0, MODE_FIRST = 1 };
 
@@ -99,6 +102,8 @@ struct Spec {
                                    //   sequential cut, oracle.hpp:127-139); solo walker only
     int don_period;                // check for idle walkers every don_period option steps (2^n)
     int backoff_cap_ns;            // idle walkers poll the queue with back-off up to this
+    unsigned long long* timeline;  // trace >= 3 only: [0] launch t0 (ns), [1 + b] walker-busy ns
+                                   //   in bin b of TL_BIN_NS (null otherwise)
     int env_n[MAXK + 1];           // product-term envelope over unplaced levels >= j
     double env_a[MAXK + 1][MAXENV];
     double env_b[MAXK + 1][MAXENV];
@@ -178,6 +183,7 @@ struct Walk {
     // set (sel_set): block statistics and contributions read it instead of the option table
     double sB[MAXK], sBase[MAXK], sFp[MAXK];
     int sU[MAXK], sDU[MAXK];
+    unsigned long long t_start;  // trace >= 3: start of the current piece (globaltimer)
     uint16_t opt[MAXK];
     int16_t oc[MAXK];
     int16_t oe[MAXK];  // option range end per level (exclusive)

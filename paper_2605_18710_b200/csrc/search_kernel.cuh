@@ -30,6 +30,11 @@ struct Ctl {
     int has_hit;            // FIRST: a hit is published; MIN: an argmin leaf is stored
     double leaf_val;
     alignas(128) unsigned long long nodes, leaves;
+    // trace >= 3 only: walker-ns inside pieces, pieces walked, hand-over request outcomes
+    // (0 ring full, 1 range < 2, 2 rest only below the level limit, 3 floor above it, 4 deep,
+    // 5 handed over, 6 pieces abandoned, 7 requests; 8 + l: requests at level l)
+    unsigned long long busy, pieces;
+    unsigned long long dbg[16];
 };
 
 // Hooks of one walker (a warp).  Everything that steers control flow is decided by
@@ -67,7 +72,7 @@ struct WarpHooks {
         return v0 == v1 && before;
     }
     // 0 continue, 2 abandon (MIN restart, or a FIRST hit precedes all that is left),
-    // 3 idle walkers are waiting: donate shallow work
+    // 3 idle walkers are waiting: donate shallow work (4: deeper levels too)
     __device__ int abort() {
         ++steps;
         // global control state is read only every don_period steps: a per-step L2 round
@@ -221,9 +226,55 @@ struct WarpHooks {
         }
     }
     __device__ void level(int j) { cur_level = j; }
+    __device__ void note(const Spec& S, int i) {
+        if (S.timeline && lane_id() == 0) atomicAdd(&ctl->dbg[i], 1ull);
+    }
 };
 
 constexpr int WPC = 4;  // walkers (warps) per CTA
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// trace timeline: spread one piece's busy interval [a, b) over the 0.25 ms bins
+__device__ __noinline__ static void timeline_add(unsigned long long* tl, unsigned long long a, unsigned long long b) {
+    unsigned long long t0 = *(volatile unsigned long long*)tl;
+    if (t0 == 0) {
+        atomicCAS(tl, 0ull, a);
+        t0 = *(volatile unsigned long long*)tl;
+    }
+    if (a < t0) a = t0;
+    if (b <= a) return;
+    for (unsigned long long bin = (a - t0) / TL_BIN_NS; bin < (unsigned long long)TL_BINS; ++bin) {
+        const unsigned long long lo = t0 + bin * TL_BIN_NS, hi = lo + TL_BIN_NS;
+        const unsigned long long x = a > lo ? a : lo, y = b < hi ? b : hi;
+        if (y <= x) break;
+        atomicAdd(&tl[1 + bin], y - x);
+    }
+}
+
+// trace >= 3: account one finished piece (busy time, timeline, log of long pieces)
+__device__ __noinline__ static void trace_piece(const Spec& S, Ctl* ctl, unsigned long long g0, int d0,
+                                                unsigned long long nodes) {
+    unsigned long long* tl = S.timeline;
+    const unsigned long long g1 = gtimer();
+    atomicAdd(&ctl->busy, g1 - g0);
+    atomicAdd(&ctl->pieces, 1ull);
+    timeline_add(tl, g0, g1);
+    if (g1 - g0 > 2000000ull) {  // pieces longer than 2 ms: start, end, depth, nodes
+        unsigned long long* lg = tl + 1 + TL_BINS;
+        const unsigned long long i = atomicAdd(lg, 1ull);
+        if (i < (unsigned long long)TL_LOG) {
+            lg[1 + 4 * i] = g0 - tl[0];
+            lg[2 + 4 * i] = g1 - tl[0];
+            lg[3 + 4 * i] = (unsigned long long)d0;
+            lg[4 + 4 * i] = nodes;
+        }
+    }
+}
 
 // A launch runs up to MAXBATCH independent searches (one per module set of a GAHC round /
 // probe wave): search s owns CTAs [cta_off[s], cta_off[s+1]), its own Spec, control block,
@@ -397,7 +448,9 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
         h.inc_cache = POS_INF;
         h.inc_cache = h.bcast_inc();
         const int d0 = piece.depth;
+        if (S.timeline && lane == 0) w.t_start = gtimer();
         dfs_warp(S, R, w, d0, h);
+        if (S.timeline && lane == 0) trace_piece(S, ctl, w.t_start, d0, h.nodes);
         nodes += h.nodes;
         leaves += h.leaves;
         __syncwarp();

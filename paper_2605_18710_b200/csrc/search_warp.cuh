@@ -503,23 +503,43 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
         if (w.ph[j] == 0) {
             h.level(j);
             const int ab = h.abort();
-            if (ab == 2) return 2;
+            if (ab == 2) {
+                h.note(S, 6);
+                return 2;
+            }
             if (ab == 3 || ab == 4) {
+                h.note(S, 7);
                 // only shallow work is worth a hand-over (cursor traffic beats tiny
                 // subtrees) — except in the tail, when most walkers are starving
                 const int maxl = ab == 4 ? S.don_max_level_tail : S.don_max_level;
                 while (floor_lvl < j && !level_has_rest_warp(S, w, floor_lvl)) ++floor_lvl;
+                h.note(S, 8 + (j < 7 ? j : 7));
                 if (floor_lvl < j && floor_lvl <= maxl) {
-                    if (h.donate(w, floor_lvl, 1, -1)) ++floor_lvl;
+                    if (h.donate(w, floor_lvl, 1, -1)) {
+                        ++floor_lvl;
+                        h.note(S, 5);
+                    } else {
+                        h.note(S, 0);
+                    }
                 } else if (floor_lvl == j && j <= maxl) {
                     // all that is left is this level's option range: hand over its upper half
                     const int a = w.oc[j] + 1, e = w.oe[j];
                     if (e - a >= 2) {
                         const int mid = a + (e - a) / 2;
-                        if (h.donate(w, j, 0, mid) && lane == 0) w.oe[j] = (int16_t)mid;
+                        if (h.donate(w, j, 0, mid)) {
+                            if (lane == 0) w.oe[j] = (int16_t)mid;
+                            h.note(S, 5);
+                        }
                         __syncwarp();
+                    } else {
+                        h.note(S, 1);
                     }
+                } else if (floor_lvl < j) {
+                    h.note(S, 2);  // rest only below maxl
+                } else {
+                    h.note(S, 3);  // floor == j > maxl
                 }
+                if (ab == 4) h.note(S, 4);
             }
             if (j == k - 1 && MG_NONNEG(S)) {
                 if (last_level_batch(S, R, w, j, ps_lvl, h)) return 1;
