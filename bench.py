@@ -215,6 +215,9 @@ def reference_arm(args) -> None:
 
 
 N_EVAL = 1 << 20  # allocations per evaluator step
+# dram__bytes_read.sum + dram__bytes_write.sum of k_evaluate_fast on this workload, one
+# `ncu --set full` capture (profiles/r2_ncu_k_evaluate_fast.md): 763.6 MB + 12.2 MB
+EVAL_TRAFFIC_PER_LAUNCH = 775.9e6
 
 
 def evaluator_leg(pl, torch, dev, steps: int, warmup: int, peak: float, peak_kind: str) -> dict:
@@ -236,7 +239,9 @@ def evaluator_leg(pl, torch, dev, steps: int, warmup: int, peak: float, peak_kin
         flush_l2(torch, dev)
         pl.evaluate(tE, tG, tO, st, None, device=True)
     s = pl.evaluate_stats()
+    s0 = s
     k_ms = s["kernel_ms"] / max(1, s["launches"])
+    f_ms = s["fast_kernel_ms"] / max(1, s["launches"])
     alg = s["alg_bytes"] / max(1, s["launches"])
     achieved = alg / (k_ms / 1e3) / 1e9 if k_ms > 0 else 0.0
     hE, hG, hO = (torch.from_numpy(x).pin_memory() for x in (ent, gpus, off))
@@ -251,12 +256,17 @@ def evaluator_leg(pl, torch, dev, steps: int, warmup: int, peak: float, peak_kin
     return {"metric": "allocations scored/sec (K1 stage_time, mosaic_gpu_evaluate)",
             "value": n / (k_ms / 1e3) if k_ms > 0 else 0.0, "unit": "allocations/s",
             "allocations": n, "entries": int(len(ent)), "gpu_ids": int(len(gpus)),
-            "kernel_ms": k_ms,
+            "kernel_ms": k_ms, "fast_kernel_ms": f_ms,
+            "full_path_allocs": s0["full_path_allocs"],
+            "kernels": "k_evaluate_fast (include_self, <= 32 entries, distinct modules) + "
+                       "k_evaluate over the worklist of allocations it hands over",
             "e2e": {"value": n / e2e_s, "unit": "allocations/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": n * 8, "timing": "host wall clock, pinned host arrays"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if peak else None, "traffic": None,
-                         "kernel": "k_evaluate (eval.cu)", "peak_kind": peak_kind,
+                         "frac": achieved / peak if peak else None,
+                         "traffic": EVAL_TRAFFIC_PER_LAUNCH,
+                         "kernel": "k_evaluate_fast + k_evaluate (eval.cu), per call",
+                         "peak_kind": peak_kind,
                          "algorithmic_bytes": "per allocation 16 B (offset + stage time) + "
                                               "32 B per entry + 4 B per GPU id"},
             "data": "synthetic: random module subsets of cfg5, candidate options, "

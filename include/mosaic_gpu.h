@@ -157,6 +157,12 @@ int mosaic_gpu_evaluate(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* entrie
 int mosaic_gpu_evaluate_stats(mosaic_gpu_ctx* ctx, double* kernel_ms, int64_t* launches,
                               int64_t* alg_bytes);
 
+/* K1 path split since the last counter reset: time of the fast kernel (include_self, no
+ * per-entry output, <= 32 entries, every module at most once) and how many allocations went
+ * through the full-semantics kernel instead (worklist or non-fast calls). */
+int mosaic_gpu_evaluate_paths(mosaic_gpu_ctx* ctx, double* fast_kernel_ms,
+                              int64_t* full_path_allocs);
+
 /* Batched stage search (the plan enumerator + best-plan reduction of one GAHC round):
  * out[i] = stage_eval (MOSAIC_SEARCH_STAGE_EVAL) or ExactStageSolver::solve
  * (MOSAIC_SEARCH_EXACT) of module set masks[i].  The n computations advance together;

@@ -240,6 +240,17 @@ int mosaic_gpu_evaluate_stats(mosaic_gpu_ctx* ctx, double* kernel_ms, int64_t* l
     });
 }
 
+int mosaic_gpu_evaluate_paths(mosaic_gpu_ctx* ctx, double* fast_kernel_ms,
+                              int64_t* full_path_allocs) {
+    return guard([&] {
+        if (!ctx) throw Error(MOSAIC_RANGE, "null context");
+        auto& e = ctx->pl->engine();
+        if (fast_kernel_ms) *fast_kernel_ms = e.evaluate_fast_ms();
+        if (full_path_allocs) *full_path_allocs = e.evaluate_fallback_allocs();
+        return MOSAIC_OK;
+    });
+}
+
 int mosaic_gpu_stage_eval(mosaic_gpu_ctx* ctx, uint64_t mask, mosaic_gpu_stage_result* out) {
     return guard([&] {
         StageResult r = ctx->pl->stage_eval(mask);

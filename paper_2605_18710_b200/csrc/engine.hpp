@@ -130,6 +130,8 @@ class Engine {
     double evaluate_kernel_ms() const { return evk_ms_; }
     long long evaluate_kernel_launches() const { return evk_n_; }
     long long evaluate_alg_bytes() const { return evk_bytes_; }
+    double evaluate_fast_ms() const { return evf_ms_; }
+    long long evaluate_fallback_allocs() const { return ev_fallback_; }
 
     // fn == nullptr with world > 1: measure this rank's share only (no merge; the result
     // is NOT the stage's answer — used to simulate shard balance on one device)
@@ -158,6 +160,8 @@ class Engine {
         d2h_ = 0;
         alg_bytes_ = 0;
         evk_ms_ = 0;
+        evf_ms_ = 0;
+        ev_fallback_ = 0;
         evk_n_ = 0;
         evk_bytes_ = 0;
     }
@@ -236,6 +240,14 @@ class Engine {
     int* h_everr_ = nullptr;
     int ev_grid_ = 0;
     size_t ev_smem_ = 0;
+    // fast path (k_evaluate_fast) + the worklist of allocations it leaves to k_evaluate
+    void* ev_list_ = nullptr;
+    size_t ev_list_cap_ = 0;
+    int evf_grid_ = 0;
+    size_t evf_smem_ = 0;
+    double evf_ms_ = 0;
+    long long ev_fallback_ = 0;
+    void* evc_ = nullptr;
     double evk_ms_ = 0;
     long long evk_n_ = 0, evk_bytes_ = 0;
     void* eva_ = nullptr;

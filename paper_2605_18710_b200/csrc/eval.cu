@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -51,10 +52,11 @@ struct KEParams {
     long long n_ent, n_gpu_ids;
 };
 
-struct KEStats {  // device-side error bits and the bytes actually streamed
+struct KEStats {  // device-side error bits, the bytes actually streamed, the worklist size
     int err;
     int pad;
     unsigned long long gpu_ids, entries;
+    unsigned long long nlist;  // allocations k_evaluate_fast left to k_evaluate
 };
 
 // Per-warp shared memory: mask[2G] u32 (bit e of mask[r] / mask[G + r] <=> GPU r hosts
@@ -111,7 +113,7 @@ __device__ __forceinline__ double ke_wmax(double v) {
 __global__ void __launch_bounds__(32 * KE_WARPS, 4)
     k_evaluate(const EvalABI* __restrict__ ent, const int* __restrict__ gpus,
                const long long* __restrict__ off, long long n, KEParams P, double* st,
-               double* rect, KEStats* stats) {
+               double* rect, KEStats* stats, const long long* __restrict__ list) {
     extern __shared__ __align__(16) unsigned char ke_smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;  // lanes below this one
@@ -136,7 +138,11 @@ __global__ void __launch_bounds__(32 * KE_WARPS, 4)
     unsigned long long ids = 0, ents = 0;
     const bool self_in = P.include_self != 0;
     const long long stride = (long long)gridDim.x * KE_WARPS;
-    for (long long a = (long long)blockIdx.x * KE_WARPS + wid; a < n; a += stride) {
+    // with a worklist: only the allocations k_evaluate_fast handed over (same stream, so
+    // its count is final when this kernel starts)
+    const long long nn = list ? (long long)*(volatile unsigned long long*)&stats->nlist : n;
+    for (long long t = (long long)blockIdx.x * KE_WARPS + wid; t < nn; t += stride) {
+        const long long a = list ? list[t] : t;
         const long long e0 = off[a], e1 = off[a + 1];
         const long long ne64 = e1 - e0;
         if (ne64 <= 0 || e0 < 0 || e1 > P.n_ent || ne64 > KE_MAXE) {
@@ -421,6 +427,211 @@ __global__ void __launch_bounds__(32 * KE_WARPS, 4)
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// k_evaluate_fast — the common case at the memory roofline's instruction budget:
+// include_self, no per-entry output, <= 32 entries, every module at most once.
+//
+// Then every entry is its module's "self" entry and, with include_self, a GPU's delta
+// depends only on its resident set R_r, so
+//     stage_time = max(0, max_e (base_e + max_{r in gpus_e} delta(R_r)))
+//                = max(0, max_r (max_{e in R_r} base_e + delta(R_r)))
+// because fp addition rounds monotonically (x <= y => fl(x + d) <= fl(y + d)): the max can
+// move inside the sum without changing a bit.  One pass over the GPU slots (resident bitmap
+// built from the id stream with one shared atomic per 32 ids) replaces the per-entry maxima.
+// Anything else — duplicate modules, malformed entries or GPU lists, a NaN / below -1e300
+// slot value — is appended to a worklist that k_evaluate (the full reference semantics)
+// processes right after, on the same stream.
+// ---------------------------------------------------------------------------------------
+constexpr int KF_WARPS = 8;
+__host__ __device__ inline size_t kf_warp_bytes(int G) {
+    return (((size_t)G * 4 + 15) & ~(size_t)15) + 32 * 16;
+}
+
+// Set bit `bit` of mask[g] for one GPU id (ids outside the cluster flag the allocation).
+__device__ __forceinline__ void kf_mark(unsigned* mask, int g, int G, unsigned bit, bool& bad) {
+    if ((unsigned)g < (unsigned)G)
+        atomicOr(&mask[g], bit);
+    else
+        bad = true;
+}
+
+// NS = GPU slots per lane (G <= 32 * NS, unrolled); NS = 0: any G (loop).
+template <int NS>
+__global__ void __launch_bounds__(32 * KF_WARPS)
+    k_evaluate_fast(const EvalABI* __restrict__ ent, const int* __restrict__ gpus,
+                    const long long* __restrict__ off, long long n, KEParams P, double* st,
+                    KEStats* stats, long long* __restrict__ list) {
+    extern __shared__ __align__(16) unsigned char kf_smem[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u, le = lt | (1u << lane);
+    const int G = NS ? 32 * NS : P.G;
+    const int Gr = P.G;
+    unsigned char* wb = kf_smem + (size_t)wid * kf_warp_bytes(Gr);
+    unsigned* mask = reinterpret_cast<unsigned*>(wb);
+    double2* ebb = reinterpret_cast<double2*>(wb + (((size_t)Gr * 4 + 15) & ~(size_t)15));
+    // invariant: every mask word is zero between allocations (the slot pass clears)
+    for (int g = lane; g < Gr; g += 32) mask[g] = 0u;
+    __syncwarp();
+    unsigned long long ids = 0, ents = 0;
+    const double e1c = P.e1, e2c = P.e2, e3c = P.e3;
+    const bool addv = P.additive != 0;
+    const int L1 = P.L + 1;
+    const long long stride = (long long)gridDim.x * KF_WARPS;
+    for (long long a = (long long)blockIdx.x * KF_WARPS + wid; a < n; a += stride) {
+        const long long a0 = off[a], a1 = off[a + 1];
+        const long long ne64 = a1 - a0;
+        bool hand = ne64 < 0 || ne64 > 32 || a0 < 0 || a1 > P.n_ent;
+        if (!hand && ne64 == 0) {
+            if (lane == 0) st[a] = 0.0;  // the reference's `worst` seed
+            continue;
+        }
+        const int ne = hand ? 0 : (int)ne64;
+        const bool has = lane < ne;
+        int mod = -1 - lane, ng = 0;
+        long long goff = 0;
+        double bw = 0.0, bs = 0.0;
+        if (has) {
+            const int4* ep = reinterpret_cast<const int4*>(ent + a0 + lane);
+            const int4 w0 = __ldg(ep);
+            const int4 w1 = __ldg(ep + 1);
+            mod = w0.x;
+            const int d = w0.y, u = w0.z;
+            ng = w0.w;
+            goff = (long long)(((unsigned long long)(unsigned)w1.w << 32) | (unsigned)w1.z);
+            // handed over: malformed entries, entries without GPUs, options outside the
+            // rate tables (the full kernel reproduces the reference's lazy errors), rates
+            // outside the range where the fused max cannot overflow (|B| <= 4, |base| <= 1e300)
+            if (mod < 0 || mod >= P.n_mod || (w1.x != 0 && w1.x != P.L) || ng <= 0 ||
+                goff < 0 || goff + ng > P.n_gpu_ids || u < 0 || u > P.L || d < 1 || d > Gr) {
+                hand = true;
+            } else {
+                bw = __ldg(P.B + mod * L1 + u);
+                bs = __ldg(P.base + (mod * Gr + (d - 1)) * L1 + u);
+                hand = !(fabs(bw) <= 4.0) || !(fabs(bs) <= 1e300);
+            }
+        }
+        const unsigned same = __match_any_sync(KE_FULL, mod);
+        if (__any_sync(KE_FULL, hand || (has && (same & lt) != 0))) {
+            if (lane == 0) list[atomicAdd(&stats->nlist, 1ULL)] = a;
+            continue;
+        }
+        if (has) ebb[lane] = make_double2(bw, bs);
+        // the value of a GPU whose only resident is this entry (the same operations as the
+        // slot loop below on a one-bit set, so the same bits)
+        double solo_v;
+        {
+            const double s1 = 0.0 + bw, p1 = 1.0 * bw;
+            const double d0 = e1c + e2c * s1;
+            solo_v = bs + (addv ? d0 + 0.0 : d0 + e3c * p1);
+        }
+        // resident bitmaps from the id stream: bit e of mask[r] <=> r in entries[e].gpus
+        int bad = 0;
+        const long long g0 = __shfl_sync(KE_FULL, goff, 0);
+        const long long nxt = __shfl_up_sync(KE_FULL, goff + ng, 1);
+        const int T = (int)(__shfl_sync(KE_FULL, goff + ng, ne - 1) - g0);
+        if (__all_sync(KE_FULL, !has || lane == 0 || goff == nxt)) {
+            // GPU lists stored back to back (the packed layout): one flat pass over the
+            // allocation's ids, two 32-id chunks per step; id j belongs to the last entry
+            // starting at or before j
+            int rl = has ? (int)(goff - g0) : 0x7fffffff;  // this entry's start - chunk base
+            const int* gp = gpus + g0 + lane;
+            int ecar = -1;  // entry of the id before the chunk
+            for (int c0 = 0; c0 < T; c0 += 64, gp += 64, rl -= 64) {
+                const bool in0 = c0 + lane < T, in1 = c0 + 32 + lane < T;
+                const int ga = in0 ? __ldg(gp) : 0;
+                const int gb = in1 ? __ldg(gp + 32) : 0;
+                const unsigned sa = __reduce_or_sync(KE_FULL, (unsigned)rl < 32u ? 1u << rl : 0u);
+                const unsigned sbb = __reduce_or_sync(
+                    KE_FULL, (unsigned)(rl - 32) < 32u ? 1u << (rl - 32) : 0u);
+                const int ea = ecar + __popc(sa & le);
+                ecar += __popc(sa);
+                const int eb = ecar + __popc(sbb & le);
+                ecar += __popc(sbb);
+                if (in0) {
+                    if ((unsigned)ga < (unsigned)Gr) atomicOr(&mask[ga], 1u << ea); else bad = 1;
+                }
+                if (in1) {
+                    if ((unsigned)gb < (unsigned)Gr) atomicOr(&mask[gb], 1u << eb); else bad = 1;
+                }
+            }
+        } else {
+            for (int e = 0; e < ne; ++e) {
+                const int c = __shfl_sync(KE_FULL, ng, e);
+                const int* gl = gpus + __shfl_sync(KE_FULL, goff, e);
+                const unsigned bit = 1u << e;
+                for (int i = lane; i < c; i += 32) {
+                    const int g = __ldg(gl + i);
+                    if ((unsigned)g < (unsigned)Gr) atomicOr(&mask[g], bit); else bad = 1;
+                }
+            }
+        }
+        __syncwarp();
+        // one pass over the GPU slots.  A slot with one resident contributes that entry's
+        // solo value (collected as a bitmap); a shared slot gets its delta (residents summed
+        // in entry order: the reference's bits) plus the largest base latency among them.
+        double best = 0.0;
+        unsigned solo = 0u;
+        auto slot = [&](int g) {
+            unsigned m = mask[g];
+            if (m) {
+                mask[g] = 0u;
+                if (m & (m - 1u)) {
+                    double s = 0.0, p = 1.0, mb = -INFINITY;
+                    do {
+                        const int f = __ffs(m) - 1;
+                        m &= m - 1;
+                        const double2 v = ebb[f];
+                        s = s + v.x;
+                        p = p * v.x;
+                        mb = v.y > mb ? v.y : mb;
+                    } while (m);
+                    const double d0 = e1c + e2c * s;
+                    const double v = mb + (addv ? d0 + 0.0 : d0 + e3c * p);
+                    best = v > best ? v : best;
+                } else {
+                    solo |= m;
+                }
+            }
+        };
+        if (NS) {
+            #pragma unroll
+            for (int k = 0; k < (NS ? NS : 1); ++k)
+                if (32 * k + lane < Gr) slot(32 * k + lane);
+        } else {
+            for (int g = lane; g < G; g += 32) slot(g);
+        }
+        solo = __reduce_or_sync(KE_FULL, solo);
+        if (solo >> lane & 1u) best = solo_v > best ? solo_v : best;
+        if (__any_sync(KE_FULL, bad)) {  // GPU ids outside the cluster: full semantics
+            if (lane == 0) list[atomicAdd(&stats->nlist, 1ULL)] = a;
+            continue;
+        }
+        ents += (unsigned long long)ne;
+        ids += (unsigned long long)(unsigned)T;
+        // best >= +0 and finite: its bit pattern orders like its value (two 32-bit maxima)
+        const unsigned long long bb = (unsigned long long)__double_as_longlong(best > 0.0 ? best : 0.0);
+        const unsigned hi = __reduce_max_sync(KE_FULL, (unsigned)(bb >> 32));
+        const unsigned lo = __reduce_max_sync(KE_FULL, (unsigned)(bb >> 32) == hi ? (unsigned)bb : 0u);
+        if (lane == 0) st[a] = __longlong_as_double((long long)((unsigned long long)hi << 32 | lo));
+    }
+    if (lane == 0) {
+        atomicAdd(&stats->gpu_ids, ids);
+        atomicAdd(&stats->entries, ents);
+    }
+}
+
+using KFastFn = void (*)(const EvalABI*, const int*, const long long*, long long, KEParams,
+                         double*, KEStats*, long long*);
+static KFastFn kf_select(int G) {
+    switch ((G + 31) / 32) {
+        case 1: return k_evaluate_fast<1>;
+        case 2: return k_evaluate_fast<2>;
+        case 3: return k_evaluate_fast<3>;
+        case 4: return k_evaluate_fast<4>;
+        default: return k_evaluate_fast<0>;
+    }
+}
+
 void Engine::free_eval() {
     cudaFree(d_tab_base_);
     cudaFree(d_tab_B_);
@@ -436,7 +647,11 @@ void Engine::free_eval() {
     h_everr_ = nullptr;
     if (eva_) cudaEventDestroy((cudaEvent_t)eva_);
     if (evb_) cudaEventDestroy((cudaEvent_t)evb_);
-    eva_ = evb_ = nullptr;
+    if (evc_) cudaEventDestroy((cudaEvent_t)evc_);
+    eva_ = evb_ = evc_ = nullptr;
+    cudaFree(ev_list_);
+    ev_list_ = nullptr;
+    ev_list_cap_ = 0;
 }
 
 void Engine::set_rate_tables(const std::vector<double>& base, const std::vector<double>& B,
@@ -463,11 +678,13 @@ void Engine::set_rate_tables(const std::vector<double>& base, const std::vector<
     if (!d_everr_) {
         CKE(cudaMalloc(&d_everr_, sizeof(KEStats)));
         CKE(cudaMallocHost(&h_everr_, sizeof(KEStats)));
-        cudaEvent_t a, b;
+        cudaEvent_t a, b, c;
         CKE(cudaEventCreate(&a));
         CKE(cudaEventCreate(&b));
+        CKE(cudaEventCreate(&c));
         eva_ = a;
         evb_ = b;
+        evc_ = c;
     }
     ev_smem_ = KE_WARPS * ke_warp_bytes(G);
     {
@@ -486,6 +703,22 @@ void Engine::set_rate_tables(const std::vector<double>& base, const std::vector<
                                                       ev_smem_));
     CKE(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
     ev_grid_ = std::max(1, per_sm) * sms;
+    evf_smem_ = KF_WARPS * kf_warp_bytes(G);
+    {
+        static std::mutex mu;
+        static size_t set = 0;
+        std::lock_guard<std::mutex> lk(mu);
+        if (evf_smem_ > set) {
+            for (int g : {32, 64, 96, 128, 160})
+                CKE(cudaFuncSetAttribute(kf_select(g), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)evf_smem_));
+            set = evf_smem_;
+        }
+    }
+    per_sm = 0;
+    CKE(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf_select(G), 32 * KF_WARPS,
+                                                      evf_smem_));
+    evf_grid_ = std::max(1, per_sm) * sms;
 }
 
 int Engine::evaluate_abi(const EvalABI* ent, long long n_ent, const int* gpus, long long n_gpu_ids,
@@ -541,12 +774,46 @@ int Engine::evaluate_abi(const EvalABI* ent, long long n_ent, const int* gpus, l
     P.e3 = tab_e3_;
     P.n_ent = n_ent;
     P.n_gpu_ids = n_gpu_ids;
-    const long long want = (n + KE_WARPS - 1) / KE_WARPS;
-    const unsigned grid = (unsigned)std::min<long long>(want, ev_grid_);
+    // fast path for the common case (include_self, no per-entry output, 16-B aligned entry
+    // records); the allocations it cannot take go through the worklist to k_evaluate
+    // coefficients small enough that no slot value can overflow or drop below -1e300 with
+    // |B| <= 4 and |base| <= 1e300 (the fast kernel hands other entries over)
+    const double emax = std::fabs(tab_e1_) + 128.0 * std::fabs(tab_e2_) +
+                        18446744073709551616.0 * std::fabs(tab_e3_);
+    const bool fast = tab_self_ && !drect && (reinterpret_cast<uintptr_t>(de) & 15) == 0 &&
+                      emax < 1e290 && tab_G_ <= 1024 && n_gpu_ids < (1LL << 31);
+    long long* dlist = nullptr;
+    if (fast) {
+        if (ev_list_cap_ < (size_t)n) {
+            cudaFree(ev_list_);
+            ev_list_ = nullptr;
+            dev_bytes_ -= (long long)ev_list_cap_ * 8;
+            CKE(cudaMalloc(&ev_list_, (size_t)n * 8));
+            ev_list_cap_ = (size_t)n;
+            dev_bytes_ += (long long)n * 8;
+        }
+        dlist = static_cast<long long*>(ev_list_);
+    }
     CKE(cudaEventRecord((cudaEvent_t)eva_, s));
-    k_evaluate<<<grid, 32 * KE_WARPS, ev_smem_, s>>>(de, dg, doff, n, P, dst, drect,
-                                                     reinterpret_cast<KEStats*>(d_everr_));
-    CKE(cudaGetLastError());
+    if (fast) {
+        const long long wantf = (n + KF_WARPS - 1) / KF_WARPS;
+        const unsigned gridf = (unsigned)std::min<long long>(wantf, evf_grid_);
+        kf_select(tab_G_)<<<gridf, 32 * KF_WARPS, evf_smem_, s>>>(
+            de, dg, doff, n, P, dst, reinterpret_cast<KEStats*>(d_everr_), dlist);
+        CKE(cudaGetLastError());
+        ++launches_;
+        ++own_launches_;
+    }
+    CKE(cudaEventRecord((cudaEvent_t)evc_, s));
+    {
+        // the worklist's length is only known on the device: a full persistent grid that
+        // exits at once when the list is empty
+        const long long want = fast ? (long long)ev_grid_ : (n + KE_WARPS - 1) / KE_WARPS;
+        const unsigned grid = (unsigned)std::min<long long>(want, ev_grid_);
+        k_evaluate<<<grid, 32 * KE_WARPS, ev_smem_, s>>>(
+            de, dg, doff, n, P, dst, drect, reinterpret_cast<KEStats*>(d_everr_), dlist);
+        CKE(cudaGetLastError());
+    }
     CKE(cudaEventRecord((cudaEvent_t)evb_, s));
     ++launches_;
     ++own_launches_;
@@ -560,12 +827,15 @@ int Engine::evaluate_abi(const EvalABI* ent, long long n_ent, const int* gpus, l
         }
     }
     CKE(cudaStreamSynchronize(s));
-    float ms = 0;
+    float ms = 0, msf = 0;
     CKE(cudaEventElapsedTime(&ms, (cudaEvent_t)eva_, (cudaEvent_t)evb_));
+    CKE(cudaEventElapsedTime(&msf, (cudaEvent_t)eva_, (cudaEvent_t)evc_));
     evk_ms_ += ms;
+    evf_ms_ += msf;
     eval_ms_ += ms;
     ++evk_n_;
     const KEStats* ks = reinterpret_cast<const KEStats*>(h_everr_);
+    ev_fallback_ += fast ? (long long)ks->nlist : n;
     // algorithmic bytes: offsets + entries + GPU ids read, stage times (+ rectified) written
     evk_bytes_ += (long long)((n + 1) * 8 + ks->entries * sizeof(EvalABI) + ks->gpu_ids * 4 +
                               n * 8 + (rect ? ks->entries * 8 : 0));

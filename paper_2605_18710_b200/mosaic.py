@@ -164,6 +164,7 @@ EXPORTS = [
     "mosaic_gpu_baseline_plan", "mosaic_gpu_simulate",
     "mosaic_gpu_cache_masks", "mosaic_gpu_cache_entry", "mosaic_gpu_set_tuning",
     "mosaic_gpu_device_bytes", "mosaic_gpu_evaluate", "mosaic_gpu_evaluate_stats",
+    "mosaic_gpu_evaluate_paths",
 ]
 
 _lib = None
@@ -247,6 +248,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "mosaic_gpu_device_bytes": (C.c_int64, [vp]),
         "mosaic_gpu_evaluate": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int64, vp, C.c_int64,
                                           vp, vp, C.c_uint32]),
+        "mosaic_gpu_evaluate_paths": (C.c_int, [vp, P(C.c_double), P(C.c_int64)]),
         "mosaic_gpu_evaluate_stats": (C.c_int, [vp, P(C.c_double), P(C.c_int64),
                                                 P(C.c_int64)]),
         "mosaic_gpu_cache_masks": (C.c_int, [vp, P(C.c_uint64), C.c_int64, P(C.c_int64)]),
@@ -622,7 +624,10 @@ class Planner:
         ms, n, b = C.c_double(), C.c_int64(), C.c_int64()
         _raise(load_library().mosaic_gpu_evaluate_stats(self._ctx, C.byref(ms), C.byref(n),
                                                         C.byref(b)))
-        return {"kernel_ms": ms.value, "launches": n.value, "alg_bytes": b.value}
+        fms, nf = C.c_double(), C.c_int64()
+        _raise(load_library().mosaic_gpu_evaluate_paths(self._ctx, C.byref(fms), C.byref(nf)))
+        return {"kernel_ms": ms.value, "launches": n.value, "alg_bytes": b.value,
+                "fast_kernel_ms": fms.value, "full_path_allocs": nf.value}
 
     def make_baseline_plan(self, policy: str) -> "DeploymentPlan":
         """make_baseline_plan (simulator.hpp:283-313): 'megatron' or 'distmm', full-quota

@@ -173,3 +173,108 @@ def test_large_clusters_match_reference_bits():
              for m, d, u, gp in r["entries"]]) for r in rs]
         assert pl.stage_time(allocs) == [hexf(r["t"]) for r in rs], (inst, extra)
         pl.close()
+
+
+def _pack(allocs):
+    """[(m, d, u, gpus), ...] per allocation -> the flat ABI arrays."""
+    cols, gl, off = [[], [], [], [], []], [], [0]
+    for a in allocs:
+        for m, d, u, g in a:
+            for c, v in zip(cols, (m, d, u, len(g), len(gl))):
+                c.append(v)
+            gl.extend(g)
+        off.append(len(cols[0]))
+    ent = mosaic.pack_eval_entries(*[np.array(c, dtype=np.int64) for c in cols])
+    return ent, np.array(gl or [0], dtype=np.int32), np.array(off, dtype=np.int64)
+
+
+def _fast_vs_full(pl, ent, gpus, off):
+    """Stage times without per-entry output (k_evaluate_fast + worklist) against the full
+    path (per-entry output requested: k_evaluate on everything), bit for bit."""
+    n = len(off) - 1
+    s0 = pl.evaluate_stats()
+    st_fast = np.full(n, -7.0)
+    pl.evaluate(ent, gpus, off, st_fast)
+    s1 = pl.evaluate_stats()
+    st_full = np.full(n, -7.0)
+    pl.evaluate(ent, gpus, off, st_full, np.zeros(max(1, len(ent))))
+    assert np.array_equal(st_fast.view(np.int64), st_full.view(np.int64)), \
+        np.nonzero(st_fast.view(np.int64) != st_full.view(np.int64))[0][:10]
+    return st_fast, s1["full_path_allocs"] - s0["full_path_allocs"]
+
+
+@pytest.mark.parametrize("spec,extra", [("cfg5", ()), ("cfg4", ("additive",)),
+                                        ("cfg3", ("e=1e-3,-2e-4,5e-4",)),
+                                        ("cfg2", ()), ("cfg5", ("noself",))])
+def test_fast_path_bits_random(spec, extra):
+    # the monotone-max reformulation of k_evaluate_fast equals the per-entry maxima
+    pl = planner(spec, extra=list(extra))
+    ent, gpus, off = random_allocations(pl, 30000, seed=17)
+    _, full = _fast_vs_full(pl, ent, gpus, off)
+    if "noself" in extra:
+        assert full == len(off) - 1  # without include_self the fast kernel does not apply
+    else:
+        assert full == 0, full        # distinct modules: every allocation on the fast path
+    pl.close()
+
+
+def test_fast_path_worklist_and_edges():
+    # duplicate modules, repeated / unsorted GPU ids, empty allocations, entries without
+    # GPUs, out-of-table options and > 32 entries mixed into one batch: those go through
+    # the worklist to the full kernel, the rest stay on the fast path, all bit-exact
+    pl = planner("cfg5")
+    L = pl.quota_levels
+    rng = np.random.default_rng(23)
+    opts = [[(r.opt.dp_degree, r.opt.quota_units) for r in pl.candidate_options(m)]
+            for m in range(8)]
+    allocs, expect_full = [], 0
+    for i in range(3000):
+        kind = i % 6
+        k = int(rng.integers(1, 9))
+        mods = sorted(rng.choice(8, size=k, replace=False).tolist())
+        a = []
+        for m in mods:
+            d, u = opts[m][int(rng.integers(0, len(opts[m])))]
+            g = rng.choice(128, size=d, replace=False).tolist()
+            a.append((m, d, u, g))
+        if kind == 1:                       # duplicate module -> worklist
+            a.append(a[0])
+            expect_full += 1
+        elif kind == 2:                     # repeated + unsorted ids in one entry
+            m, d, u, g = a[-1]
+            a[-1] = (m, d, u, g + g[:1])
+        elif kind == 3:                     # an entry without GPUs -> worklist
+            m, d, u, g = a[0]
+            a[0] = (m, d, u, [])
+            expect_full += 1
+        elif kind == 4 and i % 12 == 4:     # empty allocation
+            a = []
+        elif kind == 5 and i % 30 == 5:     # > 32 entries -> worklist
+            a = [(j % 8, *opts[j % 8][0], [j]) for j in range(40)]
+            expect_full += 1
+        allocs.append(a)
+    ent, gpus, off = _pack(allocs)
+    st, full = _fast_vs_full(pl, ent, gpus, off)
+    assert full == expect_full, (full, expect_full)
+    # and against the reference-API path on a slice
+    sa = [mosaic.StageAllocation([mosaic.Entry(m, mosaic.DeploymentOption(d, u, L), g)
+                                  for m, d, u, g in a]) for a in allocs[:400]]
+    assert pl.stage_time(sa) == list(st[:400])
+    pl.close()
+
+
+def test_fast_path_reference_goldens():
+    # every reference edge / large-cluster golden row through the fast path
+    for name in ("stime_edge.json", "stime_large_g.json"):
+        rows = load_golden(name)
+        groups = {}
+        for row in rows:
+            if row["t"] is not None:
+                groups.setdefault((row["inst"], tuple(row["extra"])), []).append(row)
+        for (inst, extra), rs in groups.items():
+            pl = planner(inst, extra=list(extra))
+            ent, gpus, off = _pack([r["entries"] for r in rs])
+            st = np.zeros(len(rs))
+            pl.evaluate(ent, gpus, off, st)
+            assert list(st) == [hexf(r["t"]) for r in rs], (name, inst, extra)
+            pl.close()
