@@ -480,6 +480,9 @@ int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value) {
         const long long v = (long long)value;
         if (k == "don_depth") t.don_depth = (int)v;
         else if (k == "don_tail") t.don_tail = (int)v;
+        else if (k == "don_depth_small") t.don_depth_small = (int)v;
+        else if (k == "don_depth_first") t.don_depth_first = (int)v;
+        else if (k == "don_tail_first") t.don_tail_first = (int)v;
         else if (k == "don_period") {
             if (v < 1 || (v & (v - 1))) throw Error(MOSAIC_INVALID_ARGUMENT, "don_period: power of two");
             t.don_period = (int)v;

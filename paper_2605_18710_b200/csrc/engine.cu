@@ -428,9 +428,13 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         hs->shard_level = S.k >= 3 ? 2 : S.k - 1;
         if (tune_.shard_level >= 0) hs->shard_level = std::min(tune_.shard_level, S.k - 1);
         // donation policy: hand over only shallow levels, when the queue has run dry
-        hs->don_max_level = S.k >= 6 ? S.k - 1 - tune_.don_depth : (S.k >= 3 ? S.k - 3 : 0);
+        const bool first_ = S.mode == MODE_FIRST;
+        const int ddep = first_ && tune_.don_depth_first >= 0 ? tune_.don_depth_first : tune_.don_depth;
+        const int dtail = first_ && tune_.don_tail_first >= 0 ? tune_.don_tail_first : tune_.don_tail;
+        hs->don_max_level = S.k >= 6 ? S.k - 1 - ddep
+                                     : (S.k >= 3 ? std::max(0, S.k - 1 - tune_.don_depth_small) : 0);
         // long-running pieces may also hand over levels <= k-3 (see WarpHooks::abort)
-        hs->don_max_level_tail = std::max(hs->don_max_level, S.k - 1 - tune_.don_tail);
+        hs->don_max_level_tail = std::max(hs->don_max_level, S.k - 1 - dtail);
         hs->deep_after = tune_.deep_after;
         hs->lookahead = tune_.lookahead;
         hs->don_period = tune_.don_period;

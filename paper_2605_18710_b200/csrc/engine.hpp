@@ -79,6 +79,9 @@ enum {
 struct Tuning {
     int don_depth = 3;      // donate levels <= k-1-don_depth (measured best on cfg5)
     int don_tail = 2;       // long-running pieces: levels <= k-1-don_tail
+    int don_depth_small = 2;  // stages of 3..5 modules: donate levels <= k-1-don_depth_small
+    int don_depth_first = -1; // FIRST searches of >= 6 modules: own depth (-1: don_depth)
+    int don_tail_first = -1;  // FIRST searches: own don_tail (-1: don_tail)
     int don_period = 4;     // power of two; control reads every 4 steps (tools/knob_solve.sh)
     int backoff_cap = 2048; // ns, idle walkers polling back-off cap (measured)
     double small_tree = 2e5;  // option tuples x G below which one walker runs the search alone

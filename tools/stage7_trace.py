@@ -8,6 +8,6 @@ from paper_2605_18710_b200 import mosaic  # noqa: E402
 
 pl = mosaic.Planner.from_spec("cfg5", device=0)
 pl.stage_eval([0, 1, 2])
-pl.set_tuning(trace=1)
+pl.set_tuning(trace=int(sys.argv[1]) if len(sys.argv) > 1 else 1)
 r = pl.stage_eval(list(range(7)))
 print(r.stage_time.hex(), r.stats, file=sys.stderr)
