@@ -298,7 +298,9 @@ int mosaic_gpu_merge_ranks(const void* records, int world, int mode, int k, int*
 
 /* Search-engine knobs for experiments (tools/tune.py); defaults are the measured best and
  * nothing reads the environment.  Keys: don_depth, don_depth_small (stages of 3..5 modules hand
- * over levels <= k-1-don_depth_small), don_tail (levels <= k-1-don_tail may be handed
+ * over levels <= k-1-don_depth_small), don_depth_first / don_tail_first (FIRST searches' own
+ * values, -1: the common ones), tail_idle (> 0: the deeper hand-overs also while more than
+ * 1/tail_idle of the walkers are idle), don_tail (levels <= k-1-don_tail may be handed
  * over by long-running pieces), don_period (power of two), backoff_ns, small_tree, deep_after,
  * lookahead, generic_kernel, shard_level, ring_per_walker, trace (1: one line per device search,
  * 2: per launch, 3: as 1 plus walker occupancy, a busy-walker timeline, hand-over outcomes and

@@ -436,6 +436,7 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         // long-running pieces may also hand over levels <= k-3 (see WarpHooks::abort)
         hs->don_max_level_tail = std::max(hs->don_max_level, S.k - 1 - dtail);
         hs->deep_after = tune_.deep_after;
+        hs->tail_idle = tune_.tail_idle;
         hs->lookahead = tune_.lookahead;
         hs->don_period = tune_.don_period;
         hs->backoff_cap_ns = tune_.backoff_cap;

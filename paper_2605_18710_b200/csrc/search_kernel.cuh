@@ -55,6 +55,7 @@ struct WarpHooks {
     int don_period;
     int may_donate;
     long long deep_after;
+    int tail_idle;
     // solo: the only walker of its search (no hand-overs): control state it alone writes is
     // kept in registers, so the DFS makes no L2 round trips for it
     int solo;
@@ -104,7 +105,12 @@ struct WarpHooks {
                         if (qn == 0)  // queue drained and walkers waiting
                             // a walker that has been on its piece for long holds a big
                             // subtree: let it split deeper levels too
-                            code = steps > deep_after ? 4 : 3;
+                            code = steps > deep_after ||
+                                           (tail_idle > 0 &&
+                                            (unsigned long long)idle * tail_idle >
+                                                *(volatile unsigned int*)&ctl->walkers)
+                                       ? 4
+                                       : 3;
                     }
                 }
             }
@@ -370,6 +376,7 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
         h.don_period = S.don_period;
         h.may_donate = 0;
         h.deep_after = S.deep_after;
+        h.tail_idle = S.tail_idle;
         h.solo = 1;
         h.local_abort = 0;
         h.has_hit_local = ctl->has_hit;
@@ -441,6 +448,7 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
         h.don_period = S.don_period;
         h.may_donate = S.donate;
         h.deep_after = S.deep_after;
+        h.tail_idle = S.tail_idle;
         h.solo = 0;
         h.local_abort = 0;
         h.has_hit_local = 0;
