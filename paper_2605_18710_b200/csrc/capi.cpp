@@ -484,6 +484,8 @@ int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value) {
         else if (k == "don_depth_first") t.don_depth_first = (int)v;
         else if (k == "don_tail_first") t.don_tail_first = (int)v;
         else if (k == "tail_idle") t.tail_idle = (int)v;
+        else if (k == "fuse_k") t.fuse_k = (int)v;
+        else if (k == "fuse_tree") t.fuse_tree = v;
         else if (k == "don_period") {
             if (v < 1 || (v & (v - 1))) throw Error(MOSAIC_INVALID_ARGUMENT, "don_period: power of two");
             t.don_period = (int)v;

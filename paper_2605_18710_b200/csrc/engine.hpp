@@ -95,6 +95,8 @@ struct Tuning {
     int ring_per_walker = 16;  // cursor-ring slots per resident walker
     int trace = 0;          // one stderr line per device search
     int spec_k = 4;         // GAHC: batch-evaluate a round's candidates of up to spec_k modules
+    int fuse_k = 1;         // stage_evals of <= fuse_k modules run their MIN proof with the first probe
+    double fuse_tree = 2e5; // ... and so do stages with option tuples x G <= fuse_tree
     int restart_k = 5;      // MIN proofs of stages with >= restart_k modules restart on a big drop
     // measurement only (tools/): search rank share_rank's share of a share_world-way
     // sharded search on this one device, without merging — NOT the stage's answer

@@ -332,6 +332,19 @@ StageJob Planner::stage_eval_job(uint64_t mask, StageResult* out) {
     std::vector<Entry> argmin;  // an allocation reaching Tstar
     long long probes = 0;
     SearchOp op;
+    // small stages (<= fuse_k modules, or option tuples x G <= fuse_tree): the MIN proof does
+    // not need the first probe's leaf as its bound, so it runs in the same wave as that probe
+    // (ub = +inf) — one launch fewer; larger trees are cheaper to prove below the probe's
+    // leaf in a second wave
+    SearchOp mop;
+    std::vector<int> mop_order;
+    bool fuse_min = nonneg && (int)mods.size() < eng_->tuning().restart_k;
+    if (fuse_min) {
+        double tuples = (double)P_.gpu_count;
+        for (int m : mods) tuples *= (double)std::max<size_t>(1, opts_[m].size());
+        fuse_min = (int)mods.size() <= eng_->tuning().fuse_k || tuples <= eng_->tuning().fuse_tree;
+    }
+    bool min_ran = false, min_awaited = false, min_used = false;
     // FeasibilitySearch::run(tau) replayed: the first leaf in fail-first DFS order.
     // T* lies in [Tstar*(1 - TIE_EPS - rounding), Tstar]: below that band no leaf reaches
     // tau; inside it the probe is decided by an exact FIRST search, seeded with the argmin.
@@ -355,7 +368,17 @@ StageJob Planner::stage_eval_job(uint64_t mask, StageResult* out) {
             for (auto& [c_, m_] : cnt_) ORDER.push_back(m_);                               \
             const bool seed_ = nonneg && have_T && !argmin.empty() && Tstar <= th_;        \
             if (prep_first(ORDER, true, th_, op, res.st, seed_ ? &argmin : nullptr, Tstar)) { \
-                const mg::SearchResult sr_ = co_await SearchAwait{&op};                    \
+                if (fuse_min) { /* the MIN proof rides along with the first FIRST search */ \
+                    fuse_min = false;                                                      \
+                    min_ran = prep_min(mods, POS_INF, mop, res.st, mop_order);             \
+                }                                                                          \
+                if (min_ran && !min_used && !min_awaited) {                                \
+                    min_awaited = true;                                                    \
+                    co_await SearchAwait2{&op, &mop};                                      \
+                } else {                                                                   \
+                    co_await SearchAwait{&op};                                             \
+                }                                                                          \
+                const mg::SearchResult sr_ = op.res;                                       \
                 if (sr_.overflow) throw Error(TOO_LARGE, "stage needs more than 128 GPU blocks"); \
                 if (sr_.found) {                                                           \
                     LEAF = sr_.leaf;                                                       \
@@ -387,7 +410,20 @@ StageJob Planner::stage_eval_job(uint64_t mask, StageResult* out) {
         argmin = leaf_entries(best_order, best);
         double ub = t_best;
         std::vector<int> morder;
-        while (true) {
+        if (min_awaited && mop.res.found) {
+            // the ridden-along MIN proof (ub = +inf, no restarts): T* within the tie band
+            // of the minimum, bounded by the probe's leaf like the sequential proof
+            const mg::SearchResult& r = mop.res;
+            if (r.overflow) throw Error(TOO_LARGE, "stage needs more than 128 GPU blocks");
+            min_used = true;
+            if (r.value < t_best) {
+                if (r.leaf.nb > 0) argmin = leaf_entries(mop_order, r.leaf);
+                Tstar = r.value;
+            } else {
+                Tstar = t_best;
+            }
+        }
+        while (!min_used) {
             if (!prep_min(mods, ub, op, res.st, morder)) {
                 Tstar = ub;
                 break;
@@ -537,6 +573,7 @@ void Planner::run_jobs(std::vector<StageJob>& jobs, std::vector<char>* failed) {
             if (!j.h.done() && j.h.promise().op) {
                 reqs.push_back(j.h.promise().op->req);
                 who.push_back(&j);
+                if (j.h.promise().op2) reqs.push_back(j.h.promise().op2->req);
             }
         if (reqs.empty()) break;
         const double t1 = now_s();
@@ -545,10 +582,13 @@ void Planner::run_jobs(std::vector<StageJob>& jobs, std::vector<char>* failed) {
         t0 = now_s();
         t_dev += t0 - t1;
         ++waves;
+        size_t r = 0;
         for (size_t i = 0; i < who.size(); ++i) {
             auto& pr = who[i]->h.promise();
-            pr.op->res = res[i];
+            pr.op->res = res[r++];
+            if (pr.op2) pr.op2->res = res[r++];
             pr.op = nullptr;
+            pr.op2 = nullptr;
             who[i]->h.resume();
         }
     }

@@ -89,6 +89,7 @@ struct SearchOp {
 struct StageJob {
     struct promise_type {
         SearchOp* op = nullptr;  // the search this job waits for (null: running or done)
+        SearchOp* op2 = nullptr; // a second, independent search of the same wave (or null)
         std::exception_ptr exc;
         StageJob get_return_object() {
             return StageJob{std::coroutine_handle<promise_type>::from_promise(*this)};
@@ -120,6 +121,18 @@ struct SearchAwait {
         h.promise().op = op;
     }
     mg::SearchResult await_resume() const noexcept { return op->res; }
+};
+
+// Two independent searches of one job in the same wave (results in a->res, b->res).
+struct SearchAwait2 {
+    SearchOp* a;
+    SearchOp* b;
+    bool await_ready() const noexcept { return false; }
+    void await_suspend(std::coroutine_handle<StageJob::promise_type> h) const noexcept {
+        h.promise().op = a;
+        h.promise().op2 = b;
+    }
+    void await_resume() const noexcept {}
 };
 
 class Planner {
