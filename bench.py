@@ -444,6 +444,7 @@ def main() -> None:
         t_max = ttbp * 1000.0 * args.steps
     best_plan = res.plan.predicted_iteration_time
     searches_per_solve = res.trace.stage_eval_calls
+    peer_links = pl.counters()["peer_links"]
 
     # ---- e2e through the C ABI with host buffers (create + sample + read back) ----
     for _ in range(args.warmup):  # untimed: first-use allocations of the process
@@ -504,7 +505,10 @@ def main() -> None:
         "same_config": headline,
         "time_to_best_plan_s": ttbp, "best_plan_iteration_time": best_plan,
         "full_solve": {"stage_eval_calls": searches_per_solve, "median_ms": ttbp * 1000.0,
-                       "data_plane": plane},
+                       "data_plane": plane,
+                       # ranks whose search control blocks this rank mapped (CUDA IPC) for
+                       # in-search incumbent / earliest-hit sharing
+                       "peer_links": peer_links if world > 1 else None},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "timing": "host wall clock, create+sample+readback"},
         "gpu_launches": ctr["own_launches"],

@@ -157,6 +157,11 @@ int mosaic_gpu_evaluate(mosaic_gpu_ctx* ctx, const mosaic_gpu_eval_entry* entrie
 int mosaic_gpu_evaluate_stats(mosaic_gpu_ctx* ctx, double* kernel_ms, int64_t* launches,
                               int64_t* alg_bytes);
 
+/* Peer ranks whose search control blocks this context has mapped (CUDA IPC over NVLink) for
+ * in-search incumbent / earliest-hit sharing of sharded searches (0 before the first sharded
+ * launch, or when mapping failed: sharing then happens only at the end-of-launch merge). */
+int mosaic_gpu_peer_links(mosaic_gpu_ctx* ctx);
+
 /* K1 path split since the last counter reset: time of the fast kernel (include_self, no
  * per-entry output, <= 32 entries, every module at most once) and how many allocations went
  * through the full-semantics kernel instead (worklist or non-fast calls). */
@@ -307,7 +312,11 @@ int mosaic_gpu_merge_ranks(const void* records, int world, int mode, int k, int*
  * a log of long pieces of each launch's first search), spec_k (GAHC candidates up to this many modules are batched),
  * fuse_k / fuse_tree (stage_evals of at most fuse_k modules, or of at most fuse_tree option
  * tuples x GPUs, run their MIN proof in the first probe's launch), restart_k (MIN proofs of stages with at least this many modules restart on a big drop), and the measurement-only share_rank / share_world (search one
- * rank's share of a sharded search on this device, unmerged: NOT the stage's answer).
+ * rank's share of a sharded search on this device, unmerged: NOT the stage's answer), share_all
+ * (> 1: every large search runs as that many option-prefix shards in one launch on this device
+ * and is merged by the multi-GPU rule — the real answer, for shard-balance measurements) and
+ * share_peers (1, default: shards of a MIN proof lower each other's incumbent during the search
+ * — peer GPUs' control blocks mapped through CUDA IPC; 0: only at the end-of-launch merge).
  * MOSAIC_INVALID_ARGUMENT for an unknown key. */
 int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value);
 /* Device memory held by the context's engine (option table, cursor ring, control). */

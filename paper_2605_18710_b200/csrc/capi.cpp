@@ -240,6 +240,11 @@ int mosaic_gpu_evaluate_stats(mosaic_gpu_ctx* ctx, double* kernel_ms, int64_t* l
     });
 }
 
+int mosaic_gpu_peer_links(mosaic_gpu_ctx* ctx) {
+    if (!ctx) return 0;
+    return ctx->pl->engine().peer_links();
+}
+
 int mosaic_gpu_evaluate_paths(mosaic_gpu_ctx* ctx, double* fast_kernel_ms,
                               int64_t* full_path_allocs) {
     return guard([&] {
@@ -486,6 +491,8 @@ int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value) {
         else if (k == "tail_idle") t.tail_idle = (int)v;
         else if (k == "fuse_k") t.fuse_k = (int)v;
         else if (k == "fuse_tree") t.fuse_tree = v;
+        else if (k == "share_all") t.share_all = (int)v;
+        else if (k == "share_peers") t.share_peers = (int)v;
         else if (k == "don_period") {
             if (v < 1 || (v & (v - 1))) throw Error(MOSAIC_INVALID_ARGUMENT, "don_period: power of two");
             t.don_period = (int)v;

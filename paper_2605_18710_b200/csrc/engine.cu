@@ -193,6 +193,7 @@ Engine::~Engine() {
     cudaSetDevice(device_);
     cudaStreamSynchronize(S_(stream_));
     free_eval();
+    unlink_peers();
     free_nccl();
     if (d_tl_) cudaFree(d_tl_);
     EngineRes r;
@@ -347,8 +348,134 @@ void Engine::kernel_for(const std::vector<BatchReq>& reqs, size_t b0, size_t b1,
     *grid = it->second;
 }
 
+bool Engine::is_small(const BatchReq& q) const {
+    double tuples = 1.0;
+    for (int l = 0; l < q.S.k; ++l) tuples *= (double)(q.S.lvl_n[l] > 0 ? q.S.lvl_n[l] : 1);
+    return q.force_solo || tuples * q.S.G <= tune_.small_tree;
+}
+
+// Peer GPUs' staging blobs through CUDA IPC: each rank exports its blob once, the handles
+// are all-gathered over the rank plane, every rank maps the others' (over NVLink).  A rank
+// that cannot map a peer just does not write to it (sharing is an optimisation).
+void Engine::link_peers() {
+    peers_tried_ = true;
+    peer_blob_.assign(world_, nullptr);
+    peer_best_.assign(world_, nullptr);
+    cudaIpcMemHandle_t mine[2];
+    std::memset(mine, 0, sizeof mine);
+    if (cudaIpcGetMemHandle(&mine[0], d_blob_) != cudaSuccess ||
+        cudaIpcGetMemHandle(&mine[1], d_best_) != cudaSuccess) {
+        cudaGetLastError();
+        std::memset(mine, 0, sizeof mine);
+    }
+    std::vector<cudaIpcMemHandle_t> all(2 * (size_t)world_);
+    if (nccl_comm_)
+        nccl_allgather(mine, all.data(), sizeof mine);
+    else if (ag_(ag_user_, mine, all.data(), sizeof mine) != 0)
+        throw std::runtime_error("all-gather failed");
+    const cudaIpcMemHandle_t zero{};
+    for (int r = 0; r < world_; ++r) {
+        if (r == rank_ || std::memcmp(&all[2 * r], &zero, sizeof zero) == 0) continue;
+        void *p = nullptr, *b = nullptr;
+        if (cudaIpcOpenMemHandle(&p, all[2 * r], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess &&
+            cudaIpcOpenMemHandle(&b, all[2 * r + 1], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+            peer_blob_[r] = p;
+            peer_best_[r] = b;
+        } else {
+            cudaGetLastError();
+            if (p) cudaIpcCloseMemHandle(p);
+        }
+    }
+}
+
+void Engine::unlink_peers() {
+    for (void* p : peer_blob_)
+        if (p) cudaIpcCloseMemHandle(p);
+    for (void* p : peer_best_)
+        if (p) cudaIpcCloseMemHandle(p);
+    peer_blob_.clear();
+    peer_best_.clear();
+    peers_tried_ = false;
+}
+
+// share_all simulation on one device: every large search becomes share_all shards (the
+// multi-GPU option-prefix split) in the same launch, merged with the multi-GPU rule.
+std::vector<SearchResult> Engine::search_batch_sim(std::vector<BatchReq>& all_reqs) {
+    const int W = std::min(tune_.share_all, 8);
+    // sub-batches whose shards fit one launch (MAXBATCH searches)
+    std::vector<SearchResult> all_out;
+    all_out.reserve(all_reqs.size());
+    size_t a = 0;
+    while (a < all_reqs.size()) {
+        size_t b = a, used = 0;
+        while (b < all_reqs.size()) {
+            const size_t c = is_small(all_reqs[b]) ? 1 : (size_t)W;
+            if (used + c > (size_t)MAXBATCH) break;
+            used += c;
+            ++b;
+        }
+        std::vector<BatchReq> sub(all_reqs.begin() + a, all_reqs.begin() + b);
+        std::vector<SearchResult> so = search_batch_sim_chunk(sub, W);
+        all_out.insert(all_out.end(), so.begin(), so.end());
+        a = b;
+    }
+    return all_out;
+}
+
+std::vector<SearchResult> Engine::search_batch_sim_chunk(std::vector<BatchReq>& reqs, int W) {
+    std::vector<BatchReq> ex;
+    std::vector<int> first(reqs.size()), cnt(reqs.size());
+    for (size_t i = 0; i < reqs.size(); ++i) {
+        first[i] = (int)ex.size();
+        if (is_small(reqs[i])) {
+            ex.push_back(reqs[i]);
+            cnt[i] = 1;
+            continue;
+        }
+        for (int r = 0; r < W; ++r) {
+            ex.push_back(reqs[i]);
+            ex.back().sim_rank = r;
+            ex.back().sim_world = W;
+        }
+        cnt[i] = W;
+    }
+    const void* kfn;
+    size_t smem;
+    long long grid_cap;
+    kernel_for(ex, 0, ex.size(), &kfn, &smem, &grid_cap);
+    std::vector<SearchResult> exo(ex.size());
+    launch_chunk(ex, 0, ex.size(), kfn, smem, grid_cap, exo);
+    HitPath* hbest = reinterpret_cast<HitPath*>(h_best_);
+    CK(cudaMemcpyAsync(hbest, d_best_, ex.size() * sizeof(HitPath), cudaMemcpyDeviceToHost, S_(stream_)));
+    CK(cudaStreamSynchronize(S_(stream_)));
+    std::vector<SearchResult> out(reqs.size());
+    std::vector<RankRecord> per(W);
+    for (size_t i = 0; i < reqs.size(); ++i) {
+        if (cnt[i] == 1) {
+            out[i] = exo[first[i]];
+            continue;
+        }
+        for (int r = 0; r < W; ++r) {
+            const SearchResult& x = exo[first[i] + r];
+            RankRecord& m = per[r];
+            std::memset(&m, 0, sizeof m);
+            m.has_hit = x.found ? 1 : 0;
+            m.aborted = x.aborted ? 1 : 0;
+            m.overflow = x.overflow ? 1 : 0;
+            m.inc = reqs[i].S.mode == MODE_MIN ? x.value : POS_INF;
+            if (x.found) {
+                m.path = hbest[first[i] + r];
+                m.leaf = x.leaf;
+            }
+        }
+        merge_rank_records(per.data(), W, reqs[i].S.mode, reqs[i].S.k, out[i]);
+    }
+    return out;
+}
+
 std::vector<SearchResult> Engine::search_batch(std::vector<BatchReq>& reqs) {
     CK(cudaSetDevice(device_));
+    if (tune_.share_all > 1 && world_ == 1) return search_batch_sim(reqs);
     std::vector<SearchResult> out(reqs.size());
     size_t b0 = 0;
     while (b0 < reqs.size()) {
@@ -381,9 +508,7 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
     int n_big = 0;
     for (int i = 0; i < n; ++i) {
         const Spec& S = reqs[b0 + i].S;
-        double tuples = 1.0;
-        for (int l = 0; l < S.k; ++l) tuples *= (double)(S.lvl_n[l] > 0 ? S.lvl_n[l] : 1);
-        small[i] = reqs[b0 + i].force_solo || tuples * S.G <= tune_.small_tree;
+        small[i] = is_small(reqs[b0 + i]);
         if (small[i]) {
             // one walker owns the whole tree (solo mode, search_kernel.cuh); with several ranks
             // a small search runs whole on ONE rank (its owner) instead of sharded everywhere
@@ -406,6 +531,7 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         qtot += (long long)ctas[i] * WPC * std::max(1, tune_.ring_per_walker);
     }
     ensure_front(qtot);
+    if (sharded() && tune_.share_peers && !peers_tried_) link_peers();
     const unsigned long long t0 = ticket_base_;
     for (int i = 0; i < n; ++i) {
         BatchReq& q = reqs[b0 + i];
@@ -443,6 +569,31 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         // small trees: hand-overs cost more than they parallelise; the root's walker finishes
         hs->donate = small[i] ? 0 : 1;
         hs->timeline = nullptr;
+        hs->n_peer = 0;
+        if (q.sim_world > 1) {
+            // share_all simulation: this launch holds every shard of the search, the siblings
+            // sit next to it in the blob
+            hs->shard_rank = q.sim_rank;
+            hs->shard_world = q.sim_world;
+            if (tune_.share_peers)
+                for (int r = 0; r < q.sim_world && hs->n_peer < 8; ++r)
+                    if (r != q.sim_rank) {
+                        const size_t x = (size_t)(i - q.sim_rank + r);
+                        hs->peer_ctl[hs->n_peer] = static_cast<char*>(d_blob_) + x * BLOB_STRIDE + BLOB_CTL;
+                        hs->peer_best[hs->n_peer] = static_cast<HitPath*>(d_best_) + x;
+                        hs->peer_leaf[hs->n_peer] = static_cast<char*>(d_blob_) + x * BLOB_STRIDE + BLOB_LEAF;
+                        ++hs->n_peer;
+                    }
+        } else if (sharded() && !small[i] && !peer_blob_.empty()) {
+            // the same search's control block on every other rank (IPC-mapped peer memory)
+            for (int r = 0; r < world_ && hs->n_peer < 8; ++r)
+                if (r != rank_ && peer_blob_[r] && peer_best_[r]) {
+                    hs->peer_ctl[hs->n_peer] = static_cast<char*>(peer_blob_[r]) + (size_t)i * BLOB_STRIDE + BLOB_CTL;
+                    hs->peer_best[hs->n_peer] = static_cast<HitPath*>(peer_best_[r]) + i;
+                    hs->peer_leaf[hs->n_peer] = static_cast<char*>(peer_blob_[r]) + (size_t)i * BLOB_STRIDE + BLOB_LEAF;
+                    ++hs->n_peer;
+                }
+        }
         if (tune_.trace >= 3 && i == 0 && !small[i]) {
             if (!d_tl_) CK(cudaMalloc(&d_tl_, (2 + TL_BINS + 4 * TL_LOG) * sizeof(unsigned long long)));
             CK(cudaMemsetAsync(d_tl_, 0, (2 + TL_BINS + 4 * TL_LOG) * sizeof(unsigned long long), s));
@@ -665,8 +816,8 @@ void Engine::evaluate(const std::vector<EvalEntry>& ent, const std::vector<int>&
 
 // Multi-GPU: ranks search disjoint option-prefix shards of every search of a launch and
 // exchange one RankRecord per search (one all-gather per launch through the caller's
-// callback).  MIN takes the smallest incumbent (its argmin leaf from the rank holding it,
-// lowest rank on ties) and restarts everywhere if any rank restarted; FIRST takes the hit
+// callback).  MIN takes the smallest incumbent and the smallest leaf any rank stored (lowest
+// rank on ties) and restarts everywhere if any rank restarted; FIRST takes the hit
 // that is earliest in reference DFS order.
 static int host_path_cmp(const HitPath& a, const HitPath& b, int k) {
     for (int l = 0; l < k; ++l) {
@@ -689,15 +840,21 @@ int merge_rank_records(const RankRecord* all, int world, int mode, int k, Search
             best = x.inc;
             minr = r;
         }
-        if (x.has_hit && (win < 0 || host_path_cmp(x.path, all[win].path, k) < 0)) win = r;
+        if (mode == MODE_MIN) {
+            // shards share incumbents during the search, so every rank may end at the global
+            // incumbent: the argmin leaf is the smallest leaf a rank stored itself
+            if (x.has_hit && (win < 0 || x.leaf.value < all[win].leaf.value)) win = r;
+        } else if (x.has_hit && (win < 0 || host_path_cmp(x.path, all[win].path, k) < 0)) {
+            win = r;
+        }
     }
     res.overflow = overflow;
     if (mode == MODE_MIN) {
         res.aborted = aborted;
         res.value = best;
-        res.found = all[minr].has_hit != 0;
-        if (res.found) res.leaf = all[minr].leaf;
-        return minr;
+        res.found = win >= 0;
+        if (res.found) res.leaf = all[win].leaf;
+        return win >= 0 ? win : minr;
     }
     res.found = win >= 0;
     if (win >= 0) res.leaf = all[win].leaf;

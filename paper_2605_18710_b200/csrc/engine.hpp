@@ -32,6 +32,7 @@ struct BatchReq {
     const Leaf* seed_leaf = nullptr;     // ... as a path in this search's order
     SearchStats* st = nullptr;     // counters of the caller
     bool force_solo = false;       // one walker in DFS order whatever the tree size
+    int sim_rank = -1, sim_world = 0;  // share_all simulation: shard sim_rank of sim_world
 };
 
 // What a rank contributes to the merge of one sharded search (one all-gather per launch:
@@ -101,6 +102,13 @@ struct Tuning {
     // measurement only (tools/): search rank share_rank's share of a share_world-way
     // sharded search on this one device, without merging — NOT the stage's answer
     int share_rank = 0, share_world = 1;
+    // share_all > 1 (one device): every large search runs as share_all option-prefix shards
+    // in ONE launch and is merged like a multi-GPU search (shard balance and the effect of
+    // share_peers measured on one GPU)
+    int share_all = 0;
+    // sharded MIN proofs lower each other's incumbents during the search (peer Ctl words:
+    // CUDA IPC-mapped on the other GPUs, or the sibling shards of a share_all launch)
+    int share_peers = 1;
 };
 
 class Engine {
@@ -143,6 +151,7 @@ class Engine {
     // is NOT the stage's answer — used to simulate shard balance on one device)
     void set_shard(int rank, int world, AllGatherFn fn, void* user) {
         free_nccl();
+        unlink_peers();
         rank_ = rank;
         world_ = world;
         ag_ = fn;
@@ -151,6 +160,11 @@ class Engine {
     // the in-library data plane: a NCCL communicator from a unique id (nccl_plane.cu)
     void set_shard_nccl(int rank, int world, const void* nccl_id);
     Tuning& tuning() { return tune_; }
+    int peer_links() const {
+        int n = 0;
+        for (void* p : peer_blob_) n += p != nullptr;
+        return n;
+    }
     // bytes of device memory the engine holds (option table, ring, control blocks)
     long long device_bytes() const { return dev_bytes_; }
     long long launches() const { return launches_; }
@@ -195,6 +209,14 @@ class Engine {
     int owner_of(int i) const { return world_ > 1 ? i % world_ : 0; }
     std::vector<int> owned_;  // per search of the current launch: owner rank, -1 = sharded
     void free_nccl();
+    // peer GPUs' blob bases (CUDA IPC), exchanged once through the all-gather plane
+    void link_peers();
+    void unlink_peers();
+    std::vector<void*> peer_blob_, peer_best_;
+    bool peers_tried_ = false;
+    std::vector<SearchResult> search_batch_sim(std::vector<BatchReq>& reqs);
+    std::vector<SearchResult> search_batch_sim_chunk(std::vector<BatchReq>& reqs, int W);
+    bool is_small(const BatchReq& q) const;
     void* nccl_comm_ = nullptr;
     void* d_rec_ = nullptr;
     void* d_tl_ = nullptr;  // trace >= 3: busy-walker timeline of the last launch

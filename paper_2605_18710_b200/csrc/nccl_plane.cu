@@ -68,6 +68,7 @@ void Engine::set_shard_nccl(int rank, int world, const void* id) {
     if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("bad rank / world");
     if (cudaSetDevice(device_) != cudaSuccess) throw std::runtime_error("cudaSetDevice");
     free_nccl();
+    unlink_peers();
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof uid);
     ncclComm_t comm = nullptr;

@@ -104,6 +104,14 @@ struct Spec {
     int don_period;                // check for idle walkers every don_period option steps (2^n)
     int backoff_cap_ns;            // idle walkers poll the queue with back-off up to this
     unsigned long long* timeline;  // trace >= 3 only: [0] launch t0 (ns), [1 + b] walker-busy ns
+    // sharded searches: the control blocks (Ctl*) of this search's other shards — on peer
+    // GPUs (CUDA IPC over NVLink) or, simulated, in the same launch.  MIN: an improving leaf
+    // lowers every shard's incumbent (and raises their restart flag) right away.  FIRST: a
+    // hit is also published to every shard, whose walkers then drop the work after it.
+    void* peer_ctl[8];
+    void* peer_best[8];  // FIRST: their published earliest hit (HitPath) and its leaf
+    void* peer_leaf[8];
+    int n_peer;
                                    //   in bin b of TL_BIN_NS (null otherwise)
     int env_n[MAXK + 1];           // product-term envelope over unplaced levels >= j
     double env_a[MAXK + 1][MAXENV];

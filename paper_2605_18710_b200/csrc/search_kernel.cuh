@@ -41,6 +41,7 @@ struct Ctl {
 // lane 0 and broadcast, so the warp stays converged.
 struct WarpHooks {
     Ctl* ctl;
+    const Spec* sp;
     int mode;
     long long steps;
     double inc_cache;
@@ -134,8 +135,33 @@ struct WarpHooks {
             }
             __threadfence();
             atomicExch(&ctl->lock, 0);
+            // the other shards of this search: same seqlocked publication in their control
+            // blocks (one lock held at a time), system-scope fences for peer GPUs
+            if (better)
+                for (int p = 0; p < sp->n_peer; ++p)
+                    publish_peer(static_cast<Ctl*>(sp->peer_ctl[p]),
+                                 static_cast<HitPath*>(sp->peer_best[p]),
+                                 static_cast<Leaf*>(sp->peer_leaf[p]), wk, j, v);
         }
         __syncwarp();
+    }
+    __device__ static void publish_peer(Ctl* pc, HitPath* pb, Leaf* pl, const Walk& wk, int j,
+                                        double v) {
+        while (atomicCAS(&pc->lock, 0, 1) != 0) __nanosleep(64);
+        __threadfence_system();
+        const bool better = !*(volatile int*)&pc->has_hit ||
+                            path_cmp((const volatile HitPath*)pb, wk, j) > 0;
+        if (better) {
+            atomicAdd(&pc->ver, 1);
+            __threadfence_system();
+            path_store((volatile HitPath*)pb, wk, j);
+            store_leaf(wk, j, v, *pl);
+            *(volatile int*)&pc->has_hit = 1;
+            __threadfence_system();
+            atomicAdd(&pc->ver, 1);
+        }
+        __threadfence_system();
+        atomicExch(&pc->lock, 0);
     }
     // push the cursor "rest of level l" onto the ring queue (ticket t -> slot t % cap,
     // published by writing ready[slot] = t + 1)
@@ -208,6 +234,13 @@ struct WarpHooks {
             if (v < abort_below) {
                 atomicExch(&ctl->abort, 1);
                 local_abort = 1;
+            }
+            // the other shards of this search prune with it at once (remote atomics over
+            // NVLink for peer GPUs): no waiting for the end-of-launch merge
+            for (int p = 0; p < sp->n_peer; ++p) {
+                Ctl* pc = static_cast<Ctl*>(sp->peer_ctl[p]);
+                atomicMin(&pc->inc, (unsigned long long)__double_as_longlong(v));
+                if (v < abort_below) atomicExch(&pc->abort, 1);
             }
             while (atomicCAS(&ctl->lock, 0, 1) != 0) __nanosleep(64);
             __threadfence();
@@ -362,6 +395,7 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
         load_cont_warp(S, R, *root, w, MG_MODE(S) == MODE_FIRST);
         WarpHooks h;
         h.ctl = ctl;
+        h.sp = &S;
         h.mode = MG_MODE(S);
         h.steps = 0;
         h.refresh = 0;
@@ -434,6 +468,7 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
         load_cont_warp(S, R, piece, w, MG_MODE(S) == MODE_FIRST);
         WarpHooks h;
         h.ctl = ctl;
+        h.sp = &S;
         h.mode = MG_MODE(S);
         h.steps = 0;
         h.refresh = 0;

@@ -164,7 +164,7 @@ EXPORTS = [
     "mosaic_gpu_baseline_plan", "mosaic_gpu_simulate",
     "mosaic_gpu_cache_masks", "mosaic_gpu_cache_entry", "mosaic_gpu_set_tuning",
     "mosaic_gpu_device_bytes", "mosaic_gpu_evaluate", "mosaic_gpu_evaluate_stats",
-    "mosaic_gpu_evaluate_paths",
+    "mosaic_gpu_evaluate_paths", "mosaic_gpu_peer_links",
 ]
 
 _lib = None
@@ -249,6 +249,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "mosaic_gpu_evaluate": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int64, vp, C.c_int64,
                                           vp, vp, C.c_uint32]),
         "mosaic_gpu_evaluate_paths": (C.c_int, [vp, P(C.c_double), P(C.c_int64)]),
+        "mosaic_gpu_peer_links": (C.c_int, [vp]),
         "mosaic_gpu_evaluate_stats": (C.c_int, [vp, P(C.c_double), P(C.c_int64),
                                                 P(C.c_int64)]),
         "mosaic_gpu_cache_masks": (C.c_int, [vp, P(C.c_uint64), C.c_int64, P(C.c_int64)]),
@@ -710,7 +711,8 @@ class Planner:
                 "h2d_bytes": L.mosaic_gpu_h2d_bytes(self._ctx),
                 "d2h_bytes": L.mosaic_gpu_d2h_bytes(self._ctx),
                 "device_ms": L.mosaic_gpu_search_ms(self._ctx),
-                "alg_bytes": L.mosaic_gpu_alg_bytes(self._ctx)}
+                "alg_bytes": L.mosaic_gpu_alg_bytes(self._ctx),
+                "peer_links": L.mosaic_gpu_peer_links(self._ctx)}
 
     def mark(self, which: int) -> None:
         load_library().mosaic_gpu_mark(self._ctx, which)

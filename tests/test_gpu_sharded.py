@@ -27,6 +27,9 @@ def test_two_ranks_same_plan(workload, port):
     assert line["n_gpus"] == 2
     gold = load_golden("configs.json")[workload]["solve"]
     assert line["best_plan_iteration_time"] == hexf(gold["iteration_time"])
+    # the two ranks mapped each other's search control blocks (CUDA IPC) for in-search
+    # incumbent / earliest-hit sharing
+    assert line["full_solve"]["peer_links"] == 1, line["full_solve"]
 
 
 def test_bench_spawns_ranks_for_gpus_flag():
@@ -57,3 +60,34 @@ def test_in_library_nccl_plane_world1():
         r = pl.solve()
         assert r.plan.predicted_iteration_time == hexf(gold[w]["solve"]["iteration_time"])
         pl.close()
+
+
+def _sig(r):
+    return (r.stage_time, r.stats.feasibility_calls,
+            [(e.module, e.option.dp_degree, e.option.quota_units, tuple(e.gpus))
+             for e in r.allocation.entries])
+
+
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_share_all_shards_equal_unsharded(W):
+    # every large search split into W option-prefix shards in ONE launch, merged by the
+    # multi-GPU rule, with and without in-search incumbent / earliest-hit sharing between the
+    # shards: stage_evals and exact stages identical to the unsharded ones, the cfg4 plan
+    # equal to the reference's
+    mosaic = pytest.importorskip("paper_2605_18710_b200.mosaic")
+    pl = mosaic.Planner.from_spec("cfg5", device=0)
+    masks = [[0, 1, 2, 3], [0, 2, 3, 4], [0, 1, 2, 3, 4], [0, 2, 3, 4, 5]]
+    base = [_sig(pl.stage_eval(m)) for m in masks]
+    ex_base = [_sig(pl.exact_stage(m)) for m in masks[:2]]
+    for peers in (0, 1):
+        pl.set_tuning(share_all=W, share_peers=peers)
+        pl.clear_cache()
+        assert [_sig(pl.stage_eval(m)) for m in masks] == base, (W, peers)
+        assert [_sig(pl.exact_stage(m)) for m in masks[:2]] == ex_base, (W, peers)
+    pl.set_tuning(share_all=0, share_peers=1)
+    pl.close()
+    gold = load_golden("configs.json")["cfg4"]["solve"]
+    p4 = mosaic.Planner.from_spec("cfg4", device=0)
+    p4.set_tuning(share_all=W)
+    assert p4.solve().plan.predicted_iteration_time == hexf(gold["iteration_time"])
+    p4.close()
