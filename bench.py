@@ -274,6 +274,11 @@ def evaluator_leg(pl, torch, dev, steps: int, warmup: int, peak: float, peak_kin
 
 
 TRAFFIC_CSV = "profiles/r2_dram_sample.csv"
+# `ncu --set full` of the dominant launch (cfg5 7-encoder MIN proof, 408.9 ms):
+# profiles/r2_ncu_ksearch_min_cfg5_k7.ncu-rep
+NCU_MIN7 = {"smem_wavefronts_frac_of_peak": 0.355, "lsu_pipe_frac": 0.375,
+            "issue_active_frac": 0.437, "fp64_pipe_frac": 0.070,
+            "source": "profiles/r2_ncu_ksearch_min7.md"}
 
 
 def dram_traffic_per_launch():
@@ -480,6 +485,18 @@ def main() -> None:
     alg_bytes = ctr.get("alg_bytes", 0)
     avg_launch_s = ks_ms / ks_n / 1000.0
     achieved = (alg_bytes / ks_n) / avg_launch_s / 1e9 if avg_launch_s > 0 else 0.0
+    # SURVEY.md §8(d)'s on-chip roofline: the same algorithmic bytes against the measured
+    # shared-memory bandwidth, beside the shared-memory pipe utilisation ncu measured on the
+    # dominant launch (the 7-encoder MIN proof, profiles/r2_ncu_ksearch_min7.md)
+    try:
+        smem_peak = mosaic.smem_peak_gbs(local)
+    except mosaic.MosaicError:
+        smem_peak = None
+    roofline_smem = {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
+                     "frac": achieved / smem_peak if smem_peak else None,
+                     "peak_kind": "measured (mosaic_gpu_smem_peak: conflict-free 16-B shared "
+                                  "loads on every SM, this run)",
+                     "ncu_min_proof": NCU_MIN7}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1 and headline and os.path.exists(REF_DRIVER):
@@ -521,6 +538,7 @@ def main() -> None:
                                           "x 3 fp64, SURVEY.md 8d)",
                      "note": "branch-bound tree search; HBM is not the binding resource "
                              "(DESIGN.md)"},
+        "roofline_smem": roofline_smem,
         "cpu_baseline": cpu,
         "evaluator": evaluator,
         "clocks": clk.summary(),

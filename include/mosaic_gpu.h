@@ -162,6 +162,10 @@ int mosaic_gpu_evaluate_stats(mosaic_gpu_ctx* ctx, double* kernel_ms, int64_t* l
  * launch, or when mapping failed: sharing then happens only at the end-of-launch merge). */
 int mosaic_gpu_peer_links(mosaic_gpu_ctx* ctx);
 
+/* Calibration (SURVEY.md §8(d) roofline denominator): measured shared-memory load bandwidth
+ * of `device` in GB/s (conflict-free 16-B loads on every SM, best of 5 timed launches). */
+int mosaic_gpu_smem_peak(int device, double* gbs_out);
+
 /* K1 path split since the last counter reset: time of the fast kernel (include_self, no
  * per-entry output, <= 32 entries, every module at most once) and how many allocations went
  * through the full-semantics kernel instead (worklist or non-fast calls). */

@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX_HOST", "g++")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["engine.cu", "eval.cu", "nccl_plane.cu", "pack.cu", "sim.cu"]
+CU_SOURCES = ["engine.cu", "eval.cu", "nccl_plane.cu", "pack.cu", "sim.cu", "calib.cu"]
 # engine_fast.cu is compiled once per search mode (specialised MIN / FIRST kernels)
 CU_VARIANTS = [("engine_fast.cu", "engine_fast_min", ["-DMG_FAST_MODE=0"]),
                ("engine_fast.cu", "engine_fast_first", ["-DMG_FAST_MODE=1"]),

@@ -240,6 +240,14 @@ int mosaic_gpu_evaluate_stats(mosaic_gpu_ctx* ctx, double* kernel_ms, int64_t* l
     });
 }
 
+int mosaic_gpu_smem_peak(int device, double* gbs_out) {
+    return guard([&] {
+        if (!gbs_out) throw Error(MOSAIC_RANGE, "null output");
+        *gbs_out = mg::smem_peak_gbs(device, 5);
+        return MOSAIC_OK;
+    });
+}
+
 int mosaic_gpu_peer_links(mosaic_gpu_ctx* ctx) {
     if (!ctx) return 0;
     return ctx->pl->engine().peer_links();

@@ -48,6 +48,8 @@ struct RankRecord {
 // for the multi-process CPU tests).  Returns the winning rank (-1: no FIRST hit).
 int merge_rank_records(const RankRecord* all, int world, int mode, int k, SearchResult& res);
 size_t nccl_id_bytes();
+// calib.cu: measured shared-memory load bandwidth (GB/s), the SURVEY §8(d) roofline denominator
+double smem_peak_gbs(int device, int reps);
 void nccl_unique_id(void* out);  // ncclGetUniqueId through the run-time loaded NCCL
 
 struct EvalEntry {  // device evaluator input (one per allocation entry)

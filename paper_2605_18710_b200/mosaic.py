@@ -164,7 +164,7 @@ EXPORTS = [
     "mosaic_gpu_baseline_plan", "mosaic_gpu_simulate",
     "mosaic_gpu_cache_masks", "mosaic_gpu_cache_entry", "mosaic_gpu_set_tuning",
     "mosaic_gpu_device_bytes", "mosaic_gpu_evaluate", "mosaic_gpu_evaluate_stats",
-    "mosaic_gpu_evaluate_paths", "mosaic_gpu_peer_links",
+    "mosaic_gpu_evaluate_paths", "mosaic_gpu_peer_links", "mosaic_gpu_smem_peak",
 ]
 
 _lib = None
@@ -250,6 +250,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                           vp, vp, C.c_uint32]),
         "mosaic_gpu_evaluate_paths": (C.c_int, [vp, P(C.c_double), P(C.c_int64)]),
         "mosaic_gpu_peer_links": (C.c_int, [vp]),
+        "mosaic_gpu_smem_peak": (C.c_int, [C.c_int, P(C.c_double)]),
         "mosaic_gpu_evaluate_stats": (C.c_int, [vp, P(C.c_double), P(C.c_int64),
                                                 P(C.c_int64)]),
         "mosaic_gpu_cache_masks": (C.c_int, [vp, P(C.c_uint64), C.c_int64, P(C.c_int64)]),
@@ -832,6 +833,14 @@ def candidate_options(planner: Planner, module: int) -> list[CandidateOption]:
 
 
 MAXB = 128  # GPU blocks per search level (search_core.cuh)
+
+
+def smem_peak_gbs(device: int = 0) -> float:
+    """Measured shared-memory load bandwidth of the device (GB/s): the on-chip roofline
+    denominator of SURVEY.md §8(d)."""
+    g = C.c_double()
+    _raise(load_library().mosaic_gpu_smem_peak(device, C.byref(g)))
+    return g.value
 
 
 def nccl_unique_id() -> bytes:
