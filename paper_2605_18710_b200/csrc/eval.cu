@@ -444,7 +444,8 @@ __global__ void __launch_bounds__(32 * KE_WARPS, 4)
 // ---------------------------------------------------------------------------------------
 constexpr int KF_WARPS = 8;
 __host__ __device__ inline size_t kf_warp_bytes(int G) {
-    return (((size_t)G * 4 + 15) & ~(size_t)15) + 32 * 16;
+    // resident bitmaps mask[G] | entry rates ebb[32] (double2) | shared resident sets[G]
+    return 2 * (((size_t)G * 4 + 15) & ~(size_t)15) + 32 * 16;
 }
 
 // Set bit `bit` of mask[g] for one GPU id (ids outside the cluster flag the allocation).
@@ -469,6 +470,7 @@ __global__ void __launch_bounds__(32 * KF_WARPS)
     unsigned char* wb = kf_smem + (size_t)wid * kf_warp_bytes(Gr);
     unsigned* mask = reinterpret_cast<unsigned*>(wb);
     double2* ebb = reinterpret_cast<double2*>(wb + (((size_t)Gr * 4 + 15) & ~(size_t)15));
+    unsigned* sets = reinterpret_cast<unsigned*>(reinterpret_cast<unsigned char*>(ebb) + 32 * 16);
     // invariant: every mask word is zero between allocations (the slot pass clears)
     for (int g = lane; g < Gr; g += 32) mask[g] = 0u;
     __syncwarp();
@@ -567,38 +569,46 @@ __global__ void __launch_bounds__(32 * KF_WARPS)
         }
         __syncwarp();
         // one pass over the GPU slots.  A slot with one resident contributes that entry's
-        // solo value (collected as a bitmap); a shared slot gets its delta (residents summed
-        // in entry order: the reference's bits) plus the largest base latency among them.
+        // solo value (collected as a bitmap); a shared slot's resident set goes to a list,
+        // once per distinct set among 32 neighbouring slots (GPU windows make neighbours
+        // share sets), and each listed set gets its delta (residents summed in entry order:
+        // the reference's bits) plus the largest base latency among its residents.
         double best = 0.0;
         unsigned solo = 0u;
-        auto slot = [&](int g) {
-            unsigned m = mask[g];
-            if (m) {
-                mask[g] = 0u;
-                if (m & (m - 1u)) {
-                    double s = 0.0, p = 1.0, mb = -INFINITY;
-                    do {
-                        const int f = __ffs(m) - 1;
-                        m &= m - 1;
-                        const double2 v = ebb[f];
-                        s = s + v.x;
-                        p = p * v.x;
-                        mb = v.y > mb ? v.y : mb;
-                    } while (m);
-                    const double d0 = e1c + e2c * s;
-                    const double v = mb + (addv ? d0 + 0.0 : d0 + e3c * p);
-                    best = v > best ? v : best;
-                } else {
-                    solo |= m;
-                }
-            }
+        int nsets = 0;
+        auto slots32 = [&](int g0) {
+            const int g = g0 + lane;
+            unsigned m = g < Gr ? mask[g] : 0u;
+            if (m) mask[g] = 0u;
+            const bool multi = (m & (m - 1u)) != 0u;
+            if (!multi) solo |= m;
+            const unsigned same = __match_any_sync(KE_FULL, m);
+            const bool lead = multi && (same & lt) == 0u;
+            const unsigned bal = __ballot_sync(KE_FULL, lead);
+            if (lead) sets[nsets + __popc(bal & lt)] = m;
+            nsets += __popc(bal);
         };
         if (NS) {
             #pragma unroll
-            for (int k = 0; k < (NS ? NS : 1); ++k)
-                if (32 * k + lane < Gr) slot(32 * k + lane);
+            for (int k = 0; k < (NS ? NS : 1); ++k) slots32(32 * k);
         } else {
-            for (int g = lane; g < G; g += 32) slot(g);
+            for (int g0 = 0; g0 < G; g0 += 32) slots32(g0);
+        }
+        __syncwarp();
+        for (int i = lane; i < nsets; i += 32) {
+            unsigned m = sets[i];
+            double s = 0.0, p = 1.0, mb = -INFINITY;
+            do {
+                const int f = __ffs(m) - 1;
+                m &= m - 1;
+                const double2 v = ebb[f];
+                s = s + v.x;
+                p = p * v.x;
+                mb = v.y > mb ? v.y : mb;
+            } while (m);
+            const double d0 = e1c + e2c * s;
+            const double v = mb + (addv ? d0 + 0.0 : d0 + e3c * p);
+            best = v > best ? v : best;
         }
         solo = __reduce_or_sync(KE_FULL, solo);
         if (solo >> lane & 1u) best = solo_v > best ? solo_v : best;
