@@ -216,8 +216,8 @@ def reference_arm(args) -> None:
 
 N_EVAL = 1 << 20  # allocations per evaluator step
 # dram__bytes_read.sum + dram__bytes_write.sum of k_evaluate_fast on this workload, one
-# `ncu --set full` capture (profiles/r2_ncu_k_evaluate_fast.md): 763.6 MB + 12.2 MB
-EVAL_TRAFFIC_PER_LAUNCH = 775.9e6
+# `ncu --set full` capture (profiles/r2_ncu_k_evaluate_fast.md): 761.9 MB + 12.0 MB
+EVAL_TRAFFIC_PER_LAUNCH = 773.8e6
 
 
 def evaluator_leg(pl, torch, dev, steps: int, warmup: int, peak: float, peak_kind: str) -> dict:
