@@ -306,7 +306,8 @@ int mosaic_gpu_merge_ranks(const void* records, int world, int mode, int k, int*
                            double* leaf_value);
 
 /* Search-engine knobs for experiments (tools/tune.py); defaults are the measured best and
- * nothing reads the environment.  Keys: don_depth, don_depth_small (stages of 3..5 modules hand
+ * nothing reads the environment.  Keys: don_period_small (control-read period of stages below
+ * restart_k modules), don_depth, don_depth_small (stages of 3..5 modules hand
  * over levels <= k-1-don_depth_small), don_depth_first / don_tail_first (FIRST searches' own
  * values, -1: the common ones), tail_idle (> 0: the deeper hand-overs also while more than
  * 1/tail_idle of the walkers are idle), don_tail (levels <= k-1-don_tail may be handed

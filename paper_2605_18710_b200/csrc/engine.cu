@@ -564,7 +564,9 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         hs->deep_after = tune_.deep_after;
         hs->tail_idle = tune_.tail_idle;
         hs->lookahead = tune_.lookahead;
-        hs->don_period = tune_.don_period;
+        // small stages: control reads every step (faster ramp-up of trees of a few hundred
+        // nodes); large ones every don_period steps (the L2 round trip per step costs more)
+        hs->don_period = S.k < tune_.restart_k ? tune_.don_period_small : tune_.don_period;
         hs->backoff_cap_ns = tune_.backoff_cap;
         // small trees: hand-overs cost more than they parallelise; the root's walker finishes
         hs->donate = small[i] ? 0 : 1;

@@ -86,6 +86,7 @@ struct Tuning {
     int don_depth_first = -1; // FIRST searches of >= 6 modules: own depth (-1: don_depth)
     int don_tail_first = -1;  // FIRST searches: own don_tail (-1: don_tail)
     int don_period = 4;     // power of two; control reads every 4 steps (tools/knob_solve.sh)
+    int don_period_small = 1;  // the same for stages below restart_k modules (bench sample sweep)
     int backoff_cap = 2048; // ns, idle walkers polling back-off cap (measured)
     double small_tree = 2e5;  // option tuples x G below which one walker runs the search alone
     long long deep_after = 16384;  // steps on one piece before deeper hand-overs are allowed
