@@ -563,6 +563,7 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         hs->don_max_level_tail = std::max(hs->don_max_level, S.k - 1 - dtail);
         hs->deep_after = tune_.deep_after;
         hs->tail_idle = tune_.tail_idle;
+        hs->tail_after = tune_.tail_after;
         hs->lookahead = tune_.lookahead;
         // small stages: control reads every step (faster ramp-up of trees of a few hundred
         // nodes); large ones every don_period steps (the L2 round trip per step costs more)
@@ -613,6 +614,7 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         // so ring slots never need clearing: a stale ready value belongs to an older ticket
         hc->outstanding = 1;
         hc->q_head = t0;
+        hc->q_base = t0;
         hc->q_tail = t0 + 1;
         hc->q_cap = (unsigned long long)ctas[i] * WPC * std::max(1, tune_.ring_per_walker);
         hc->walkers = (unsigned)(ctas[i] * WPC);

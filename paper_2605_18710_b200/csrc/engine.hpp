@@ -90,7 +90,8 @@ struct Tuning {
     int backoff_cap = 2048; // ns, idle walkers polling back-off cap (measured)
     double small_tree = 2e5;  // option tuples x G below which one walker runs the search alone
     long long deep_after = 16384;  // steps on one piece before deeper hand-overs are allowed
-    int tail_idle = 0;      // > 0: deeper hand-overs also once more than 1/tail_idle walkers idle
+    int tail_idle = 0;      // > 0: tail phase once the ramp-up is over and > 1/tail_idle walkers idle
+    long long tail_after = 256;  // ... in which deeper hand-overs need only this many steps
     // child look-ahead (can every remaining level still place an option?): off by default —
     // the lane-parallel option screen at the next level does the same job for less
     int lookahead = 0;

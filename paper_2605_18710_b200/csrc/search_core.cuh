@@ -95,7 +95,8 @@ struct Spec {
     int don_max_level;             // work donation: only levels <= this are handed over
     int don_max_level_tail;        //   ... or <= this once a walker ran deep_after steps on a piece
     long long deep_after;
-    int tail_idle;                 // > 0: deeper hand-overs too once idle * tail_idle > walkers
+    int tail_idle;                 // > 0: tail phase once idle * tail_idle > walkers (after ramp-up)
+    long long tail_after;          //   ... in which deeper hand-overs need only tail_after steps
     int lookahead;
     int donate;                    // 0: never hand work over (one walker owns the tree)
     int seq_cut;                   // MIN, models with negative coefficients: skip an option whose

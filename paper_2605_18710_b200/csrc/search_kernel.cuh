@@ -22,6 +22,7 @@ struct Ctl {
     alignas(128) unsigned long long q_head;
     alignas(128) unsigned long long q_tail;
     unsigned long long q_cap;
+    unsigned long long q_base;  // first ticket of this launch (q_head - q_base: pieces taken)
     alignas(128) unsigned long long outstanding;  // queued + in-flight cursors
     alignas(128) unsigned int idle;
     unsigned int walkers;  // resident walkers of this launch
@@ -57,6 +58,7 @@ struct WarpHooks {
     int may_donate;
     long long deep_after;
     int tail_idle;
+    long long tail_after;
     // solo: the only walker of its search (no hand-overs): control state it alone writes is
     // kept in registers, so the DFS makes no L2 round trips for it
     int solo;
@@ -106,12 +108,15 @@ struct WarpHooks {
                         if (qn == 0)  // queue drained and walkers waiting
                             // a walker that has been on its piece for long holds a big
                             // subtree: let it split deeper levels too
-                            code = steps > deep_after ||
-                                           (tail_idle > 0 &&
-                                            (unsigned long long)idle * tail_idle >
-                                                *(volatile unsigned int*)&ctl->walkers)
-                                       ? 4
-                                       : 3;
+                        {
+                            // tail phase (tail_idle > 0): the ramp-up is over (every walker
+                            // has had a piece) and more than 1/tail_idle of them are idle
+                            const unsigned wk = *(volatile unsigned int*)&ctl->walkers;
+                            const bool tail =
+                                tail_idle > 0 && (unsigned long long)idle * tail_idle > wk &&
+                                *(volatile unsigned long long*)&ctl->q_head - ctl->q_base > wk;
+                            code = steps > (tail ? tail_after : deep_after) ? 4 : 3;
+                        }
                     }
                 }
             }
@@ -411,6 +416,7 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
         h.may_donate = 0;
         h.deep_after = S.deep_after;
         h.tail_idle = S.tail_idle;
+        h.tail_after = S.tail_after;
         h.solo = 1;
         h.local_abort = 0;
         h.has_hit_local = ctl->has_hit;
@@ -484,6 +490,7 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
         h.may_donate = S.donate;
         h.deep_after = S.deep_after;
         h.tail_idle = S.tail_idle;
+        h.tail_after = S.tail_after;
         h.solo = 0;
         h.local_abort = 0;
         h.has_hit_local = 0;
