@@ -633,12 +633,20 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         }
     }
     CK(cudaEventRecord((cudaEvent_t)ev0_, s));
-    for (int i = 0; i < n; ++i)
-        if (reqs[b0 + i].S.mode == MODE_FIRST && reqs[b0 + i].seed_path && reqs[b0 + i].seed_leaf) {
-            CK(cudaMemcpyAsync(static_cast<HitPath*>(d_best_) + i, hbest + i, sizeof(HitPath),
-                               cudaMemcpyHostToDevice, s));
-            h2d_ += sizeof(HitPath);
+    {
+        // seeded FIRST searches: their hit paths in ONE copy (the range spanning them)
+        int s0 = -1, s1 = -1;
+        for (int i = 0; i < n; ++i)
+            if (reqs[b0 + i].S.mode == MODE_FIRST && reqs[b0 + i].seed_path && reqs[b0 + i].seed_leaf) {
+                if (s0 < 0) s0 = i;
+                s1 = i;
+            }
+        if (s0 >= 0) {
+            CK(cudaMemcpyAsync(static_cast<HitPath*>(d_best_) + s0, hbest + s0,
+                               (size_t)(s1 - s0 + 1) * sizeof(HitPath), cudaMemcpyHostToDevice, s));
+            h2d_ += (long long)(s1 - s0 + 1) * sizeof(HitPath);
         }
+    }
     // every search's Spec | Ctl | Leaf | root Cont in one upload
     CK(cudaMemcpyAsync(d_blob_, h_pin_, (size_t)n * BLOB_STRIDE, cudaMemcpyHostToDevice, s));
     h2d_ += (long long)n * BLOB_STRIDE;
