@@ -105,14 +105,19 @@ inline bool build_spec(const Model& M, const SearchReq& q, Spec& S) {
         S.thp = q.ub >= POS_INF ? POS_INF : q.ub * (1.0 - TIE_EPS);
     else
         S.thp = q.theta >= POS_INF ? POS_INF : q.theta * (1.0 + 1e-12);
-    // module-index position -> level
-    std::vector<std::pair<int, int>> ml;
-    for (int l = 0; l < k; ++l) ml.push_back({q.level_module[l], l});
-    std::sort(ml.begin(), ml.end());
+    // module-index position -> level (no heap: this runs once per device search)
+    std::pair<int, int> ml[MAXK];
+    for (int l = 0; l < k; ++l) ml[l] = {q.level_module[l], l};
+    std::sort(ml, ml + k);
     for (int p = 0; p < k; ++p) S.pos_lvl[p] = ml[p].second;
 
-    std::vector<double> bmin(k, 1.0);
-    std::vector<int> forced(k, 1), dmin(k, 0);
+    double bmin[MAXK];
+    int forced[MAXK], dmin[MAXK];
+    for (int l = 0; l < k; ++l) {
+        bmin[l] = 1.0;
+        forced[l] = 1;
+        dmin[l] = 0;
+    }
     // fast path (non-negative coefficients, index built): the option list stops at the first
     // row with base + e1 above the threshold (rows are sorted by base latency); a row is usable
     // iff its bound (= base + e1 [+ e2 B]) is within the threshold — the scan below, exactly
@@ -173,53 +178,65 @@ inline bool build_spec(const Model& M, const SearchReq& q, Spec& S) {
     for (int l = k - 1; l >= 0; --l) S.suffix_min[l] = S.suffix_min[l + 1] + dmin[l];
 
     // Product-term envelope g_j(P) = min over subsets T of unplaced levels >= j that
-    // contain every forced level of  e2*sum_T Bmin + e3*P*prod_T Bmin.
+    // contain every forced level of  e2*sum_T Bmin + e3*P*prod_T Bmin.  Lines dominated at
+    // both ends of P in [0, 1] by another single line are dropped (ties: the lower index
+    // stays).  Scratch vectors are reused across calls: this runs once per device search.
     const double e3 = S.additive ? 0.0 : M.e3;
+    thread_local std::vector<double> la, lb;
+    thread_local std::vector<int> kept;
     for (int j = 0; j <= k; ++j) {
         const int nf = k - j;
-        std::vector<std::pair<double, double>> lines;
-        if (nf <= 12) {
-            for (int T = 0; T < (1 << nf); ++T) {
-                bool ok = true;
-                double a = 0.0, b = e3;
-                for (int i = 0; i < nf; ++i) {
-                    if (T >> i & 1) {
-                        a += M.e2 * bmin[j + i];
-                        b *= bmin[j + i];
-                    } else if (forced[j + i]) {
-                        ok = false;
-                    }
+        la.clear();
+        lb.clear();
+        for (int T = 0; T < (1 << nf); ++T) {
+            bool ok = true;
+            double a = 0.0, b = e3;
+            for (int i = 0; i < nf; ++i) {
+                if (T >> i & 1) {
+                    a += M.e2 * bmin[j + i];
+                    b *= bmin[j + i];
+                } else if (forced[j + i]) {
+                    ok = false;
                 }
-                if (ok) lines.push_back({a, b});
             }
-        } else {
-            lines.push_back({0.0, 0.0});
+            if (ok) {
+                la.push_back(a);
+                lb.push_back(b);
+            }
         }
-        // keep the lower envelope on P in [0, 1]
-        std::vector<std::pair<double, double>> keep;
-        for (size_t i = 0; i < lines.size(); ++i) {
+        const int n = (int)la.size();
+        kept.assign(n, 0);
+        for (int i = 0; i < n; ++i) {
             bool dom = false;
-            for (size_t h = 0; h < lines.size() && !dom; ++h) {
+            for (int h = 0; h < n && !dom; ++h) {
                 if (h == i) continue;
-                bool le0 = lines[h].first <= lines[i].first;
-                bool le1 = lines[h].first + lines[h].second <= lines[i].first + lines[i].second;
-                bool strict = lines[h].first < lines[i].first ||
-                              lines[h].first + lines[h].second < lines[i].first + lines[i].second;
+                const bool le0 = la[h] <= la[i];
+                const bool le1 = la[h] + lb[h] <= la[i] + lb[i];
+                const bool strict = la[h] < la[i] || la[h] + lb[h] < la[i] + lb[i];
                 if (le0 && le1 && (strict || h < i)) dom = true;
             }
-            if (!dom) keep.push_back(lines[i]);
+            kept[i] = dom ? 0 : 1;
         }
-        if ((int)keep.size() > MAXENV) {
+        int nk = 0;
+        for (int i = 0; i < n; ++i) nk += kept[i];
+        if (nk > MAXENV) {
             // conservative: fall back to the weakest bound (min over all lines at P)
-            double a = POS_INF, b = 0.0;
-            for (auto& l : keep) a = std::min(a, l.first);
-            keep.assign(1, {a, b});
-        }
-        S.env_n[j] = (int)keep.size();
-        // envelope is a lower bound: scale down by a hair so rounding cannot tighten it
-        for (int i = 0; i < S.env_n[j]; ++i) {
-            S.env_a[j][i] = keep[i].first * (1.0 - 1e-12);
-            S.env_b[j][i] = keep[i].second * (1.0 - 1e-12);
+            double a = POS_INF;
+            for (int i = 0; i < n; ++i)
+                if (kept[i]) a = std::min(a, la[i]);
+            S.env_n[j] = 1;
+            S.env_a[j][0] = a * (1.0 - 1e-12);
+            S.env_b[j][0] = 0.0;
+        } else {
+            // envelope is a lower bound: scale down by a hair so rounding cannot tighten it
+            int c = 0;
+            for (int i = 0; i < n; ++i)
+                if (kept[i]) {
+                    S.env_a[j][c] = la[i] * (1.0 - 1e-12);
+                    S.env_b[j][c] = lb[i] * (1.0 - 1e-12);
+                    ++c;
+                }
+            S.env_n[j] = c;
         }
         if (S.env_n[j] == 0) {
             S.env_n[j] = 1;
