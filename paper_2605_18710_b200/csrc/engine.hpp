@@ -92,6 +92,7 @@ struct Tuning {
     long long deep_after = 16384;  // steps on one piece before deeper hand-overs are allowed
     int tail_idle = 0;      // > 0: tail phase once the ramp-up is over and > 1/tail_idle walkers idle
     long long tail_after = 256;  // ... in which deeper hand-overs need only this many steps
+    int don_min_rest = 0;   // deeper (tail) hand-overs need this many options left (0: any)
     // child look-ahead (can every remaining level still place an option?): off by default —
     // the lane-parallel option screen at the next level does the same job for less
     int lookahead = 0;

@@ -97,6 +97,7 @@ struct Spec {
     long long deep_after;
     int tail_idle;                 // > 0: tail phase once idle * tail_idle > walkers (after ramp-up)
     long long tail_after;          //   ... in which deeper hand-overs need only tail_after steps
+    int don_min_rest;              // deeper hand-overs: at least this many options left (0: any)
     int lookahead;
     int donate;                    // 0: never hand work over (one walker owns the tree)
     int seq_cut;                   // MIN, models with negative coefficients: skip an option whose

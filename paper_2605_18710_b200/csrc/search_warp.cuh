@@ -514,7 +514,11 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                 const int maxl = ab == 4 ? S.don_max_level_tail : S.don_max_level;
                 while (floor_lvl < j && !level_has_rest_warp(S, w, floor_lvl)) ++floor_lvl;
                 h.note(S, 8 + (j < 7 ? j : 7));
-                if (floor_lvl < j && floor_lvl <= maxl) {
+                // deeper than the shallow limit (tail rule only): hand over a level's rest only
+                // if it still holds at least don_min_rest options (tiny pieces churn the ring)
+                const bool big_enough = floor_lvl <= S.don_max_level || S.don_min_rest <= 0 ||
+                                        (int)w.oe[floor_lvl] - (int)w.oc[floor_lvl] - 1 >= S.don_min_rest;
+                if (floor_lvl < j && floor_lvl <= maxl && big_enough) {
                     if (h.donate(w, floor_lvl, 1, -1)) {
                         ++floor_lvl;
                         h.note(S, 5);
