@@ -312,6 +312,10 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = every rank runs its own copy of the sample (independent "
+                         "planning requests, no collective); strong = the sample's stage_evals "
+                         "dealt over the ranks")
     ap.add_argument("--no-evaluator", action="store_true", help="skip the K1 evaluator leg")
     ap.add_argument("--workload", default="cfg5",
                     help="cfg5 (default, the headline); cfg1..cfg4 time only the full solve "
@@ -373,7 +377,14 @@ def main() -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t[0])
 
-    mine = deal(SAMPLE["masks"], rank, world) if headline else []
+    # weak (default): per-GPU work fixed — every rank runs the whole sample, as independent
+    # planning requests would arrive at a multi-GPU planner; strong: the 29 stage_evals dealt
+    weak = args.scaling == "weak" or world == 1
+    if headline:
+        mine = list(SAMPLE["masks"]) if weak else deal(SAMPLE["masks"], rank, world)
+    else:
+        mine = []
+    copies = world if weak else 1  # samples processed per step over all ranks
     want = {m["mask"]: float.fromhex(m["t"]) for m in mine}
 
     def run_sample(pl) -> None:
@@ -404,7 +415,7 @@ def main() -> None:
     barrier()
     ctr = pl.counters()
     t_max = max_over_ranks(sum(dev_ms))
-    value = SAMPLE_LEAVES * args.steps / (t_max / 1000.0) if t_max > 0 else 0.0
+    value = copies * SAMPLE_LEAVES * args.steps / (t_max / 1000.0) if t_max > 0 else 0.0
 
     # ---- time to the best plan: the full solve (frontier sharded over ranks) ----
     plane = None
@@ -468,7 +479,7 @@ def main() -> None:
         e2e_s += time.perf_counter() - t0
         h2d, d2h = c2["h2d_bytes"], c2["d2h_bytes"]
     e2e_s = max_over_ranks(e2e_s)
-    e2e_value = SAMPLE_LEAVES * args.steps / e2e_s if e2e_s > 0 and headline else None
+    e2e_value = copies * SAMPLE_LEAVES * args.steps / e2e_s if e2e_s > 0 and headline else None
 
     peak, peak_kind = peaks()
     evaluator = None
@@ -514,11 +525,15 @@ def main() -> None:
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / max(1, args.steps),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak" if weak else "strong", "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic", "config": dict(CONFIG if headline else {"workload": WORKLOAD},
                                             l2="flushed between steps (256 MiB write)",
-                                            parallelism=f"sample masks dealt over {world} "
-                                                        f"GPU(s); solve frontier sharded"),
+                                            parallelism=(f"every one of {world} GPU(s) runs its own "
+                                                         f"copy of the sample (no collective)"
+                                                         if weak else
+                                                         f"sample masks dealt over {world} GPU(s)")
+                                                        + "; full solve frontier sharded"),
         "same_config": headline,
         "time_to_best_plan_s": ttbp, "best_plan_iteration_time": best_plan,
         "full_solve": {"stage_eval_calls": searches_per_solve, "median_ms": ttbp * 1000.0,

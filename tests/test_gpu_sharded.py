@@ -35,8 +35,8 @@ def test_two_ranks_same_plan(workload, port):
 def test_bench_spawns_ranks_for_gpus_flag():
     # `bench.py --gpus 2` launches its own two ranks (torchrun) when not started by one; on
     # one GPU both share cuda:0 (--same-device, gloo).  The headline line must report both
-    # ranks, the cfg5 sample dealt over them (stage times checked against the reference's
-    # inside bench.py) and the sharded full solve's plan.
+    # ranks, weak scaling (each rank runs its own copy of the cfg5 sample, stage times checked
+    # against the reference's inside bench.py) and the sharded full solve's plan.
     cmd = [sys.executable, "bench.py", "--gpus", "2", "--same-device", "--dist-backend", "gloo",
            "--steps", "1", "--warmup", "3", "--no-cpu-baseline", "--no-evaluator"]
     env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
@@ -44,6 +44,7 @@ def test_bench_spawns_ranks_for_gpus_flag():
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["same_config"] is True and line["value"] > 0
+    assert line["scaling"] == "weak"
     traj = load_golden("trajectory_gpu.json")["cfg5@L32"]
     assert line["best_plan_iteration_time"] == hexf(traj["iteration_time"])
 
@@ -91,3 +92,15 @@ def test_share_all_shards_equal_unsharded(W):
     p4.set_tuning(share_all=W)
     assert p4.solve().plan.predicted_iteration_time == hexf(gold["iteration_time"])
     p4.close()
+
+
+def test_bench_strong_scaling_deals_the_sample():
+    # --scaling strong: the 29 stage_evals dealt over the ranks (fixed total work)
+    cmd = [sys.executable, "bench.py", "--gpus", "2", "--same-device", "--dist-backend", "gloo",
+           "--steps", "1", "--warmup", "3", "--no-cpu-baseline", "--no-evaluator",
+           "--scaling", "strong"]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong" and line["value"] > 0
