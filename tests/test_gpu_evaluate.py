@@ -278,3 +278,11 @@ def test_fast_path_reference_goldens():
             pl.evaluate(ent, gpus, off, st)
             assert list(st) == [hexf(r["t"]) for r in rs], (name, inst, extra)
             pl.close()
+
+
+def test_smem_peak_calibration():
+    # SURVEY §8(d)'s on-chip roofline denominator: 128 B per clock per SM on a B200 is
+    # 148 x 1.965 GHz x 128 B = 37.2 TB/s; the measured figure must be near it (not an
+    # artefact such as loads the compiler folded away, which would read ~2x)
+    bw = mosaic.smem_peak_gbs(0)
+    assert 20_000 < bw < 40_000, bw
