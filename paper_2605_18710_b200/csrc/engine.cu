@@ -565,6 +565,7 @@ void Engine::launch_chunk(std::vector<BatchReq>& reqs, size_t b0, size_t b1, con
         hs->tail_idle = tune_.tail_idle;
         hs->tail_after = tune_.tail_after;
         hs->don_min_rest = tune_.don_min_rest;
+        hs->local_don = tune_.local_handover;
         hs->lookahead = tune_.lookahead;
         // small stages: control reads every step (faster ramp-up of trees of a few hundred
         // nodes); large ones every don_period steps (the L2 round trip per step costs more)

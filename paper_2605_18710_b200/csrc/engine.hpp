@@ -93,6 +93,7 @@ struct Tuning {
     int tail_idle = 0;      // > 0: tail phase once the ramp-up is over and > 1/tail_idle walkers idle
     long long tail_after = 256;  // ... in which deeper hand-overs need only this many steps
     int don_min_rest = 0;   // deeper (tail) hand-overs need this many options left (0: any)
+    int local_handover = 1; // 1: busy walkers hand pieces to idle siblings of their CTA (smem)
     // child look-ahead (can every remaining level still place an option?): off by default —
     // the lane-parallel option screen at the next level does the same job for less
     int lookahead = 0;

@@ -98,6 +98,7 @@ struct Spec {
     int tail_idle;                 // > 0: tail phase once idle * tail_idle > walkers (after ramp-up)
     long long tail_after;          //   ... in which deeper hand-overs need only tail_after steps
     int don_min_rest;              // deeper hand-overs: at least this many options left (0: any)
+    int local_don;                 // 1: idle siblings of a CTA get pieces through shared memory
     int lookahead;
     int donate;                    // 0: never hand work over (one walker owns the tree)
     int seq_cut;                   // MIN, models with negative coefficients: skip an option whose
@@ -133,7 +134,9 @@ struct Rows {
 // level `depth`: 0 = try the options after `oc`, 1 = try the compositions after `x` of
 // option opt[depth] (within [lo, hi]).  The root is {depth 0, ph 0, oc -1}.  Items
 // are ordered by `key`, which follows the reference DFS order.
-struct alignas(16) Cont {
+// CAP blocks at `depth`: the ring's cursors hold MAXB, the CTA-local hand-off slot fewer.
+template <int CAP>
+struct alignas(16) ContT {
     unsigned long long key;
     uint16_t opt[MAXK];
     uint16_t depth, nb, ph;
@@ -141,12 +144,13 @@ struct alignas(16) Cont {
     int16_t oe;  // options at `depth` stop before oe (range split by work donation)
     int16_t pad16;
     int used;
-    uint16_t bsz[MAXB];
-    uint16_t bmk[MAXB];
-    uint16_t x[MAXB];
-    uint16_t lo[MAXB];
-    uint16_t hi[MAXB];
+    uint16_t bsz[CAP];
+    uint16_t bmk[CAP];
+    uint16_t x[CAP];
+    uint16_t lo[CAP];
+    uint16_t hi[CAP];
 };
+using Cont = ContT<MAXB>;
 
 // Position of a FIRST hit in the reference DFS order: (option, composition) per level.
 struct HitPath {

@@ -38,11 +38,27 @@ struct Ctl {
     unsigned long long dbg[16];
 };
 
+// CTA-local hand-off: one cursor slot per CTA in shared memory that a busy walker fills for
+// an idle sibling (no ring ticket, no L2 round trip, no contention with the grid).  The
+// payload is packed into 32-bit words written and read with shared-memory atomics (the flag
+// `state` orders them; atomics keep the two warps' accesses race-free by construction):
+//   hdr[0] depth | nb << 16, hdr[1] ph | oc << 16, hdr[2] oe, hdr[3] used, hdr[4..9] opt pairs;
+//   blk[b] = {bsz | bmk << 16, x | lo << 16, hi} for the LOCAL_CAP blocks at `depth`.
+// state: 0 empty, 1 being written or read, 2 full.
+constexpr int LOCAL_CAP = 32;  // blocks a local piece can carry (levels <= 5 always fit)
+struct LocalSlot {
+    int state;
+    int idle;  // siblings of this CTA waiting for work
+    unsigned hdr[10];
+    unsigned blk[LOCAL_CAP][3];
+};
+
 // Hooks of one walker (a warp).  Everything that steers control flow is decided by
 // lane 0 and broadcast, so the warp stays converged.
 struct WarpHooks {
     Ctl* ctl;
     const Spec* sp;
+    LocalSlot* ls;
     int mode;
     long long steps;
     double inc_cache;
@@ -100,6 +116,9 @@ struct WarpHooks {
             } else {
                 if (mode == MODE_FIRST && *(volatile int*)&ctl->has_hit && hit_precedes()) {
                     code = 2;
+                } else if (may_donate && sp->local_don && *(volatile int*)&ls->idle > 0 &&
+                           *(volatile int*)&ls->state == 0) {
+                    code = 5;  // a sibling of this CTA waits and the local slot is free
                 } else {
                     unsigned int idle = may_donate ? *(volatile unsigned int*)&ctl->idle : 0u;
                     if (idle) {
@@ -196,6 +215,52 @@ struct WarpHooks {
         if (lane_id() == 0) {
             __threadfence();
             atomicExch(&ready[slot], (int)(t + 1));  // ... before it is published
+        }
+        __syncwarp();
+        return true;
+    }
+    // hand "rest of level l" (ph 1) or options mid.. (ph 0) to an idle sibling through the
+    // CTA's shared-memory slot; counts in `outstanding` like a ring piece
+    __device__ bool donate_local(const Walk& wk, int l, int ph, int mid) {
+        const int nb = wk.nb[l];
+        if (nb > LOCAL_CAP) return false;  // (warp-uniform: shared-memory walk state)
+        int ok = 0;
+        const int lane = lane_id();
+        if (lane == 0 && atomicCAS(&ls->state, 0, 1) == 0) {
+            atomicAdd(&ctl->outstanding, 1ULL);
+            ok = 1;
+        }
+        ok = __shfl_sync(FULLW, ok, 0);
+        if (!ok) return false;
+        // the same cursor store_cont_warp writes: "rest of level l" (ph 1) or options
+        // mid.. (ph 0), packed
+        const int o = wk.loff[l];
+        if (lane < nb) {
+            const unsigned b0 = wk.bsz[o + lane], m0 = wk.bmk[o + lane];
+            atomicExch(&ls->blk[lane][0], b0 | m0 << 16);
+            if (ph) {
+                atomicExch(&ls->blk[lane][1], (unsigned)wk.x[o + lane] | (unsigned)wk.lo[o + lane] << 16);
+                atomicExch(&ls->blk[lane][2], (unsigned)wk.hi[o + lane]);
+            }
+        }
+        if (lane < 6) {
+            const unsigned a = 2 * lane < l ? wk.opt[2 * lane] : 0u;
+            const unsigned b = 2 * lane + 1 < l ? wk.opt[2 * lane + 1] : 0u;
+            atomicExch(&ls->hdr[4 + lane], a | b << 16);
+        } else if (lane == 6) {
+            atomicExch(&ls->hdr[0], (unsigned)l | (unsigned)nb << 16);
+        } else if (lane == 7) {
+            const int oc = ph ? (int)wk.opt[l] : mid - 1;
+            atomicExch(&ls->hdr[1], (unsigned)ph | (unsigned)(uint16_t)(int16_t)oc << 16);
+        } else if (lane == 8) {
+            atomicExch(&ls->hdr[2], (unsigned)(uint16_t)wk.oe[l]);
+        } else if (lane == 9) {
+            atomicExch(&ls->hdr[3], (unsigned)wk.used[l]);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            atomicExch(&ls->state, 2);
         }
         __syncwarp();
         return true;
@@ -343,7 +408,7 @@ constexpr size_t BLOB_STRIDE = BLOB_ROOT + blob_align(sizeof(Cont));
 
 // dynamic shared memory of one CTA for a stage of k modules over G GPUs
 static inline size_t smem_bytes(int G, int k, bool lean) {
-    return SMEM_SPEC + WPC * walk_layout(G, k, lean).bytes;
+    return SMEM_SPEC + WPC * walk_layout(G, k, lean).bytes + ((sizeof(LocalSlot) + 15) & ~size_t(15));
 }
 
 // One resident persistent grid per stage search.  Each warp is a walker: it pops a
@@ -382,6 +447,12 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
         const int* src = reinterpret_cast<const int*>(Sg);
         int* dst = reinterpret_cast<int*>(smem);
         for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+        if (threadIdx.x == 0) {
+            LocalSlot* l0 = reinterpret_cast<LocalSlot*>(
+                smem + SMEM_SPEC + WPC * walk_layout(Sg->G, Sg->k, MG_SPECIALIZE).bytes);
+            atomicExch(&l0->state, 0);
+            atomicExch(&l0->idle, 0);
+        }
         __syncthreads();
     }
     const int wid = threadIdx.x >> 5;
@@ -392,6 +463,7 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
     if (solo && ((int)blockIdx.x != map.cta_off[sid_sh] || wid != 0)) return;
     const size_t wbytes = walk_layout(S.G, S.k, MG_SPECIALIZE).bytes;
     unsigned char* wbase = smem + SMEM_SPEC + wid * wbytes;
+    LocalSlot* ls = reinterpret_cast<LocalSlot*>(smem + SMEM_SPEC + WPC * wbytes);
     Walk& w = *reinterpret_cast<Walk*>(wbase);
     if (lane == 0) walk_carve(w, wbase, S.G, S.k, MG_SPECIALIZE);
     __syncwarp();
@@ -401,6 +473,7 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
         WarpHooks h;
         h.ctl = ctl;
         h.sp = &S;
+        h.ls = ls;
         h.mode = MG_MODE(S);
         h.steps = 0;
         h.refresh = 0;
@@ -440,6 +513,12 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
             const unsigned backoff_cap = S.backoff_cap_ns;
             while (true) {
                 if (*(volatile int*)&ctl->abort) break;
+                // a sibling's piece in the CTA's slot first (shared memory, no contention)
+                if (S.local_don && *(volatile int*)&ls->state == 2 &&
+                    atomicCAS(&ls->state, 2, 1) == 2) {
+                    ticket = -2;
+                    break;
+                }
                 unsigned long long h = *(volatile unsigned long long*)&ctl->q_head;
                 unsigned long long t = *(volatile unsigned long long*)&ctl->q_tail;
                 if (h < t) {
@@ -452,12 +531,16 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
                 if (*(volatile unsigned long long*)&ctl->outstanding == 0) break;
                 if (!idle) {
                     atomicAdd(&ctl->idle, 1u);
+                    if (S.local_don) atomicAdd(&ls->idle, 1);
                     idle = true;
                 }
                 __nanosleep(backoff);
                 backoff = backoff < backoff_cap ? backoff * 2 : backoff_cap;
             }
-            if (idle) atomicSub(&ctl->idle, 1u);
+            if (idle) {
+                atomicSub(&ctl->idle, 1u);
+                if (S.local_don) atomicSub(&ls->idle, 1);
+            }
             // the root piece ships with the launch (`root`), every other piece is published
             // in the ring by its donor
             if (ticket >= 0 && ticket + 1 != ready0) {
@@ -467,14 +550,53 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
             }
         }
         ticket = __shfl_sync(FULLW, ticket, 0);
-        if (ticket < 0) break;
-        const long long slot = (long long)((unsigned long long)ticket % ctl->q_cap);
-        __threadfence();
-        const Cont& piece = ticket + 1 == ready0 ? *root : Q[slot];
-        load_cont_warp(S, R, piece, w, MG_MODE(S) == MODE_FIRST);
+        if (ticket == -1) break;
+        int d0;
+        if (ticket == -2) {
+            // the sibling's piece: unpack it from the slot (atomic reads), free the slot,
+            // then rebuild the walk from it exactly like a ring piece
+            __threadfence_block();
+            ContT<LOCAL_CAP> c;
+            const unsigned h0 = atomicOr(&ls->hdr[0], 0u), h1 = atomicOr(&ls->hdr[1], 0u);
+            c.depth = (uint16_t)(h0 & 0xffffu);
+            c.nb = (uint16_t)(h0 >> 16);
+            c.ph = (uint16_t)(h1 & 0xffffu);
+            c.oc = (int16_t)(uint16_t)(h1 >> 16);
+            c.oe = (int16_t)(uint16_t)(atomicOr(&ls->hdr[2], 0u) & 0xffffu);
+            c.used = (int)atomicOr(&ls->hdr[3], 0u);
+            c.key = 0;
+            #pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                const unsigned v = atomicOr(&ls->hdr[4 + i], 0u);
+                c.opt[2 * i] = (uint16_t)(v & 0xffffu);
+                c.opt[2 * i + 1] = (uint16_t)(v >> 16);
+            }
+            if (lane < c.nb) {
+                const unsigned a = atomicOr(&ls->blk[lane][0], 0u);
+                c.bsz[lane] = (uint16_t)(a & 0xffffu);
+                c.bmk[lane] = (uint16_t)(a >> 16);
+                if (c.ph) {
+                    const unsigned b = atomicOr(&ls->blk[lane][1], 0u);
+                    c.x[lane] = (uint16_t)(b & 0xffffu);
+                    c.lo[lane] = (uint16_t)(b >> 16);
+                    c.hi[lane] = (uint16_t)(atomicOr(&ls->blk[lane][2], 0u) & 0xffffu);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) atomicExch(&ls->state, 0);
+            d0 = c.depth;
+            load_cont_warp(S, R, c, w, MG_MODE(S) == MODE_FIRST);
+        } else {
+            const long long slot = (long long)((unsigned long long)ticket % ctl->q_cap);
+            __threadfence();
+            const Cont& piece = ticket + 1 == ready0 ? *root : Q[slot];
+            load_cont_warp(S, R, piece, w, MG_MODE(S) == MODE_FIRST);
+            d0 = piece.depth;
+        }
         WarpHooks h;
         h.ctl = ctl;
         h.sp = &S;
+        h.ls = ls;
         h.mode = MG_MODE(S);
         h.steps = 0;
         h.refresh = 0;
@@ -497,7 +619,6 @@ __global__ void __launch_bounds__(32 * WPC, MG_SPECIALIZE ? 7 : 6) MG_KSEARCH_NA
         h.abort_below = ctl->abort_below;
         h.inc_cache = POS_INF;
         h.inc_cache = h.bcast_inc();
-        const int d0 = piece.depth;
         if (S.timeline && lane == 0) w.t_start = gtimer();
         dfs_warp(S, R, w, d0, h);
         if (S.timeline && lane == 0) trace_piece(S, ctl, w.t_start, d0, h.nodes);

@@ -507,6 +507,28 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
                 h.note(S, 6);
                 return 2;
             }
+            if (ab == 5) {
+                // a sibling of this CTA is idle: hand it the shallowest rest (any level above
+                // the closed-form last one) through the CTA's shared-memory slot
+                h.note(S, 7);
+                while (floor_lvl < j && !level_has_rest_warp(S, w, floor_lvl)) ++floor_lvl;
+                if (floor_lvl < j && floor_lvl <= k - 2) {
+                    if (h.donate_local(w, floor_lvl, 1, -1)) {
+                        ++floor_lvl;
+                        h.note(S, 5);
+                    }
+                } else if (floor_lvl == j && j <= k - 2) {
+                    const int a = w.oc[j] + 1, e = w.oe[j];
+                    if (e - a >= 2) {
+                        const int mid = a + (e - a) / 2;
+                        if (h.donate_local(w, j, 0, mid)) {
+                            if (lane == 0) w.oe[j] = (int16_t)mid;
+                            h.note(S, 5);
+                        }
+                        __syncwarp();
+                    }
+                }
+            }
             if (ab == 3 || ab == 4) {
                 h.note(S, 7);
                 // only shallow work is worth a hand-over (cursor traffic beats tiny
@@ -941,7 +963,8 @@ __device__ int dfs_warp(const Spec& S, const Rows& R, Walk& w, int d0, H& h) {
 }
 
 // ---- cursor load / store by a whole warp ----
-__device__ __forceinline__ void load_cont_warp(const Spec& S, const Rows& R, const Cont& c, Walk& w,
+template <class C>
+__device__ __forceinline__ void load_cont_warp(const Spec& S, const Rows& R, const C& c, Walk& w,
                                                bool ancestors = true) {
     const int lane = lane_id();
     const int dep = c.depth;
@@ -995,7 +1018,8 @@ __device__ __forceinline__ void load_cont_warp(const Spec& S, const Rows& R, con
 
 // Cursor for the rest of level l: ph 1 = compositions after the current x of opt[l], then
 // the options after it up to oe[l]; ph 0 = options oc_from+1 .. oe[l]-1 (range split).
-__device__ __forceinline__ void store_cont_warp(const Walk& w, int l, int ph, Cont& c,
+template <class C>
+__device__ __forceinline__ void store_cont_warp(const Walk& w, int l, int ph, C& c,
                                                 int oc_from = -1) {
     const int lane = lane_id();
     const int o = w.loff[l];
