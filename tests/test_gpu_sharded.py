@@ -104,3 +104,18 @@ def test_bench_strong_scaling_deals_the_sample():
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["scaling"] == "strong" and line["value"] > 0
+
+
+def test_local_handover_on_off_identical():
+    # CTA-local hand-off of search pieces (shared-memory slot) on and off: identical results
+    mosaic = pytest.importorskip("paper_2605_18710_b200.mosaic")
+    pl = mosaic.Planner.from_spec("cfg5", device=0)
+    masks = [[0, 1, 2, 3], [0, 2, 3, 4], [0, 1, 2, 3, 4]]
+    res = {}
+    for lh in (1, 0):
+        pl.set_tuning(local_handover=lh)
+        pl.clear_cache()
+        res[lh] = ([_sig(pl.stage_eval(m)) for m in masks],
+                   [_sig(pl.exact_stage(m)) for m in masks[:2]])
+    assert res[0] == res[1]
+    pl.close()
