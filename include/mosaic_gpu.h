@@ -315,7 +315,9 @@ int mosaic_gpu_merge_ranks(const void* records, int world, int mode, int k, int*
  * lookahead, generic_kernel, shard_level, ring_per_walker, trace (1: one line per device search,
  * 2: per launch, 3: as 1 plus walker occupancy, a busy-walker timeline, hand-over outcomes and
  * a log of long pieces of each launch's first search), spec_k (GAHC candidates up to this many modules are batched),
- * fuse_k / fuse_tree (stage_evals of at most fuse_k modules, or of at most fuse_tree option
+ * min_order (level order of MIN proofs: 4 = largest minimal solo latency first, default; 0 =
+ * fewest viable options first; any order gives the same T*), min_perm (measurement only),
+ * local_handover, fuse_k / fuse_tree (stage_evals of at most fuse_k modules, or of at most fuse_tree option
  * tuples x GPUs, run their MIN proof in the first probe's launch), restart_k (MIN proofs of stages with at least this many modules restart on a big drop), and the measurement-only share_rank / share_world (search one
  * rank's share of a sharded search on this device, unmerged: NOT the stage's answer), share_all
  * (> 1: every large search runs as that many option-prefix shards in one launch on this device

@@ -500,6 +500,8 @@ int mosaic_gpu_set_tuning(mosaic_gpu_ctx* ctx, const char* key, double value) {
         else if (k == "tail_after") t.tail_after = (long long)v;
         else if (k == "don_min_rest") t.don_min_rest = (int)v;
         else if (k == "local_handover") t.local_handover = (int)v;
+        else if (k == "min_order") t.min_order = (int)v;
+        else if (k == "min_perm") t.min_perm = (long long)v;
         else if (k == "fuse_k") t.fuse_k = (int)v;
         else if (k == "don_period_small") {
             if (v < 1 || ((long long)v & ((long long)v - 1))) throw Error(MOSAIC_INVALID_ARGUMENT, "don_period_small must be a power of two");

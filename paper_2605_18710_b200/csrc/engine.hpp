@@ -94,6 +94,10 @@ struct Tuning {
     long long tail_after = 256;  // ... in which deeper hand-overs need only this many steps
     int don_min_rest = 0;   // deeper (tail) hand-overs need this many options left (0: any)
     int local_handover = 1; // 1: busy walkers hand pieces to idle siblings of their CTA (smem)
+    int min_order = 4;      // MIN proof level order: 0 fewest viable options first, 1 most,
+                            // 2 / 3 largest / smallest minimal base latency first, 4 largest
+                            // minimal solo latency, 5 largest minimal footprint, 6 0 + 2 ties
+    long long min_perm = 0; // measurement: > 0 = that permutation of the modules (1-based)
     // child look-ahead (can every remaining level still place an option?): off by default —
     // the lane-parallel option screen at the next level does the same job for less
     int lookahead = 0;

@@ -277,15 +277,51 @@ bool Planner::prep_min(const std::vector<int>& mods, double ub, SearchOp& op, mg
                        std::vector<int>& order) {
     const double thp = ub >= POS_INF ? POS_INF : ub * (1.0 - mg::TIE_EPS);
     std::vector<std::pair<int, int>> cnt;
+    const int mo = eng_->tuning().min_order;
     for (int m : mods) {
         // lb = (base + e1) + e2 B is exactly the row's filter bound with non-negative
         // coefficients: count rows with bound <= thp in the bound-sorted index
         const auto& b = M_.index[m].bound;
         const int c = M_.nonneg() ? (int)(std::upper_bound(b.begin(), b.end(), thp) - b.begin())
                                   : (int)M_.rows[m].size();
-        cnt.push_back({c, m});
+        // any level order gives the same T*; the order only changes the tree's size
+        int key = c;
+        if (mo == 1) key = -c;  // most viable options first
+        else if (mo == 2 || mo == 3) {
+            // by the module's smallest base latency (rows are sorted by it), largest / smallest first
+            const double mb = M_.rows[m].empty() ? 0.0 : M_.rows[m][0].base;
+            const int q = (int)std::min(2.0e9, mb * 1e8);
+            key = mo == 2 ? -q : q;
+        } else if (mo == 4) {
+            // largest minimal solo rectified latency first
+            key = -(int)std::min(2.0e9, tau_mins_[m].second * 1e8);
+        } else if (mo == 5) {
+            // largest minimal per-GPU footprint first
+            double fp = 1e300;
+            for (const auto& r : M_.rows[m]) fp = std::min(fp, r.fp);
+            key = -(int)std::min(2.0e9, fp * 1e-3);
+        } else if (mo == 6) {
+            // fewest viable options first, ties: largest minimal base latency first
+            const double mb = M_.rows[m].empty() ? 0.0 : M_.rows[m][0].base;
+            key = c * 4096 - (int)std::min(4095.0, mb * 100.0);
+        }
+        cnt.push_back({key, m});
     }
     std::stable_sort(cnt.begin(), cnt.end());
+    if (eng_->tuning().min_perm > 0) {
+        // measurement: the min_perm-th permutation (lexicographic, 1-based) of the modules
+        std::vector<int> ms(mods);
+        std::sort(ms.begin(), ms.end());
+        long long r = eng_->tuning().min_perm - 1;
+        for (size_t i = 0; i < ms.size() && r > 0; ++i) {
+            long long f = 1;
+            for (size_t t = 1; t < ms.size() - i; ++t) f *= (long long)t;
+            const long long idx = r / f;
+            r %= f;
+            std::rotate(ms.begin() + i, ms.begin() + i + idx, ms.begin() + i + idx + 1);
+        }
+        for (size_t i = 0; i < ms.size(); ++i) cnt[i] = {0, ms[i]};
+    }
     mg::SearchReq q;
     q.mode = MODE_MIN;
     q.ub = ub;
@@ -685,13 +721,11 @@ double Planner::stage_min(uint64_t mask, double ub, bool restart, mg::SearchStat
     if ((int)mods.size() > mg::MAXK) throw Error(TOO_LARGE, "stage larger than 12 modules");
     for (int m : mods) check_rows(m);
     if (restart) return min_value(mods, ub, st);
-    mg::SearchReq q;
-    q.mode = MODE_MIN;
-    q.ub = ub;
-    q.level_module = mods;
-    mg::Spec S;
-    if (!mg::build_spec(M_, q, S)) return ub;
-    mg::SearchResult r = eng_->search(S, ub, 0.0, st);
+    // one MIN search in the level order stage_eval's proofs use (prep_min)
+    SearchOp op;
+    std::vector<int> morder;
+    if (!prep_min(mods, ub, op, st, morder)) return ub;
+    mg::SearchResult r = eng_->search(op.req.S, ub, 0.0, st);
     if (r.overflow) throw Error(TOO_LARGE, "stage needs more than 128 GPU blocks");
     return r.value;
 }

@@ -12,7 +12,7 @@ pl = mosaic.Planner.from_spec("cfg5", device=0)
 pl.stage_eval([0, 1, 2])
 base = None
 DEFAULTS = {"don_depth": 3, "don_tail": 2, "deep_after": 16384, "don_period": 4,
-            "backoff_ns": 2048, "don_depth_first": -1, "don_tail_first": -1, "tail_idle": 0, "tail_after": 256, "don_min_rest": 0, "local_handover": 1}
+            "backoff_ns": 2048, "don_depth_first": -1, "don_tail_first": -1, "tail_idle": 0, "tail_after": 256, "don_min_rest": 0, "local_handover": 1, "min_order": 4}
 for setting in sys.argv[1:]:
     kv = dict(x.split("=") for x in setting.split())
     for k, v in {**DEFAULTS, **kv}.items():
