@@ -274,10 +274,10 @@ def evaluator_leg(pl, torch, dev, steps: int, warmup: int, peak: float, peak_kin
 
 
 TRAFFIC_CSV = "profiles/r2_dram_sample.csv"
-# `ncu --set full` of the dominant launch (cfg5 7-encoder MIN proof, 408.9 ms):
+# `ncu --set full` of the dominant launch (cfg5 7-encoder MIN proof, 363.2 ms):
 # profiles/r2_ncu_ksearch_min_cfg5_k7.ncu-rep
-NCU_MIN7 = {"smem_wavefronts_frac_of_peak": 0.355, "lsu_pipe_frac": 0.375,
-            "issue_active_frac": 0.437, "fp64_pipe_frac": 0.070,
+NCU_MIN7 = {"smem_wavefronts_frac_of_peak": 0.441, "lsu_pipe_frac": 0.435,
+            "issue_active_frac": 0.490, "fp64_pipe_frac": 0.081,
             "source": "profiles/r2_ncu_ksearch_min7.md"}
 
 
